@@ -1,0 +1,156 @@
+/*
+ * bcgpu -- B200-native (sm_100a) moment / cumulant engine, C ABI.
+ *
+ * Drop-in boundary for the reference package `blockcumulants`
+ * (/root/reference/pkg/src/blockcumulants, cited as bc/<file>:<line>).  The
+ * reference's only native boundary is the Cython module `_core`
+ * (bc/_core.pyx:126-175, imported at bc/_engines.py:26-31); everything the
+ * Python layer above it needs on the hot path -- centering, packed moments,
+ * the cumulant recursion -- is exported here with plain pointers and sizes.
+ *
+ * Conventions
+ *  - Every device pointer is caller-owned device memory (torch allocations in
+ *    the Python host layer).  Plans own only their small index tables.
+ *  - Every call is stream-ordered on `stream` (a cudaStream_t, passed as void*;
+ *    NULL = legacy default stream) and returns a status code; on failure
+ *    bcg_last_error() describes it (thread-local).
+ *  - Status codes map to the reference's error convention (bc/errors.py:4-9):
+ *    BCG_EINVAL -> ValidationError, BCG_ENOMEM -> MemoryError,
+ *    BCG_ECUDA -> RuntimeError.
+ *  - Packed tensors use the reference's flat layout exactly: block k (k-th
+ *    sorted key in lexicographic order, bc/symtensor.py:47-49) occupies
+ *    [offs[k], offs[k+1]) row-major over its edges (bc/_engines.py:46-61).
+ *  - All values are float64, all index tables int64 (C `long` on Linux, as the
+ *    reference's memoryviews require, bc/_core.pyx:126-128).
+ */
+#ifndef BCGPU_H
+#define BCGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BCG_OK 0
+#define BCG_EINVAL 1
+#define BCG_ECUDA 2
+#define BCG_ENOMEM 3
+
+/* Last error message of the calling thread ("" if none). */
+const char *bcg_last_error(void);
+/* ABI version (major*100 + minor). */
+int bcg_version(void);
+/* Number of kernel launches this library has issued in this process
+ * (evidence counter for bench.py's `gpu_launches`). */
+int64_t bcg_launch_count(void);
+
+/* ---------------------------------------------------------------------------
+ * Drop-in replacement for `_core.moment_blocks` (bc/_core.pyx:126-148).
+ * Same arguments and semantics, on DEVICE pointers:
+ *   out[offs[k] + rowmajor(o)] += sum_l prod_q xt[(col0[k,q] + o_q) * t + l]
+ * for blocks k in [k0, k1); raw product sums ACCUMULATED (no 1/t, caller
+ * zero-fills and scales, bc/_engines.py:92-100).  xt is (n, t) row-major as the
+ * reference passes it (bc/_engines.py:95); col0/edges are (K, m) int64, offs is
+ * (K+1) int64.  Errors as the reference: m outside [2, 16] -> BCG_EINVAL
+ * ("kernel supports 2 <= m <= 16", bc/_core.pyx:138-139).  Deterministic:
+ * repeated calls produce bitwise-identical sums.  The layout passed in must
+ * be the reference's (_block_layout of some (n, m, b)); it is checked.
+ * ------------------------------------------------------------------------- */
+int bcg_moment_blocks(const double *xt, int64_t n, int64_t t,
+                      const int64_t *col0, const int64_t *edges, int64_t m,
+                      int64_t K, double *out, const int64_t *offs, int64_t k0,
+                      int64_t k1, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Plans: host-built (C++) index tables for one (n, m, b), uploaded once.
+ * A plan for order m serves the order-m moment GEMM (bc/_engines.py:83-100)
+ * and the order-m cumulant recursion (bc/cumulants.py:53-136).
+ * ------------------------------------------------------------------------- */
+typedef struct bcg_plan bcg_plan;
+
+int bcg_plan_create(int64_t n, int32_t m, int32_t b, bcg_plan **plan);
+/* Host-only plan (tables built, nothing uploaded): layout queries work
+ * without a GPU; compute calls on it fail with BCG_EINVAL. */
+int bcg_plan_create_host(int64_t n, int32_t m, int32_t b, bcg_plan **plan);
+int bcg_plan_destroy(bcg_plan *plan);
+/* Host-side verification of the moment GEMM mapping: every stored element of
+ * order m is produced by exactly one (tile, row, col) and reads exactly the
+ * data columns of its (key, offsets).  BCG_OK or BCG_EINVAL with a message. */
+int bcg_plan_selfcheck(const bcg_plan *plan);
+/* K = number of stored blocks, S = stored elements (offs[K]) of order `order`
+ * (1 <= order <= m). */
+int bcg_plan_sizes(const bcg_plan *plan, int32_t order, int64_t *K, int64_t *S);
+/* Copy the reference layout of order `order` (keys 1-based, col0, edges: K x
+ * order; offs: K+1) into caller HOST buffers (bc/_engines.py:46-54). */
+int bcg_plan_layout(const bcg_plan *plan, int32_t order, int64_t *keys,
+                    int64_t *col0, int64_t *edges, int64_t *offs);
+/* Workspace bytes bcg_moment_raw needs for t samples (0 = none). */
+int bcg_moment_ws_bytes(const bcg_plan *plan, int64_t t, size_t *bytes);
+
+/* ---------------------------------------------------------------------------
+ * Column statistics of x (t x n row-major, leading dimension ldx >= n):
+ * sums[n] (if non-NULL) = sum_l x[l, c]; mean[n] (if non-NULL) = sums / t
+ * (bc/moments.py:41); sumsq[n] (if non-NULL) = sum_l x[l, c]^2;
+ * first_bad (if non-NULL, device int64) = smallest row-major linear index of a
+ * non-finite element or -1 -- the reference's isfinite scan and its "row r,
+ * column c" diagnostic (bc/moments.py:23-35).  Deterministic reduction order.
+ * ------------------------------------------------------------------------- */
+int bcg_colstats(const double *x, int64_t t, int64_t n, int64_t ldx,
+                 double *sums, double *mean, double *sumsq, int64_t *first_bad,
+                 void *stream);
+
+/* xc[l, c] = x[l, c] - mean[c]   (bc/moments.py:38-41). */
+int bcg_center(const double *x, int64_t t, int64_t n, int64_t ldx,
+               const double *mean, double *xc, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Order-m packed RAW moment sums of x (t x n row-major, ldx >= n), ACCUMULATED
+ * into out[S_m] (same semantics as bcg_moment_blocks over all blocks).  The
+ * Khatri-Rao-staged FP64 DMMA GEMM.  `ws` must hold
+ * bcg_moment_ws_bytes(plan, t) bytes (may be NULL when that is 0).
+ * ------------------------------------------------------------------------- */
+int bcg_moment_raw(const bcg_plan *plan, const double *x, int64_t t,
+                   int64_t ldx, double *out, void *ws, size_t ws_bytes,
+                   void *stream);
+/* Same, restricted to blocks [k0, k1) (only out[offs[k0]:offs[k1]] is
+ * touched; bitwise identical to the full call on those blocks) -- the
+ * block-split path of moment_parallel_blocks (bc/moments.py:99-131). */
+int bcg_moment_raw_range(const bcg_plan *plan, const double *x, int64_t t,
+                         int64_t ldx, double *out, void *ws, size_t ws_bytes,
+                         int64_t k0, int64_t k1, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Cumulant recursion, in place: on entry mk holds the order-m central moment
+ * M_m (packed, order of `plan`), on exit C_m = (M_m - B_2) - B_3 - ... with
+ *   B_sigma[key][o] = sum over min-2 partitions zeta of (1..m) into sigma
+ *                     parts (bc/partitions.py:63-98 order) of
+ *                     prod_{part} C_|part|[key|part][o|part]
+ * (bc/cumulants.py:53-84, 119-136).  lower[j] = packed C_{j+2} (device), for
+ * j = 0 .. m-4.  m <= 3 is a no-op (the cumulant is the moment).
+ * ------------------------------------------------------------------------- */
+int bcg_cumulant_recursion(const bcg_plan *plan, double *mk,
+                           const double *const *lower, void *stream);
+
+/* Same correction without the moment: out = B_sigma (bc/cumulants.py:53-84,
+ * `outer_prod_cum(m, sigma, lower)`), out has S_m elements. */
+int bcg_outer_prod_cum(const bcg_plan *plan, int32_t sigma,
+                       const double *const *lower, double *out, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Packed-buffer elementwise ops (BlockSymTensor `+ - scale`,
+ * bc/symtensor.py:185-200; the weighted reduction of moment_parallel,
+ * bc/moments.py:93-95):  out[i] = a * x[i] + c * y[i]  (y may be NULL -> c
+ * ignored).  out may alias x or y.
+ * ------------------------------------------------------------------------- */
+int bcg_axpby(int64_t len, double a, const double *x, double c,
+              const double *y, double *out, void *stream);
+/* out[i] = x[i] / d  (the reference's `out /= t`, bc/_engines.py:99). */
+int bcg_div(int64_t len, const double *x, double d, double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BCGPU_H */

@@ -1,0 +1,167 @@
+"""ctypes binding of libbcgpu.so (include/bcgpu.h) -- the C-ABI boundary.
+
+This is the only door to compute: there is no CPU fallback.  If the library
+or a CUDA device is missing, the call raises NativeUnavailableError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from functools import lru_cache
+
+import numpy as np
+
+from .errors import NativeUnavailableError, ValidationError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbcgpu.so")
+
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_dbl = ctypes.c_double
+_vp = ctypes.c_void_p
+_sz = ctypes.c_size_t
+
+# (name, restype, argtypes) -- every symbol include/bcgpu.h declares
+SIGNATURES = [
+    ("bcg_last_error", ctypes.c_char_p, []),
+    ("bcg_version", ctypes.c_int, []),
+    ("bcg_launch_count", _i64, []),
+    ("bcg_moment_blocks", ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp]),
+    ("bcg_plan_create", ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(_vp)]),
+    ("bcg_plan_create_host", ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(_vp)]),
+    ("bcg_plan_destroy", ctypes.c_int, [_vp]),
+    ("bcg_plan_selfcheck", ctypes.c_int, [_vp]),
+    ("bcg_plan_sizes", ctypes.c_int, [_vp, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    ("bcg_plan_layout", ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp]),
+    ("bcg_moment_ws_bytes", ctypes.c_int, [_vp, _i64, ctypes.POINTER(_sz)]),
+    ("bcg_colstats", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
+    ("bcg_center", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    ("bcg_moment_raw", ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
+    ("bcg_moment_raw_range", ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _sz, _i64, _i64, _vp]),
+    ("bcg_cumulant_recursion", ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    ("bcg_outer_prod_cum", ctypes.c_int, [_vp, _i32, _vp, _vp, _vp]),
+    ("bcg_axpby", ctypes.c_int, [_i64, _dbl, _vp, _dbl, _vp, _vp, _vp]),
+    ("bcg_div", ctypes.c_int, [_i64, _vp, _dbl, _vp, _vp]),
+]
+
+_lock = threading.Lock()
+
+
+@lru_cache(maxsize=1)
+def lib() -> ctypes.CDLL:
+    """Load libbcgpu.so (building it in-tree first if nvcc is available)."""
+    if not os.path.exists(LIB_PATH):
+        try:
+            from . import _build
+
+            _build.build()
+        except Exception as exc:  # pragma: no cover - depends on toolchain
+            raise NativeUnavailableError(f"libbcgpu.so is not built ({exc})") from exc
+    try:
+        handle = ctypes.CDLL(LIB_PATH)
+    except OSError as exc:
+        raise NativeUnavailableError(f"cannot load {LIB_PATH}: {exc}") from exc
+    for name, res, args in SIGNATURES:
+        fn = getattr(handle, name)
+        fn.restype = res
+        fn.argtypes = args
+    return handle
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == 0:
+        return
+    msg = lib().bcg_last_error().decode(errors="replace")
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == 1:
+        raise ValidationError(msg)
+    if rc == 3:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def torch_cuda():
+    """torch with a usable CUDA device, or NativeUnavailableError."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeUnavailableError(
+            "a CUDA device is required: this framework has no CPU fallback"
+        )
+    return torch
+
+
+def stream_handle() -> int:
+    torch = torch_cuda()
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(tensor) -> int:
+    return tensor.data_ptr()
+
+
+class Plan:
+    """Host-built index tables for one (n, m, b) (bcg_plan_create)."""
+
+    def __init__(self, n: int, m: int, b: int, host_only: bool = False):
+        self.n, self.m, self.b = int(n), int(m), int(b)
+        self.host_only = host_only
+        h = _vp()
+        fn = lib().bcg_plan_create_host if host_only else lib().bcg_plan_create
+        check(fn(self.n, self.m, self.b, ctypes.byref(h)), "plan")
+        self._h = h
+        self._lib = lib()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def sizes(self, order: int):
+        k, s = _i64(), _i64()
+        check(self._lib.bcg_plan_sizes(self._h, order, ctypes.byref(k), ctypes.byref(s)))
+        return k.value, s.value
+
+    def layout(self, order: int):
+        """(keys, col0, edges, offs) as int64 arrays (bc/_engines.py:46-54)."""
+        K, _ = self.sizes(order)
+        keys = np.empty((K, order), dtype=np.int64)
+        col0 = np.empty((K, order), dtype=np.int64)
+        edges = np.empty((K, order), dtype=np.int64)
+        offs = np.empty(K + 1, dtype=np.int64)
+        check(self._lib.bcg_plan_layout(self._h, order, keys.ctypes.data, col0.ctypes.data,
+                                        edges.ctypes.data, offs.ctypes.data))
+        return keys, col0, edges, offs
+
+    def ws_bytes(self, t: int) -> int:
+        out = _sz()
+        check(self._lib.bcg_moment_ws_bytes(self._h, int(t), ctypes.byref(out)))
+        return out.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._lib.bcg_plan_destroy(h)
+            except Exception:
+                pass
+
+
+_plans: dict = {}
+
+
+def plan(n: int, m: int, b: int) -> Plan:
+    """Cached device plan for (n, m, b)."""
+    key = (int(n), int(m), int(b))
+    with _lock:
+        p = _plans.get(key)
+        if p is None:
+            torch_cuda()
+            p = _plans[key] = Plan(*key)
+        return p
+
+
+def launch_count() -> int:
+    return int(lib().bcg_launch_count())

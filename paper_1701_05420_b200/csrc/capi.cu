@@ -1,0 +1,394 @@
+// extern "C" boundary (include/bcgpu.h).  Validation mirrors the reference's
+// errors; every launch is stream-ordered on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/bcgpu.h"
+#include "kernels.h"
+#include "plan.h"
+
+struct bcg_plan {
+  bcg::Plan p;
+};
+
+namespace bcg {
+int64_t g_launches = 0;
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+  return fail(BCG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(expr, what)                    \
+  do {                                          \
+    cudaError_t _e = (expr);                    \
+    if (_e != cudaSuccess) return cuda_fail(_e, what); \
+  } while (0)
+
+// Split-K decision shared by bcg_moment_ws_bytes and bcg_moment_raw.
+struct Slicing {
+  int KC;
+  int nslices;
+  int64_t slice_len;
+};
+
+Slicing choose_slicing(const bcg::Plan &p, int64_t t) {
+  Slicing s{bcg::pick_kc((int)p.n), 1, t};
+  if (s.KC == 0 || t <= 0) return s;
+  const int64_t ntiles = (int64_t)p.tiles.size();
+  const size_t smem = bcg::moment_smem_bytes(s.KC, (int)p.n);
+  int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / (int64_t)(smem + 1024)));
+  const int64_t concurrent = 148 * per_sm;
+  const int64_t target_units = 8 * concurrent;  // >= 8 waves keeps the tail small
+  int64_t ns = (target_units + ntiles - 1) / ntiles;
+  ns = std::min<int64_t>(ns, std::max<int64_t>(1, t / 1024));
+  const int64_t S = p.lay[p.m].offs.back();
+  const int64_t ws_cap = (int64_t)1 << 30;  // 1 GiB of split-K partials at most
+  if (ns > 1) ns = std::max<int64_t>(1, std::min<int64_t>(ns, ws_cap / (S * 8)));
+  int64_t len = (t + ns - 1) / ns;
+  len = (len + s.KC - 1) / s.KC * s.KC;
+  ns = (t + len - 1) / len;
+  s.nslices = (int)ns;
+  s.slice_len = len;
+  return s;
+}
+
+size_t ws_bytes_for(const bcg::Plan &p, const Slicing &s) {
+  return s.nslices > 1 ? (size_t)s.nslices * (size_t)p.lay[p.m].offs.back() * sizeof(double) : 0;
+}
+
+int run_moment(const bcg::Plan &p, const double *x, int64_t t, int64_t ldx, double *out, void *ws,
+               size_t ws_bytes, int64_t k0, int64_t k1, cudaStream_t stream) {
+  if (t <= 0) return BCG_OK;
+  const Slicing sl = choose_slicing(p, t);
+  if (sl.KC == 0) return fail(BCG_EINVAL, "too many columns for the moment kernel's shared-memory stage");
+  const size_t need = ws_bytes_for(p, sl);
+  if (need > ws_bytes || (need && !ws))
+    return fail(BCG_EINVAL, "workspace too small: need " + std::to_string(need) + " bytes");
+  bcg::MomentArgs a{};
+  a.x = x;
+  a.t = t;
+  a.ldx = ldx;
+  a.n = (int)p.n;
+  a.h = p.h;
+  a.r = p.r;
+  a.bulk_ok = (ldx == p.n) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && ((sl.KC * p.n * 8) % 16 == 0);
+  a.rowcols = p.d_rowcols;
+  a.colcols = p.d_colcols;
+  a.row_keybase = p.d_row_keybase;
+  a.row_olin = p.d_row_olin;
+  a.row_cstart = p.d_row_cstart;
+  a.col_rank = p.d_col_rank;
+  a.col_olin = p.d_col_olin;
+  a.col_size = p.d_col_size;
+  a.offs = p.d_offs;
+  a.tiles = p.d_tiles;
+  a.tile_kmin = p.d_tile_kmin;
+  a.tile_kmax = p.d_tile_kmax;
+  a.ntiles = (int)p.tiles.size();
+  a.R = p.R;
+  a.C = p.C;
+  a.nslices = sl.nslices;
+  a.slice_len = sl.slice_len;
+  a.out = out;
+  a.ws = static_cast<double *>(ws);
+  a.S = p.lay[p.m].offs.back();
+  a.kmin_sel = (int32_t)k0;
+  a.kmax_sel = k1 - 1 >= INT32_MAX ? INT32_MAX : (int32_t)(k1 - 1);
+  if (k0 == 0 && k1 >= p.lay[p.m].K) a.kmax_sel = INT32_MAX;
+  const int64_t grid = (int64_t)a.ntiles * sl.nslices;
+  if (grid > INT32_MAX) return fail(BCG_EINVAL, "moment grid too large");
+  CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream), "moment kernel");
+  bcg::g_launches++;
+  if (sl.nslices > 1) {
+    const auto &offs = p.lay[p.m].offs;
+    CUDA_TRY(bcg::launch_reduce_slices(a.ws, sl.nslices, a.S, offs[k0], offs[k1], out, stream), "split-K reduce");
+    bcg::g_launches++;
+  }
+  return BCG_OK;
+}
+
+std::mutex g_cache_mu;
+std::map<std::tuple<int64_t, int, int>, std::unique_ptr<bcg_plan>> g_cache;
+
+}  // namespace
+
+extern "C" {
+
+const char *bcg_last_error(void) { return g_err.c_str(); }
+int bcg_version(void) { return 100; }
+int64_t bcg_launch_count(void) { return bcg::g_launches; }
+
+int bcg_plan_create(int64_t n, int32_t m, int32_t b, bcg_plan **plan) {
+  if (!plan) return fail(BCG_EINVAL, "plan pointer is NULL");
+  auto pl = std::make_unique<bcg_plan>();
+  std::string err = bcg::build_plan(n, m, b, pl->p);
+  if (!err.empty()) return fail(BCG_EINVAL, err);
+  err = bcg::upload_plan(pl->p);
+  if (!err.empty()) {
+    bcg::free_plan(pl->p);
+    return fail(BCG_ECUDA, err);
+  }
+  *plan = pl.release();
+  return BCG_OK;
+}
+
+int bcg_plan_create_host(int64_t n, int32_t m, int32_t b, bcg_plan **plan) {
+  if (!plan) return fail(BCG_EINVAL, "plan pointer is NULL");
+  auto pl = std::make_unique<bcg_plan>();
+  std::string err = bcg::build_plan(n, m, b, pl->p);
+  if (!err.empty()) return fail(BCG_EINVAL, err);
+  *plan = pl.release();
+  return BCG_OK;
+}
+
+int bcg_plan_selfcheck(const bcg_plan *plan) {
+  if (!plan) return fail(BCG_EINVAL, "plan is NULL");
+  const bcg::Plan &p = plan->p;
+  if (p.m < 2) return BCG_OK;
+  const bcg::Layout &L = p.lay[p.m];
+  const int64_t S = L.offs.back();
+  std::vector<uint8_t> seen(S, 0);
+  for (const bcg::Tile &tl : p.tiles) {
+    for (int64_t r = tl.row0; r < std::min<int64_t>(tl.row0 + bcg::kTM, p.R); ++r) {
+      for (int64_t c = tl.col0; c < std::min<int64_t>(tl.col0 + bcg::kTN, p.C); ++c) {
+        if (c < p.row_cstart[r]) continue;
+        const int64_t k = p.row_keybase[r] + p.col_rank[c];
+        if (k < 0 || k >= L.K) return fail(BCG_EINVAL, "selfcheck: key index out of range");
+        const int64_t lin = (int64_t)p.row_olin[r] * p.col_size[c] + p.col_olin[c];
+        const int64_t addr = L.offs[k] + lin;
+        if (addr >= L.offs[k + 1]) return fail(BCG_EINVAL, "selfcheck: offset outside block");
+        if (seen[addr]) return fail(BCG_EINVAL, "selfcheck: element produced twice");
+        seen[addr] = 1;
+        // the element's data columns must be those of (key, offsets)
+        int64_t rem = lin, cols[16];
+        for (int q = p.m - 1; q >= 0; --q) {
+          const int64_t e = L.edges[k * p.m + q];
+          cols[q] = L.col0[k * p.m + q] + rem % e;
+          rem /= e;
+        }
+        for (int q = 0; q < p.h; ++q)
+          if (p.rowcols[r * p.h + q] != cols[q]) return fail(BCG_EINVAL, "selfcheck: row column mismatch");
+        for (int q = 0; q < p.r; ++q)
+          if (p.colcols[c * p.r + q] != cols[p.h + q]) return fail(BCG_EINVAL, "selfcheck: col column mismatch");
+      }
+    }
+  }
+  for (int64_t i = 0; i < S; ++i)
+    if (!seen[i]) return fail(BCG_EINVAL, "selfcheck: element never produced");
+  return BCG_OK;
+}
+
+int bcg_plan_destroy(bcg_plan *plan) {
+  if (!plan) return BCG_OK;
+  bcg::free_plan(plan->p);
+  delete plan;
+  return BCG_OK;
+}
+
+int bcg_plan_sizes(const bcg_plan *plan, int32_t order, int64_t *K, int64_t *S) {
+  if (!plan || order < 1 || order > plan->p.m) return fail(BCG_EINVAL, "order outside 1..m of the plan");
+  const auto &L = plan->p.lay[order];
+  if (K) *K = L.K;
+  if (S) *S = L.offs.back();
+  return BCG_OK;
+}
+
+int bcg_plan_layout(const bcg_plan *plan, int32_t order, int64_t *keys, int64_t *col0, int64_t *edges,
+                    int64_t *offs) {
+  if (!plan || order < 1 || order > plan->p.m) return fail(BCG_EINVAL, "order outside 1..m of the plan");
+  const auto &L = plan->p.lay[order];
+  if (keys) std::memcpy(keys, L.keys.data(), L.keys.size() * 8);
+  if (col0) std::memcpy(col0, L.col0.data(), L.col0.size() * 8);
+  if (edges) std::memcpy(edges, L.edges.data(), L.edges.size() * 8);
+  if (offs) std::memcpy(offs, L.offs.data(), L.offs.size() * 8);
+  return BCG_OK;
+}
+
+int bcg_moment_ws_bytes(const bcg_plan *plan, int64_t t, size_t *bytes) {
+  if (!plan || !bytes) return fail(BCG_EINVAL, "NULL argument");
+  if (plan->p.m < 2) {
+    *bytes = 0;
+    return BCG_OK;
+  }
+  *bytes = ws_bytes_for(plan->p, choose_slicing(plan->p, t));
+  return BCG_OK;
+}
+
+int bcg_colstats(const double *x, int64_t t, int64_t n, int64_t ldx, double *sums, double *mean, double *sumsq,
+                 int64_t *first_bad, void *stream) {
+  if (t < 1 || n < 1 || ldx < n) return fail(BCG_EINVAL, "data must be non-empty with ldx >= n");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int parts = bcg::colstats_parts(t, n);
+  double *scratch = nullptr;
+  CUDA_TRY(cudaMallocAsync(&scratch, (2 * (size_t)parts * n + 1) * sizeof(double), s), "colstats scratch");
+  cudaError_t e = bcg::launch_colstats(x, t, n, ldx, sums, mean, sumsq, first_bad, scratch, parts, s);
+  cudaFreeAsync(scratch, s);
+  if (e != cudaSuccess) return cuda_fail(e, "colstats");
+  return BCG_OK;
+}
+
+int bcg_center(const double *x, int64_t t, int64_t n, int64_t ldx, const double *mean, double *xc, void *stream) {
+  if (t < 1 || n < 1 || ldx < n) return fail(BCG_EINVAL, "data must be non-empty with ldx >= n");
+  CUDA_TRY(bcg::launch_center(x, t, n, ldx, mean, xc, static_cast<cudaStream_t>(stream)), "center");
+  return BCG_OK;
+}
+
+int bcg_moment_raw(const bcg_plan *plan, const double *x, int64_t t, int64_t ldx, double *out, void *ws,
+                   size_t ws_bytes, void *stream) {
+  if (!plan) return fail(BCG_EINVAL, "plan is NULL");
+  const bcg::Plan &p = plan->p;
+  if (p.m < 2 || p.m > 16) return fail(BCG_EINVAL, "kernel supports 2 <= m <= 16");
+  if (ldx < p.n) return fail(BCG_EINVAL, "ldx < n");
+  if (!p.d_tiles) return fail(BCG_EINVAL, "host-only plan");
+  return run_moment(p, x, t, ldx, out, ws, ws_bytes, 0, p.lay[p.m].K, static_cast<cudaStream_t>(stream));
+}
+
+int bcg_moment_raw_range(const bcg_plan *plan, const double *x, int64_t t, int64_t ldx, double *out, void *ws,
+                         size_t ws_bytes, int64_t k0, int64_t k1, void *stream) {
+  if (!plan) return fail(BCG_EINVAL, "plan is NULL");
+  const bcg::Plan &p = plan->p;
+  if (p.m < 2 || p.m > 16) return fail(BCG_EINVAL, "kernel supports 2 <= m <= 16");
+  if (ldx < p.n) return fail(BCG_EINVAL, "ldx < n");
+  if (!p.d_tiles) return fail(BCG_EINVAL, "host-only plan");
+  k0 = std::max<int64_t>(k0, 0);
+  k1 = std::min<int64_t>(k1, p.lay[p.m].K);
+  if (k1 <= k0) return BCG_OK;
+  return run_moment(p, x, t, ldx, out, ws, ws_bytes, k0, k1, static_cast<cudaStream_t>(stream));
+}
+
+int bcg_moment_blocks(const double *xt, int64_t n, int64_t t, const int64_t *col0, const int64_t *edges, int64_t m,
+                      int64_t K, double *out, const int64_t *offs, int64_t k0, int64_t k1, void *stream) {
+  if (m < 2 || m > 16) return fail(BCG_EINVAL, "kernel supports 2 <= m <= 16");
+  if (n < 1 || K < 1) return fail(BCG_EINVAL, "empty layout");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // recover b from the layout: the second key is (1, ..., 1, 2) with col0 = b
+  std::vector<int64_t> hc(std::min<int64_t>(K, 2) * m);
+  CUDA_TRY(cudaMemcpyAsync(hc.data(), col0, hc.size() * 8, cudaMemcpyDeviceToHost, s), "layout copy");
+  CUDA_TRY(cudaStreamSynchronize(s), "layout copy");
+  const int64_t b = K >= 2 ? hc[2 * m - 1] : n;
+  if (b < 1) return fail(BCG_EINVAL, "layout is not a block layout");
+  bcg_plan *pl = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto key = std::make_tuple(n, (int)m, (int)b);
+    auto it = g_cache.find(key);
+    if (it == g_cache.end()) {
+      bcg_plan *np = nullptr;
+      int rc = bcg_plan_create(n, (int32_t)m, (int32_t)b, &np);
+      if (rc) return rc;
+      it = g_cache.emplace(key, std::unique_ptr<bcg_plan>(np)).first;
+    }
+    pl = it->second.get();
+  }
+  const bcg::Layout &L = pl->p.lay[m];
+  if (L.K != K) return fail(BCG_EINVAL, "layout does not match _block_layout(n, m, b)");
+  {
+    std::vector<int64_t> hc0(K * m), he(K * m), ho(K + 1);
+    CUDA_TRY(cudaMemcpyAsync(hc0.data(), col0, hc0.size() * 8, cudaMemcpyDeviceToHost, s), "layout copy");
+    CUDA_TRY(cudaMemcpyAsync(he.data(), edges, he.size() * 8, cudaMemcpyDeviceToHost, s), "layout copy");
+    CUDA_TRY(cudaMemcpyAsync(ho.data(), offs, ho.size() * 8, cudaMemcpyDeviceToHost, s), "layout copy");
+    CUDA_TRY(cudaStreamSynchronize(s), "layout copy");
+    if (hc0 != L.col0 || he != L.edges || ho != L.offs)
+      return fail(BCG_EINVAL, "layout does not match _block_layout(n, m, b)");
+  }
+  k0 = std::max<int64_t>(k0, 0);
+  k1 = std::min<int64_t>(k1, K);
+  if (k1 <= k0 || t <= 0) return BCG_OK;
+  double *x = nullptr;
+  void *ws = nullptr;
+  const size_t wsb = ws_bytes_for(pl->p, choose_slicing(pl->p, t));
+  CUDA_TRY(cudaMallocAsync(&x, (size_t)t * n * sizeof(double), s), "transpose buffer");
+  if (wsb) {
+    cudaError_t e = cudaMallocAsync(&ws, wsb, s);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(x, s);
+      return cuda_fail(e, "workspace");
+    }
+  }
+  cudaError_t e = bcg::launch_transpose(xt, n, t, x, s);
+  int rc = e == cudaSuccess ? run_moment(pl->p, x, t, n, out, ws, wsb, k0, k1, s) : cuda_fail(e, "transpose");
+  cudaFreeAsync(x, s);
+  if (ws) cudaFreeAsync(ws, s);
+  return rc;
+}
+
+static int recursion_common(const bcg_plan *plan, double *mk, const double *const *lower, int mode, int sigma_lo,
+                            int sigma_hi, cudaStream_t s) {
+  const bcg::Plan &p = plan->p;
+  if (!p.d_offs) return fail(BCG_EINVAL, "host-only plan");
+  bcg::RecursionArgs a{};
+  a.m = p.m;
+  a.b = p.b;
+  a.n = p.n;
+  a.K = p.lay[p.m].K;
+  a.offs = p.d_offs;
+  a.keys = p.d_keys32;
+  a.sub_rank = p.d_sub_rank;
+  a.part_mask = p.d_part_mask;
+  a.nslots = p.nslots;
+  for (int sg = 0; sg < (int)p.sigma_first.size() && sg < 12; ++sg) a.sigma_first[sg] = p.sigma_first[sg];
+  a.sigma_lo = sigma_lo;
+  a.sigma_hi = sigma_hi;
+  a.p_begin = p.sigma_first[sigma_lo];
+  a.p_end = p.sigma_first[sigma_hi + 1];
+  // orders the processed partitions actually read (bc/cumulants.py:65-66)
+  bool needed[17] = {false};
+  for (int q = a.p_begin; q < a.p_end; ++q)
+    for (int i = 0; i < 8; ++i)
+      if (p.part_mask[q * 8 + i]) needed[__builtin_popcount(p.part_mask[q * 8 + i])] = true;
+  for (int k = 2; k <= p.m - 2; ++k) {
+    a.lower_offs[k] = p.d_lower_offs[k];
+    a.lower[k] = lower ? lower[k - 2] : nullptr;
+    if (needed[k] && !a.lower[k])
+      return fail(BCG_EINVAL, "missing lower cumulant of order " + std::to_string(k));
+  }
+  a.mk = mk;
+  a.mode = mode;
+  if ((size_t)p.nslots * 8 > 200 * 1024) return fail(BCG_EINVAL, "cumulant order too high for the recursion kernel");
+  CUDA_TRY(bcg::launch_recursion(a, s), "recursion kernel");
+  return BCG_OK;
+}
+
+int bcg_cumulant_recursion(const bcg_plan *plan, double *mk, const double *const *lower, void *stream) {
+  if (!plan) return fail(BCG_EINVAL, "plan is NULL");
+  if (plan->p.m <= 3) return BCG_OK;
+  return recursion_common(plan, mk, lower, 0, 2, plan->p.m / 2, static_cast<cudaStream_t>(stream));
+}
+
+int bcg_outer_prod_cum(const bcg_plan *plan, int32_t sigma, const double *const *lower, double *out, void *stream) {
+  if (!plan) return fail(BCG_EINVAL, "plan is NULL");
+  if (sigma < 2 || sigma > plan->p.m / 2)
+    return fail(BCG_EINVAL, "sigma must be in 2..m//2=" + std::to_string(plan->p.m / 2) + ", got " +
+                                std::to_string(sigma));
+  return recursion_common(plan, out, lower, 1, sigma, sigma, static_cast<cudaStream_t>(stream));
+}
+
+int bcg_axpby(int64_t len, double a, const double *x, double c, const double *y, double *out, void *stream) {
+  CUDA_TRY(bcg::launch_axpby(len, a, x, c, y, out, static_cast<cudaStream_t>(stream)), "axpby");
+  return BCG_OK;
+}
+
+int bcg_div(int64_t len, const double *x, double d, double *out, void *stream) {
+  CUDA_TRY(bcg::launch_div(len, x, d, out, static_cast<cudaStream_t>(stream)), "div");
+  return BCG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,177 @@
+// K1: column statistics, finite scan and centering (bc/moments.py:23-41,
+// bc/cumulants.py:31-39), plus small packed-buffer helpers.  All HBM-bound;
+// reductions are two-pass with a fixed order (no float atomics), so results
+// are bitwise reproducible.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace bcg {
+
+constexpr int kCsThreads = 256;
+
+// Pass 1: partition p sums rows [p*t/P, (p+1)*t/P) of every column.
+__global__ void __launch_bounds__(kCsThreads)
+    k_colstats_partial(const double *__restrict__ x, int64_t t, int64_t n, int64_t ldx, int nparts,
+                       double *__restrict__ part_sum, double *__restrict__ part_sq,
+                       unsigned long long *first_bad) {
+  __shared__ double red_s[kCsThreads], red_q[kCsThreads];
+  const int p = blockIdx.x;
+  const int64_t r0 = t * p / nparts, r1 = t * (p + 1) / nparts;
+  const int tid = threadIdx.x;
+  const int lanes = n < kCsThreads ? (int)n : kCsThreads;  // threads per row
+  const int rpi = kCsThreads / lanes;                      // rows per iteration
+  const int c0 = tid % lanes, rph = tid / lanes;
+  const bool active = rph < rpi;
+  for (int64_t cbase = 0; cbase < n; cbase += lanes) {
+    const int64_t c = cbase + c0;
+    double s = 0.0, q = 0.0;
+    if (active && c < n) {
+      for (int64_t r = r0 + rph; r < r1; r += rpi) {
+        const double v = x[r * ldx + c];
+        if (!isfinite(v)) atomicMin(first_bad, (unsigned long long)(r * n + c));
+        s += v;
+        q += v * v;
+      }
+    }
+    red_s[tid] = s;
+    red_q[tid] = q;
+    __syncthreads();
+    if (rph == 0 && c < n) {
+      double ss = 0.0, qq = 0.0;
+      for (int k = 0; k < rpi; ++k) {
+        ss += red_s[k * lanes + c0];
+        qq += red_q[k * lanes + c0];
+      }
+      part_sum[(int64_t)p * n + c] = ss;
+      part_sq[(int64_t)p * n + c] = qq;
+    }
+    __syncthreads();
+  }
+}
+
+// Pass 2: ordered sum over partitions.
+__global__ void k_colstats_final(const double *__restrict__ part_sum, const double *__restrict__ part_sq,
+                                 int nparts, int64_t n, int64_t t, double *sums, double *mean, double *sumsq,
+                                 unsigned long long *first_bad) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0, q = 0.0;
+    for (int p = 0; p < nparts; ++p) {
+      s += part_sum[(int64_t)p * n + c];
+      q += part_sq[(int64_t)p * n + c];
+    }
+    if (sums) sums[c] = s;
+    if (mean) mean[c] = s / (double)t;
+    if (sumsq) sumsq[c] = q;
+  }
+  if (first_bad && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (*first_bad >= 0x7F7F7F7F7F7F7F7FULL) *reinterpret_cast<long long *>(first_bad) = -1;
+  }
+}
+
+int colstats_parts(int64_t t, int64_t n) {
+  (void)n;
+  int64_t parts = (t + 255) / 256;
+  if (parts > 148 * 4) parts = 148 * 4;
+  if (parts < 1) parts = 1;
+  return (int)parts;
+}
+
+cudaError_t launch_colstats(const double *x, int64_t t, int64_t n, int64_t ldx, double *sums, double *mean,
+                            double *sumsq, int64_t *first_bad, double *scratch, int nparts,
+                            cudaStream_t stream) {
+  unsigned long long *fb = reinterpret_cast<unsigned long long *>(first_bad);
+  unsigned long long *fb_scratch = reinterpret_cast<unsigned long long *>(scratch + 2 * (int64_t)nparts * n);
+  if (!fb) fb = fb_scratch;
+  cudaError_t e = cudaMemsetAsync(fb, 0x7F, sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) return e;
+  k_colstats_partial<<<nparts, kCsThreads, 0, stream>>>(x, t, n, ldx, nparts, scratch, scratch + (int64_t)nparts * n,
+                                                         fb);
+  g_launches++;
+  int blocks = (int)((n + 255) / 256);
+  k_colstats_final<<<blocks, 256, 0, stream>>>(scratch, scratch + (int64_t)nparts * n, nparts, n, t, sums, mean,
+                                               sumsq, first_bad ? fb : nullptr);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+// xc = x - mean, one warp per row, lanes across columns (coalesced).
+__global__ void k_center(const double *__restrict__ x, int64_t t, int64_t n, int64_t ldx,
+                         const double *__restrict__ mean, double *__restrict__ xc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < t; r += nwarps)
+    for (int64_t c = lane; c < n; c += 32) xc[r * n + c] = x[r * ldx + c] - mean[c];
+}
+
+cudaError_t launch_center(const double *x, int64_t t, int64_t n, int64_t ldx, const double *mean, double *xc,
+                          cudaStream_t stream) {
+  int64_t blocks = (t + 7) / 8;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  k_center<<<(int)blocks, 256, 0, stream>>>(x, t, n, ldx, mean, xc);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+// x[l, c] = xt[c, l]  (reference passes the transposed data, bc/_engines.py:95)
+__global__ void k_transpose(const double *__restrict__ xt, int64_t n, int64_t t, double *__restrict__ x) {
+  __shared__ double tile[32][33];
+  const int64_t l0 = blockIdx.x * 32LL, c0 = blockIdx.y * 32LL;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, l = l0 + threadIdx.x;
+    if (c < n && l < t) tile[i][threadIdx.x] = xt[c * t + l];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t l = l0 + i, c = c0 + threadIdx.x;
+    if (c < n && l < t) x[l * n + c] = tile[threadIdx.x][i];
+  }
+}
+
+cudaError_t launch_transpose(const double *xt, int64_t n, int64_t t, double *x, cudaStream_t stream) {
+  dim3 grid((unsigned)((t + 31) / 32), (unsigned)((n + 31) / 32));
+  k_transpose<<<grid, dim3(32, 8), 0, stream>>>(xt, n, t, x);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+__global__ void k_axpby(int64_t len, double a, const double *x, double c, const double *y, double *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+    // two roundings each, no FMA contraction: the same float ops as numpy's
+    // `v * s` and `u + w` (bc/symtensor.py:185-200)
+    double v = __dmul_rn(a, x[i]);
+    if (y) v = __dadd_rn(v, __dmul_rn(c, y[i]));
+    out[i] = v;
+  }
+}
+
+cudaError_t launch_axpby(int64_t len, double a, const double *x, double c, const double *y, double *out,
+                         cudaStream_t stream) {
+  if (len <= 0) return cudaSuccess;
+  int64_t blocks = (len + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_axpby<<<(int)blocks, 256, 0, stream>>>(len, a, x, c, y, out);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+__global__ void k_div(int64_t len, const double *x, double d, double *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __ddiv_rn(x[i], d);
+}
+
+cudaError_t launch_div(int64_t len, const double *x, double d, double *out, cudaStream_t stream) {
+  if (len <= 0) return cudaSuccess;
+  int64_t blocks = (len + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_div<<<(int)blocks, 256, 0, stream>>>(len, x, d, out);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+}  // namespace bcg

@@ -1,0 +1,69 @@
+// Kernel launch interfaces shared by the C ABI (capi.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "plan.h"
+
+namespace bcg {
+
+struct MomentArgs {
+  const double *x;
+  int64_t t, ldx;
+  int n, h, r;
+  int bulk_ok;  // rows contiguous and 16-byte aligned: TMA bulk staging
+  const int16_t *rowcols, *colcols;
+  const int32_t *row_keybase, *row_olin, *row_cstart;
+  const int32_t *col_rank, *col_olin, *col_size;
+  const int64_t *offs;
+  const Tile *tiles;
+  const int32_t *tile_kmin, *tile_kmax;
+  int ntiles;
+  int64_t R, C;
+  int nslices;
+  int64_t slice_len;
+  double *out, *ws;
+  int64_t S;
+  int32_t kmin_sel, kmax_sel;
+};
+
+size_t moment_smem_bytes(int KC, int n);
+int pick_kc(int n);
+cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t stream);
+cudaError_t launch_reduce_slices(const double *ws, int nslices, int64_t S, int64_t lo, int64_t hi,
+                                 double *out, cudaStream_t stream);
+
+cudaError_t launch_colstats(const double *x, int64_t t, int64_t n, int64_t ldx, double *sums, double *mean,
+                            double *sumsq, int64_t *first_bad, double *scratch, int nparts,
+                            cudaStream_t stream);
+int colstats_parts(int64_t t, int64_t n);
+cudaError_t launch_center(const double *x, int64_t t, int64_t n, int64_t ldx, const double *mean, double *xc,
+                          cudaStream_t stream);
+cudaError_t launch_transpose(const double *xt, int64_t n, int64_t t, double *x, cudaStream_t stream);
+cudaError_t launch_div(int64_t len, const double *x, double d, double *out, cudaStream_t stream);
+cudaError_t launch_axpby(int64_t len, double a, const double *x, double c, const double *y, double *out,
+                         cudaStream_t stream);
+
+struct RecursionArgs {
+  int m, b;
+  int64_t n;
+  int64_t K;
+  const int64_t *offs;
+  const int32_t *keys;      // K x m, 1-based
+  const int32_t *sub_rank;  // K x nslots
+  const int32_t *part_mask; // per partition 8 masks
+  int nslots;
+  int p_begin, p_end;       // partitions [p_begin, p_end) processed
+  int sigma_lo, sigma_hi;   // sigma range (for grouping into B_sigma)
+  int sigma_first[12];       // sigma -> first partition (host copy)
+  const int64_t *lower_offs[16];
+  const double *lower[16];  // index = order
+  double *mk;               // in/out
+  int mode;                 // 0: mk = mk - sum_sigma B_sigma ; 1: mk = B_sigma (single sigma)
+};
+cudaError_t launch_recursion(const RecursionArgs &args, cudaStream_t stream);
+
+extern int64_t g_launches;
+
+}  // namespace bcg

@@ -1,0 +1,267 @@
+// K2: order-m packed moment as a Khatri-Rao-staged FP64 DMMA GEMM (sm_100a).
+//
+// Reference semantics: bc/_core.pyx:60-148 (raw product sums accumulated into
+// the packed buffer).  Formulation: bc/_engines.py:141-208 (gram engine) --
+// every stored block (L, R) is the sub-matrix W_L^T W_R of the Gram matrix of
+// Khatri-Rao product columns, here restricted to the useful staircase
+// {row group v = L[-1], col R with R[0] >= v} so nothing outside S_m is formed
+// except ragged tile edges.
+//
+// Per CTA (64 x 64 output tile, 4 warps of 32 x 32):
+//   1. a contiguous sample chunk X[s:s+KC, :] is staged into shared memory by
+//      a 1-D TMA bulk copy (cp.async.bulk, mbarrier complete_tx), double
+//      buffered;
+//   2. the chunk's Khatri-Rao factors  A[k][i] = prod_q X[s+k, rowcols[i][q]]
+//      and B[k][j] = prod_q X[s+k, colcols[j][q]] are built in shared memory
+//      (never in HBM), double buffered;
+//   3. warps run mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4) over the chunk, FP64
+//      accumulators in registers;
+//   4. the epilogue scatters each accumulator to its packed address
+//      offs[keybase[row] + rank[col]] + olin[row] * size[col] + olin[col],
+//      either accumulating into `out` (one K-slice) or writing a per-slice
+//      partial that k_reduce_slices sums in fixed order (deterministic split-K,
+//      no float atomics).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+#include "plan.h"
+
+namespace bcg {
+
+constexpr int kPad = 8;  // row stride (TM + 8) doubles == 64 mod 128 bytes: conflict-free fragment loads
+constexpr int kThreads = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra.uni DONE;\n"
+      "bra.uni LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int n = a.n;
+  double *xs = reinterpret_cast<double *>(smem_raw);                   // [2][KC*n]
+  double *kra = xs + 2 * KC * n;                                       // [2][KC][TM+pad]
+  double *krb = kra + 2 * KC * (kTM + kPad);                           // [2][KC][TN+pad]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(krb + 2 * KC * (kTN + kPad));
+
+  const int tid = threadIdx.x;
+  const int unit = blockIdx.x;
+  const int slice = unit / a.ntiles;
+  const int tile_id = unit - slice * a.ntiles;
+  if (a.kmin_sel > 0 || a.kmax_sel < INT32_MAX) {
+    if (a.tile_kmax[tile_id] < a.kmin_sel || a.tile_kmin[tile_id] > a.kmax_sel) return;
+  }
+  const Tile tile = a.tiles[tile_id];
+  const int64_t sbeg = (int64_t)slice * a.slice_len;
+  const int64_t send = min(a.t, sbeg + a.slice_len);
+  const int64_t slen = send - sbeg;
+  const int nch = (int)((slen + KC - 1) / KC);
+
+  // ---- per-thread Khatri-Rao assignment: one row (A) and one col (B), KC/2 samples each ----
+  const int ki = tid & 63;       // row / col within the tile
+  const int kk0 = tid >> 6;      // sample phase 0..1
+  int colA[8], colB[8];
+  const int64_t grow = (int64_t)tile.row0 + ki;
+  const int64_t gcol = (int64_t)tile.col0 + ki;
+  const bool okA = grow < a.R, okB = gcol < a.C;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    colA[q] = (okA && q < a.h) ? a.rowcols[grow * a.h + q] : 0;
+    colB[q] = (okB && q < a.r) ? a.colcols[gcol * a.r + q] : 0;
+  }
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  const uint32_t full_bytes = (uint32_t)(KC * n * sizeof(double));
+  auto chunk_full = [&](int c) { return (int64_t)(c + 1) * KC <= slen && a.bulk_ok; };
+  auto issue = [&](int c) {
+    const double *src = a.x + (sbeg + (int64_t)c * KC) * a.ldx;
+    bulk_g2s(xs + (c & 1) * KC * n, src, full_bytes, &bar[c & 1]);
+  };
+
+  const int warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  if (tid == 0 && nch > 0 && chunk_full(0)) issue(0);
+  for (int c = 0; c < nch; ++c) {
+    const int st = c & 1;
+    if (tid == 0 && c + 1 < nch && chunk_full(c + 1)) issue(c + 1);
+    double *xst = xs + st * KC * n;
+    if (chunk_full(c)) {
+      mbar_wait(&bar[st], (uint32_t)((c >> 1) & 1));
+    } else {
+      // ragged / strided chunk: plain loads, zero-filled past the slice end
+      const int64_t s0 = sbeg + (int64_t)c * KC;
+      const int rows = (int)(send - s0 < KC ? send - s0 : KC);
+      for (int idx = tid; idx < KC * n; idx += kThreads) {
+        const int rr = idx / n, cc = idx - rr * n;
+        xst[idx] = rr < rows ? a.x[(s0 + rr) * a.ldx + cc] : 0.0;
+      }
+      __syncthreads();
+    }
+    // ---- build the chunk's Khatri-Rao factors ----
+    double *ka = kra + st * KC * (kTM + kPad);
+    double *kb = krb + st * KC * (kTN + kPad);
+#pragma unroll 4
+    for (int k = kk0; k < KC; k += 2) {
+      const double *xr = xst + k * n;
+      double pa = xr[colA[0]];
+      double pb = xr[colB[0]];
+#pragma unroll
+      for (int q = 1; q < 8; ++q) {
+        if (q < a.h) pa *= xr[colA[q]];
+        if (q < a.r) pb *= xr[colB[q]];
+      }
+      ka[k * (kTM + kPad) + ki] = okA ? pa : 0.0;
+      kb[k * (kTN + kPad) + ki] = okB ? pb : 0.0;
+    }
+    __syncthreads();
+    // ---- DMMA over the chunk ----
+#pragma unroll
+    for (int k = 0; k < KC; k += 4) {
+      double fa[4], fb[4];
+      const double *pa = ka + (k + tig) * (kTM + kPad) + wm * 32 + gid;
+      const double *pb = kb + (k + tig) * (kTN + kPad) + wn * 32 + gid;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[i] = pa[8 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fb[j] = pb[8 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j], fa[i], fb[j]);
+    }
+  }
+
+  // ---- epilogue: scatter to packed addresses ----
+  double *dst = a.nslices == 1 ? a.out : a.ws + (int64_t)slice * a.S;
+  const bool accumulate = a.nslices == 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t row = (int64_t)tile.row0 + wm * 32 + 8 * i + gid;
+    if (row >= a.R) continue;
+    const int32_t kb0 = a.row_keybase[row], ro = a.row_olin[row], cs = a.row_cstart[row];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t col = (int64_t)tile.col0 + wn * 32 + 8 * j + 2 * tig + e;
+        if (col >= a.C || col < cs) continue;
+        const int32_t key = kb0 + a.col_rank[col];
+        if (key < a.kmin_sel || key > a.kmax_sel) continue;
+        const int64_t addr = a.offs[key] + (int64_t)ro * a.col_size[col] + a.col_olin[col];
+        if (accumulate)
+          dst[addr] += acc[i][j][e];
+        else
+          dst[addr] = acc[i][j][e];
+      }
+    }
+  }
+}
+
+// out[i] += sum_s ws[s * S + i]  for i in [lo, hi), slices summed in order.
+__global__ void k_reduce_slices(const double *__restrict__ ws, int nslices, int64_t S, int64_t lo,
+                                int64_t hi, double *__restrict__ out) {
+  for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < nslices; ++k) s += ws[k * S + i];
+    out[i] += s;
+  }
+}
+
+size_t moment_smem_bytes(int KC, int n) {
+  return sizeof(double) * (2 * (size_t)KC * n + 2 * (size_t)KC * (kTM + kPad) + 2 * (size_t)KC * (kTN + kPad)) +
+         2 * sizeof(uint64_t);
+}
+
+int pick_kc(int n) {
+  // keep the double-buffered sample stage <= 96 KB so >= 2 CTAs fit per SM
+  if (2 * 16 * (size_t)n * 8 <= 96 * 1024) return 16;
+  if (2 * 8 * (size_t)n * 8 <= 96 * 1024) return 8;
+  if (2 * 4 * (size_t)n * 8 <= 160 * 1024) return 4;
+  return 0;
+}
+
+cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t stream) {
+  const size_t smem = moment_smem_bytes(KC, args.n);
+  cudaError_t e;
+  switch (KC) {
+    case 16:
+      e = cudaFuncSetAttribute(k_moment_dmma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      k_moment_dmma<16><<<grid, kThreads, smem, stream>>>(args);
+      break;
+    case 8:
+      e = cudaFuncSetAttribute(k_moment_dmma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      k_moment_dmma<8><<<grid, kThreads, smem, stream>>>(args);
+      break;
+    case 4:
+      e = cudaFuncSetAttribute(k_moment_dmma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      k_moment_dmma<4><<<grid, kThreads, smem, stream>>>(args);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_slices(const double *ws, int nslices, int64_t S, int64_t lo, int64_t hi,
+                                 double *out, cudaStream_t stream) {
+  if (hi <= lo) return cudaSuccess;
+  int64_t blocks = (hi - lo + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_reduce_slices<<<(int)blocks, 256, 0, stream>>>(ws, nslices, S, lo, hi, out);
+  return cudaGetLastError();
+}
+
+}  // namespace bcg

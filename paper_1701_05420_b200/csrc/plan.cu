@@ -1,0 +1,308 @@
+// Host-side plan construction: the reference layout (bc/_engines.py:46-54),
+// the Khatri-Rao GEMM tables of the order-m moment, the staircase tile list
+// and the recursion's partition / sub-block tables.  Runs once per (n, m, b).
+#include "plan.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <functional>
+#include <numeric>
+
+namespace bcg {
+
+static int64_t binom(int64_t a, int64_t c) {
+  if (c < 0 || a < c) return 0;
+  int64_t r = 1;
+  for (int64_t i = 0; i < c; ++i) r = r * (a - i) / (i + 1);
+  return r;
+}
+
+// Rank of a sorted 1-based k-tuple among all sorted k-tuples over 1..nbar in
+// lexicographic (combinations_with_replacement) order, bc/symtensor.py:47-49:
+//   sum_q sum_{v = j_{q-1}}^{j_q - 1} C(nbar - v + k - q, k - q),  j_0 = 1.
+int64_t multiset_rank(const int64_t *key, int k, int64_t nbar) {
+  int64_t rank = 0, prev = 1;
+  for (int q = 1; q <= k; ++q) {
+    for (int64_t v = prev; v < key[q - 1]; ++v) rank += binom(nbar - v + k - q, k - q);
+    prev = key[q - 1];
+  }
+  return rank;
+}
+
+static void enum_sorted(int64_t nbar, int k, std::vector<int64_t> &out) {
+  // lexicographic sorted k-tuples: odometer that resets the tail to the
+  // incremented digit (combinations_with_replacement order)
+  std::vector<int64_t> key(k, 1);
+  if (k == 0) return;
+  while (true) {
+    out.insert(out.end(), key.begin(), key.end());
+    int q = k - 1;
+    while (q >= 0 && key[q] == nbar) --q;
+    if (q < 0) break;
+    ++key[q];
+    for (int i = q + 1; i < k; ++i) key[i] = key[q];
+  }
+}
+
+static inline int64_t edge_of(int64_t j, int64_t n, int64_t b) {
+  return std::min(j * b, n) - (j - 1) * b;
+}
+
+static void build_layout(int64_t n, int b, int64_t nbar, int order, Layout &L) {
+  L.order = order;
+  L.keys.clear();
+  enum_sorted(nbar, order, L.keys);
+  L.K = (int64_t)L.keys.size() / order;
+  L.col0.resize(L.keys.size());
+  L.edges.resize(L.keys.size());
+  L.offs.assign(L.K + 1, 0);
+  for (int64_t k = 0; k < L.K; ++k) {
+    int64_t size = 1;
+    for (int q = 0; q < order; ++q) {
+      int64_t j = L.keys[k * order + q];
+      L.col0[k * order + q] = (j - 1) * b;
+      L.edges[k * order + q] = edge_of(j, n, b);
+      size *= L.edges[k * order + q];
+    }
+    L.offs[k + 1] = L.offs[k] + size;
+  }
+}
+
+// Canonical min-2 partitions of (1..m) into sigma parts, the reference's
+// enumeration order (bc/partitions.py:63-98): element e joins each open part
+// in opening order, then opens a new one; prune when the remaining elements
+// cannot complete every short / unopened part.
+std::vector<std::vector<std::vector<int>>> partitions_min2(int m, int sigma) {
+  std::vector<std::vector<std::vector<int>>> out;
+  std::vector<std::vector<int>> parts;
+  std::function<void(int, int)> rec = [&](int e, int shortc) {
+    int left = m - e + 1;
+    if (e > m) {
+      if ((int)parts.size() == sigma && shortc == 0) out.push_back(parts);
+      return;
+    }
+    if (left < shortc + 2 * (sigma - (int)parts.size())) return;
+    for (size_t i = 0; i < parts.size(); ++i) {
+      bool single = parts[i].size() == 1;
+      parts[i].push_back(e);
+      rec(e + 1, shortc - (single ? 1 : 0));
+      parts[i].pop_back();
+    }
+    if ((int)parts.size() < sigma) {
+      parts.push_back({e});
+      rec(e + 1, shortc + 1);
+      parts.pop_back();
+    }
+  };
+  rec(1, 0);
+  return out;
+}
+
+std::string build_plan(int64_t n, int m, int b, Plan &p) {
+  if (n < 1 || m < 1 || b < 1) return "n, m and b must all be >= 1";
+  if (m > 16) return "kernel supports 2 <= m <= 16";
+  p.n = n;
+  p.m = m;
+  p.b = b;
+  p.nbar = (n + b - 1) / b;
+  if (n > 32767) return "n > 32767 columns is not supported";
+  p.lay.assign(m + 1, Layout());
+  for (int k = 1; k <= m; ++k) build_layout(n, b, p.nbar, k, p.lay[k]);
+  const Layout &LM = p.lay[m];
+  if (LM.offs.back() > (int64_t)INT32_MAX * 64) return "tensor too large";
+  if (LM.K > INT32_MAX) return "too many blocks";
+  if (m < 2) return "";
+
+  // ---- moment GEMM tables: rows = left h-tuples grouped by last entry ----
+  p.h = m / 2;
+  p.r = m - p.h;
+  const int h = p.h, r = p.r;
+  const int64_t nbar = p.nbar;
+  std::vector<int64_t> lt, rt;
+  enum_sorted(nbar, h, lt);
+  enum_sorted(nbar, r, rt);
+  const int64_t NL = (int64_t)lt.size() / h, NR = (int64_t)rt.size() / r;
+  std::vector<int64_t> lorder(NL);
+  std::iota(lorder.begin(), lorder.end(), 0);
+  // (last entry, lexicographic): lex order is already the secondary order
+  std::stable_sort(lorder.begin(), lorder.end(),
+                   [&](int64_t a, int64_t c) { return lt[a * h + h - 1] < lt[c * h + h - 1]; });
+
+  // right columns, lexicographic
+  std::vector<int64_t> rstart(NR + 1, 0);
+  for (int64_t i = 0; i < NR; ++i) {
+    int64_t sz = 1;
+    for (int q = 0; q < r; ++q) sz *= edge_of(rt[i * r + q], n, b);
+    rstart[i + 1] = rstart[i] + sz;
+  }
+  p.C = rstart[NR];
+  p.colcols.resize(p.C * r);
+  p.col_rank.resize(p.C);
+  p.col_olin.resize(p.C);
+  p.col_size.resize(p.C);
+  for (int64_t i = 0; i < NR; ++i) {
+    const int64_t *R = &rt[i * r];
+    int64_t e[16];
+    for (int q = 0; q < r; ++q) e[q] = edge_of(R[q], n, b);
+    int64_t sz = rstart[i + 1] - rstart[i];
+    for (int64_t o = 0; o < sz; ++o) {
+      int64_t c = rstart[i] + o, rem = o;
+      for (int q = r - 1; q >= 0; --q) {
+        p.colcols[c * r + q] = (int16_t)((R[q] - 1) * b + rem % e[q]);
+        rem /= e[q];
+      }
+      p.col_rank[c] = (int32_t)i;
+      p.col_olin[c] = (int32_t)o;
+      p.col_size[c] = (int32_t)sz;
+    }
+  }
+  // first column of the suffix {R : R[0] >= v}; (v, ..., v) is its first tuple
+  std::vector<int64_t> cstart_v(nbar + 2, p.C), rank_first_v(nbar + 2, NR);
+  for (int64_t v = 1; v <= nbar; ++v) {
+    std::vector<int64_t> vv(r, v);
+    int64_t rk = multiset_rank(vv.data(), r, nbar);
+    rank_first_v[v] = rk;
+    cstart_v[v] = rstart[rk];
+  }
+  // rows
+  p.R = 0;
+  for (int64_t i = 0; i < NL; ++i) {
+    int64_t sz = 1;
+    for (int q = 0; q < h; ++q) sz *= edge_of(lt[lorder[i] * h + q], n, b);
+    p.R += sz;
+  }
+  p.rowcols.resize(p.R * h);
+  p.row_keybase.resize(p.R);
+  p.row_olin.resize(p.R);
+  p.row_cstart.resize(p.R);
+  int64_t row = 0;
+  for (int64_t i = 0; i < NL; ++i) {
+    const int64_t *L = &lt[lorder[i] * h];
+    const int64_t v = L[h - 1];
+    int64_t full[16], e[16];
+    for (int q = 0; q < h; ++q) full[q] = L[q];
+    for (int q = h; q < m; ++q) full[q] = v;
+    const int64_t kbase = multiset_rank(full, m, nbar) - rank_first_v[v];
+    int64_t sz = 1;
+    for (int q = 0; q < h; ++q) sz *= (e[q] = edge_of(L[q], n, b));
+    for (int64_t o = 0; o < sz; ++o, ++row) {
+      int64_t rem = o;
+      for (int q = h - 1; q >= 0; --q) {
+        p.rowcols[row * h + q] = (int16_t)((L[q] - 1) * b + rem % e[q]);
+        rem /= e[q];
+      }
+      p.row_keybase[row] = (int32_t)kbase;
+      p.row_olin[row] = (int32_t)o;
+      p.row_cstart[row] = (int32_t)cstart_v[v];
+    }
+  }
+  if (p.R > INT32_MAX || p.C > INT32_MAX) return "GEMM dimension overflow";
+
+  // staircase tiles
+  p.tiles.clear();
+  p.tile_kmin.clear();
+  p.tile_kmax.clear();
+  for (int64_t r0 = 0; r0 < p.R; r0 += kTM) {
+    const int64_t r1 = std::min<int64_t>(r0 + kTM, p.R);
+    for (int64_t c0 = p.row_cstart[r0]; c0 < p.C; c0 += kTN) {
+      const int64_t c1 = std::min<int64_t>(c0 + kTN, p.C);
+      int64_t kmin = INT64_MAX, kmax = -1;
+      for (int64_t rr = r0; rr < r1; ++rr) {
+        int64_t cs = std::max<int64_t>(c0, p.row_cstart[rr]);
+        if (cs >= c1) continue;
+        kmin = std::min<int64_t>(kmin, p.row_keybase[rr] + p.col_rank[cs]);
+        kmax = std::max<int64_t>(kmax, p.row_keybase[rr] + p.col_rank[c1 - 1]);
+      }
+      if (kmax < 0) continue;  // tile entirely below the staircase
+      p.tiles.push_back(Tile{(int32_t)r0, (int32_t)c0});
+      p.tile_kmin.push_back((int32_t)kmin);
+      p.tile_kmax.push_back((int32_t)kmax);
+    }
+  }
+
+  // ---- recursion tables ----
+  p.part_mask.clear();
+  p.part_cnt.clear();
+  p.sigma_first.assign(m / 2 + 2, 0);
+  std::vector<std::vector<int>> slot_modes;  // per slot: modes (0-based)
+  int np = 0;
+  for (int sigma = 2; sigma <= m / 2; ++sigma) {
+    p.sigma_first[sigma] = np;
+    for (auto &parts : partitions_min2(m, sigma)) {
+      p.part_cnt.push_back(sigma);
+      for (int i = 0; i < 8; ++i) {
+        int mask = 0;
+        if (i < sigma) {
+          std::vector<int> md;
+          for (int e : parts[i]) { mask |= 1 << (e - 1); md.push_back(e - 1); }
+          slot_modes.push_back(md);
+        }
+        p.part_mask.push_back(mask);
+      }
+      ++np;
+    }
+  }
+  p.sigma_first[m / 2 + 1] = np;
+  p.nslots = (int32_t)slot_modes.size();
+  if (m >= 4) {
+    p.sub_rank.resize((size_t)LM.K * p.nslots);
+    for (int64_t k = 0; k < LM.K; ++k) {
+      const int64_t *key = &LM.keys[k * m];
+      for (int s = 0; s < p.nslots; ++s) {
+        int64_t sub[16];
+        int len = 0;
+        for (int q : slot_modes[s]) sub[len++] = key[q];
+        p.sub_rank[(size_t)k * p.nslots + s] = (int32_t)multiset_rank(sub, len, nbar);
+      }
+    }
+  }
+  return "";
+}
+
+template <typename T>
+static cudaError_t up(T **dst, const std::vector<T> &src) {
+  if (src.empty()) { *dst = nullptr; return cudaSuccess; }
+  cudaError_t e = cudaMalloc((void **)dst, src.size() * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+std::string upload_plan(Plan &p) {
+  cudaError_t e = cudaSuccess;
+#define UP(d, s) if (e == cudaSuccess) e = up(&p.d, p.s)
+  UP(d_rowcols, rowcols);
+  UP(d_colcols, colcols);
+  UP(d_row_keybase, row_keybase);
+  UP(d_row_olin, row_olin);
+  UP(d_row_cstart, row_cstart);
+  UP(d_col_rank, col_rank);
+  UP(d_col_olin, col_olin);
+  UP(d_col_size, col_size);
+  UP(d_tiles, tiles);
+  UP(d_tile_kmin, tile_kmin);
+  UP(d_tile_kmax, tile_kmax);
+  UP(d_sub_rank, sub_rank);
+  UP(d_part_mask, part_mask);
+#undef UP
+  if (e == cudaSuccess) e = up(&p.d_offs, p.lay[p.m].offs);
+  if (e == cudaSuccess && p.m >= 1) {
+    std::vector<int32_t> k32(p.lay[p.m].keys.begin(), p.lay[p.m].keys.end());
+    e = up(&p.d_keys32, k32);
+  }
+  for (int k = 2; k <= p.m - 2 && e == cudaSuccess; ++k) e = up(&p.d_lower_offs[k], p.lay[k].offs);
+  if (e != cudaSuccess) return std::string("plan upload: ") + cudaGetErrorString(e);
+  return "";
+}
+
+void free_plan(Plan &p) {
+  void *ptrs[] = {p.d_rowcols, p.d_colcols, p.d_row_keybase, p.d_row_olin, p.d_row_cstart,
+                  p.d_col_rank, p.d_col_olin, p.d_col_size, p.d_offs, p.d_tiles, p.d_tile_kmin, p.d_tile_kmax,
+                  p.d_keys32, p.d_sub_rank, p.d_part_mask};
+  for (void *q : ptrs)
+    if (q) cudaFree(q);
+  for (auto &q : p.d_lower_offs)
+    if (q) { cudaFree(q); q = nullptr; }
+}
+
+}  // namespace bcg

@@ -1,0 +1,77 @@
+// Host-built index tables for one (n, m, b).  See DESIGN.md "Data layout in HBM".
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace bcg {
+
+// The reference's _block_layout for one order (bc/_engines.py:46-54).
+struct Layout {
+  int order = 0;
+  int64_t K = 0;                 // blocks = C(nbar + order - 1, order)
+  std::vector<int64_t> keys;     // K x order, 1-based sorted keys, lexicographic
+  std::vector<int64_t> col0;     // K x order, (j - 1) * b
+  std::vector<int64_t> edges;    // K x order
+  std::vector<int64_t> offs;     // K + 1 prefix sums of block sizes
+};
+
+// Moment CTA tile (rows = left Khatri-Rao columns, cols = right ones).
+constexpr int kTM = 64;
+constexpr int kTN = 64;
+
+struct Tile {
+  int32_t row0, col0;
+};
+
+struct Plan {
+  int64_t n = 0;
+  int m = 0, b = 0;
+  int64_t nbar = 0;
+  std::vector<Layout> lay;  // index = order, 0..m (0 unused)
+
+  // --- moment GEMM (order m): left = first h modes, right = last r modes ---
+  int h = 0, r = 0;
+  int64_t R = 0, C = 0;                 // left rows, right cols
+  std::vector<int16_t> rowcols;         // R x h X-column per mode
+  std::vector<int16_t> colcols;         // C x r
+  std::vector<int32_t> row_keybase;     // key index of (L, R) = row_keybase + col_rank
+  std::vector<int32_t> row_olin;        // within-block linear offset of L's modes
+  std::vector<int32_t> row_cstart;      // first valid col of the row's group
+  std::vector<int32_t> col_rank;        // lexicographic rank of R among r-tuples
+  std::vector<int32_t> col_olin;        // within-block offset of R's modes
+  std::vector<int32_t> col_size;        // |R| = prod edges(R)
+  std::vector<Tile> tiles;
+  std::vector<int32_t> tile_kmin, tile_kmax;  // key range a tile touches
+
+  // --- recursion (order m) ---
+  // partition table: for sigma = 2..m/2, partitions in reference order
+  // (bc/partitions.py:63-98).  part_mask[p * 8 + i] = bitmask of modes (0-based)
+  // of part i of partition p; part_cnt[p] = sigma; sigma_first[s] = first p.
+  std::vector<int32_t> part_mask;
+  std::vector<int32_t> part_cnt;
+  std::vector<int32_t> sigma_first;     // size m/2 + 2, sigma_first[sigma]
+  int32_t nslots = 0;                   // total (partition, part) pairs
+  std::vector<int32_t> sub_rank;        // K_m x nslots lower-block index per slot
+
+  // --- device copies ---
+  int16_t *d_rowcols = nullptr, *d_colcols = nullptr;
+  int32_t *d_row_keybase = nullptr, *d_row_olin = nullptr, *d_row_cstart = nullptr;
+  int32_t *d_col_rank = nullptr, *d_col_olin = nullptr, *d_col_size = nullptr;
+  int64_t *d_offs = nullptr;           // offs of order m
+  Tile *d_tiles = nullptr;
+  int32_t *d_tile_kmin = nullptr, *d_tile_kmax = nullptr;
+  int32_t *d_keys32 = nullptr;          // K_m x m keys (1-based)
+  int32_t *d_sub_rank = nullptr;
+  int32_t *d_part_mask = nullptr;
+  int64_t *d_lower_offs[16] = {nullptr};  // offs of orders 2..m-2
+};
+
+// Builders (plan.cu).
+std::string build_plan(int64_t n, int m, int b, Plan &p);
+std::string upload_plan(Plan &p);
+void free_plan(Plan &p);
+int64_t multiset_rank(const int64_t *key, int k, int64_t nbar);
+std::vector<std::vector<std::vector<int>>> partitions_min2(int m, int sigma);
+
+}  // namespace bcg

@@ -1,0 +1,194 @@
+"""Cumulant tensors via the central-moment recursion (the reference's bc/cumulants.py).
+
+C_m = M_m - sum over min-2 partitions of products of lower cumulant blocks
+(bc/cumulants.py:1-13).  The moment comes from the DMMA kernel, the
+correction from the recursion kernel (csrc/recursion.cu) in place on the
+packed M_m buffer; nothing leaves HBM until the caller asks for blocks.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import numpy as np
+
+from . import _native
+from .errors import ValidationError
+from .layout import MAX_M, enumerate_partitions_min2, layout
+from .moments import (
+    _center_device,
+    _colstats,
+    _device_matrix,
+    _moment_device,
+    _raise_if_nonfinite,
+    as_data_matrix,
+    resolve_engine,
+)
+from .symtensor import BlockSymTensor
+
+CENTERING_RTOL = 1e-10  # bc/cumulants.py:26
+
+
+def _check_centered_stats(sums, sumsq, t: int) -> None:
+    """|mean| <= 1e-10 * rms per column (bc/cumulants.py:31-39)."""
+    s = sums.cpu().numpy()
+    q = sumsq.cpu().numpy()
+    means = np.abs(s / t)
+    rms = np.sqrt(q / t)
+    bad = means > CENTERING_RTOL * np.maximum(rms, 1e-300)
+    if bad.any():
+        col = int(np.argmax(bad)) + 1
+        raise ValidationError(f"data is not centered: column {col} has mean {means[col - 1]:.3e}")
+
+
+def _check_centered(X) -> None:
+    st = _colstats(X, sums=True, sumsq=True)
+    _check_centered_stats(st["sums"], st["sumsq"], X.shape[0])
+
+
+def _lower_by_order(lower: Sequence[BlockSymTensor], needed_orders) -> dict:
+    by_order = {}
+    for tensor in lower:
+        by_order[tensor.m] = tensor
+    for k in needed_orders:
+        if k not in by_order:
+            raise ValidationError(f"missing lower cumulant of order {k}")
+    return by_order
+
+
+def _lower_array(by_order: dict, m: int, n: int, b: int):
+    """C array of device pointers lower[k-2] = packed C_k (NULL if absent)."""
+    arr = (ctypes.c_void_p * 15)()
+    keep = []
+    for k in range(2, m - 1):
+        t = by_order.get(k)
+        if t is None:
+            continue
+        if (t.n, t.b) != (n, b):
+            raise ValidationError(
+                f"lower cumulant of order {k} has (n={t.n}, b={t.b}), expected (n={n}, b={b})"
+            )
+        d = t.data
+        keep.append(d)
+        arr[k - 2] = d.data_ptr()
+    return arr, keep
+
+
+def outer_prod_cum(m: int, sigma: int, lower: Sequence[BlockSymTensor],
+                   per_element: bool = False) -> BlockSymTensor:
+    """B_sigma: sum over min-2 partitions into sigma parts of the outer
+    products of lower-cumulant sub-blocks (bc/cumulants.py:53-84).  The
+    kernel is per-element already, so ``per_element`` selects the same path."""
+    if not 2 <= sigma <= m // 2:
+        raise ValidationError(f"sigma must be in 2..m//2={m // 2}, got {sigma}")
+    partitions = enumerate_partitions_min2(m, sigma)
+    needed = sorted({len(part) for parts in partitions for part in parts})
+    by_order = _lower_by_order(lower, needed)
+    ref = by_order[needed[0]]
+    n, b = ref.n, ref.b
+    torch = _native.torch_cuda()
+    plan = _native.plan(n, m, b)
+    arr, keep = _lower_array(by_order, m, n, b)
+    out = torch.empty(layout(n, m, b).size, dtype=torch.float64, device="cuda")
+    _native.check(_native.lib().bcg_outer_prod_cum(plan.handle, sigma, arr, out.data_ptr(),
+                                                   _native.stream_handle()), "outer_prod_cum")
+    del keep
+    return BlockSymTensor(n, m, b, data=out)
+
+
+def _recursion_inplace(result: BlockSymTensor, lower: Sequence[BlockSymTensor]) -> None:
+    m, n, b = result.m, result.n, result.b
+    by_order = _lower_by_order(lower, range(2, m - 1))
+    plan = _native.plan(n, m, b)
+    arr, keep = _lower_array(by_order, m, n, b)
+    _native.check(_native.lib().bcg_cumulant_recursion(plan.handle, result.data.data_ptr(), arr,
+                                                       _native.stream_handle()), "cumulant recursion")
+    del keep
+
+
+def cumulant(x_centered, m: int, lower: Sequence[BlockSymTensor], b: int = 2,
+             engine: str = "auto") -> BlockSymTensor:
+    """Order-m cumulant of centered data (bc/cumulants.py:119-136)."""
+    X = as_data_matrix(x_centered)
+    if m < 2:
+        raise ValidationError(f"order must be >= 2, got {m}")
+    _check_centered(X)
+    resolve_engine(engine)
+    if b < 1:
+        raise ValidationError(f"block size must be >= 1, got {b}")
+    if m <= 3:
+        return _moment_device(X, m, b)
+    _lower_by_order(lower, range(2, m - 1))
+    result = _moment_device(X, m, b)
+    _recursion_inplace(result, lower)
+    return result
+
+
+class CumulantSet:
+    """Cumulants C_1..C_m sharing (n, b); 1-based (bc/cumulants.py:139-170)."""
+
+    def __init__(self, c1: np.ndarray, tensors: Sequence[BlockSymTensor], b: int):
+        self.c1 = np.asarray(c1, dtype=np.float64)
+        self.tensors = list(tensors)
+        self.n = self.c1.shape[0]
+        self.b = b
+        for k, tensor in enumerate(self.tensors, start=2):
+            if tensor.m != k or tensor.n != self.n or tensor.b != b:
+                raise ValidationError("inconsistent cumulant sequence")
+
+    @property
+    def max_order(self) -> int:
+        return 1 + len(self.tensors)
+
+    def __len__(self) -> int:
+        return self.max_order
+
+    def __getitem__(self, order: int):
+        if order == 1:
+            return self.c1
+        if not 2 <= order <= self.max_order:
+            raise KeyError(f"no cumulant of order {order}")
+        return self.tensors[order - 2]
+
+    def __repr__(self):
+        return f"CumulantSet(n={self.n}, b={self.b}, orders=1..{self.max_order})"
+
+
+def cumulants_device(X, m_max: int, b: int, c1_host: bool = True):
+    """Core of cumulants_upto on a device matrix: returns (c1, [C_2..C_m]).
+
+    One colstats pass (means + finite scan), one centering pass, one
+    centering check, then per order one moment GEMM and one in-place
+    recursion -- the reference's sequence (bc/cumulants.py:182-193) without
+    its repeated validation scans.
+    """
+    t, n = X.shape
+    st = _colstats(X, mean=True, bad=True)
+    _raise_if_nonfinite(X, st["bad"])
+    tensors: list[BlockSymTensor] = []
+    if m_max >= 2:
+        Xc = _center_device(X, st["mean"])
+        _check_centered(Xc)
+        for k in range(2, m_max + 1):
+            Mk = _moment_device(Xc, k, b)
+            if k >= 4:
+                _recursion_inplace(Mk, tensors)
+            tensors.append(Mk)
+    c1 = st["mean"].cpu().numpy() if c1_host else st["mean"]
+    return c1, tensors
+
+
+def cumulants_upto(x, m_max: int, b: int = 2, engine: str = "auto") -> CumulantSet:
+    """All cumulants of order 1..m_max of the raw data (bc/cumulants.py:173-193).
+    C_1 is the raw column mean; the data is centered once on the GPU."""
+    X = _device_matrix(x)
+    if not 1 <= m_max <= MAX_M:
+        raise ValidationError(f"m_max must be in 1..{MAX_M}, got {m_max}")
+    if m_max >= 2 and X.shape[0] < 2:
+        raise ValidationError("at least two samples are required for order >= 2")
+    if b < 1:
+        raise ValidationError(f"block size must be >= 1, got {b}")
+    resolve_engine(engine)
+    c1, tensors = cumulants_device(X, m_max, b)
+    return CumulantSet(c1, tensors, b)

@@ -1,0 +1,226 @@
+"""Centering and packed moment tensors on the GPU (the reference's bc/moments.py).
+
+Same entry points, arguments and errors as the reference; the data matrix
+lives in HBM as a C-contiguous (t x n) float64 torch tensor and every pass
+over it is one of our sm_100a kernels (csrc/), reached through the C ABI
+(include/bcgpu.h).  All estimators normalise by the raw sample count t
+(bc/moments.py:1-7).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from .errors import ValidationError
+from .symtensor import BlockSymTensor
+from .layout import layout
+
+ENGINES = ("auto", "compiled", "gram", "blockwise", "cuda")
+PARALLEL_STRATEGIES = ("none", "samples", "blocks")
+
+
+def resolve_engine(engine: str) -> str:
+    """The reference's engine names (bc/_engines.py:33-43) are accepted for
+    signature compatibility; all of them run the single sm_100a backend."""
+    if engine not in ENGINES:
+        raise ValidationError(f"unknown engine {engine!r}, expected one of {ENGINES}")
+    return "cuda"
+
+
+# -- data matrix ---------------------------------------------------------------
+
+
+def _device_matrix(x):
+    """(t, n) C-contiguous float64 CUDA tensor of x (shape checks of
+    bc/moments.py:25-29, no finite scan)."""
+    torch = _native.torch_cuda()
+    if isinstance(x, torch.Tensor):
+        if x.ndim != 2:
+            raise ValidationError(f"data must be 2-D (t x n), got shape {tuple(x.shape)}")
+        t = x.to(device="cuda", dtype=torch.float64)
+        if not t.is_contiguous():
+            t = t.contiguous()
+    else:
+        arr = np.ascontiguousarray(x, dtype=np.float64)
+        if arr.ndim != 2:
+            raise ValidationError(f"data must be 2-D (t x n), got shape {arr.shape}")
+        t = torch.from_numpy(arr).to("cuda")
+    if t.shape[0] < 1 or t.shape[1] < 1:
+        raise ValidationError(f"data must be non-empty, got shape {tuple(t.shape)}")
+    return t
+
+
+def _colstats(X, sums=False, mean=False, sumsq=False, bad=False):
+    """One deterministic pass over X (bcg_colstats): column sums / means /
+    sums of squares and the first non-finite position."""
+    torch = _native.torch_cuda()
+    t, n = X.shape
+    outs = {}
+    for name, want in (("sums", sums), ("mean", mean), ("sumsq", sumsq)):
+        outs[name] = torch.empty(n, dtype=torch.float64, device=X.device) if want else None
+    outs["bad"] = torch.empty(1, dtype=torch.int64, device=X.device) if bad else None
+    p = lambda v: v.data_ptr() if v is not None else None  # noqa: E731
+    _native.check(_native.lib().bcg_colstats(
+        X.data_ptr(), t, n, n, p(outs["sums"]), p(outs["mean"]), p(outs["sumsq"]), p(outs["bad"]),
+        _native.stream_handle()), "colstats")
+    return outs
+
+
+def _raise_if_nonfinite(X, bad) -> None:
+    idx = int(bad.item())
+    if idx >= 0:
+        n = X.shape[1]
+        raise ValidationError(f"non-finite value at row {idx // n + 1}, column {idx % n + 1}")
+
+
+def as_data_matrix(x):
+    """Validate and coerce a t x n observation matrix of finite float64
+    (bc/moments.py:23-35).  Returns the CUDA tensor the kernels read."""
+    X = _device_matrix(x)
+    st = _colstats(X, bad=True)
+    _raise_if_nonfinite(X, st["bad"])
+    return X
+
+
+def _center_device(X, mean):
+    torch = _native.torch_cuda()
+    t, n = X.shape
+    out = torch.empty_like(X)
+    _native.check(_native.lib().bcg_center(X.data_ptr(), t, n, n, mean.data_ptr(), out.data_ptr(),
+                                           _native.stream_handle()), "center")
+    return out
+
+
+def center(x):
+    """Subtract each column's mean (bc/moments.py:38-41); returns a CUDA tensor."""
+    X = _device_matrix(x)
+    st = _colstats(X, mean=True, bad=True)
+    _raise_if_nonfinite(X, st["bad"])
+    return _center_device(X, st["mean"])
+
+
+# -- moments ---------------------------------------------------------------------
+
+
+def _moment_raw_into(X, m: int, b: int, out, key_range=None) -> None:
+    """Accumulate packed RAW order-m sums of X into out (bcg_moment_raw)."""
+    torch = _native.torch_cuda()
+    t, n = X.shape
+    plan = _native.plan(n, m, b)
+    wsb = plan.ws_bytes(t)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=X.device) if wsb else None
+    lib = _native.lib()
+    wsp = ws.data_ptr() if ws is not None else None
+    if key_range is None:
+        rc = lib.bcg_moment_raw(plan.handle, X.data_ptr(), t, n, out.data_ptr(), wsp, wsb,
+                                _native.stream_handle())
+    else:
+        rc = lib.bcg_moment_raw_range(plan.handle, X.data_ptr(), t, n, out.data_ptr(), wsp, wsb,
+                                      int(key_range[0]), int(key_range[1]), _native.stream_handle())
+    _native.check(rc, "moment")
+
+
+def _divide(buf, t: int) -> None:
+    _native.check(_native.lib().bcg_div(buf.numel(), buf.data_ptr(), float(t), buf.data_ptr(),
+                                        _native.stream_handle()), "scale")
+
+
+def _moment_device(X, m: int, b: int) -> BlockSymTensor:
+    """Order-m moment of a validated device matrix (m >= 2)."""
+    torch = _native.torch_cuda()
+    t, n = X.shape
+    out = torch.zeros(layout(n, m, b).size, dtype=torch.float64, device=X.device)
+    _moment_raw_into(X, m, b, out)
+    _divide(out, t)  # the reference's `out /= t` (bc/_engines.py:99)
+    return BlockSymTensor(n, m, b, data=out)
+
+
+def _means_tensor(X, b: int) -> BlockSymTensor:
+    st = _colstats(X, mean=True)
+    return BlockSymTensor(X.shape[1], 1, b, data=st["mean"])
+
+
+def moment(x, m: int, b: int = 2, engine: str = "auto") -> BlockSymTensor:
+    """Order-m moment tensor in block storage (bc/moments.py:44-63)."""
+    X = as_data_matrix(x)
+    if m < 1:
+        raise ValidationError(f"order must be >= 1, got {m}")
+    if b < 1:
+        raise ValidationError(f"block size must be >= 1, got {b}")
+    if m == 1:
+        return _means_tensor(X, b)
+    resolve_engine(engine)
+    if m > 16:
+        raise ValidationError("kernel supports 2 <= m <= 16")
+    return _moment_device(X, m, b)
+
+
+def moment_block(x, key, b: int) -> np.ndarray:
+    """One dense block of the moment tensor (bc/_engines.py:216-232), from
+    the same kernel restricted to that block."""
+    X = as_data_matrix(x)
+    t, n = X.shape
+    m = len(key)
+    if list(key) != sorted(key):
+        raise ValidationError(f"block index {tuple(key)} is not sorted")
+    n_bar = -(-n // b)
+    if any(j < 1 or j > n_bar for j in key):
+        raise ValidationError(f"block index {tuple(key)} out of range 1..{n_bar}")
+    if m == 1:
+        means = _means_tensor(X, b).packed_host()
+        return means[(key[0] - 1) * b:min(key[0] * b, n)].copy()
+    torch = _native.torch_cuda()
+    lay = layout(n, m, b)
+    k = lay.key_index(tuple(key))
+    out = torch.zeros(lay.size, dtype=torch.float64, device=X.device)
+    _moment_raw_into(X, m, b, out, key_range=(k, k + 1))
+    blk = out[int(lay.offs[k]):int(lay.offs[k + 1])].clone()
+    _divide(blk, t)
+    return blk.cpu().numpy().reshape(tuple(lay.edges[k]))
+
+
+def _chunk_bounds(t: int, p: int):
+    bounds = [t * s // p for s in range(p + 1)]
+    return [(bounds[s], bounds[s + 1]) for s in range(p)]
+
+
+def moment_parallel(x, m: int, b: int = 2, p: int = 1, engine: str = "auto") -> BlockSymTensor:
+    """Sample-split moment (bc/moments.py:71-96): contiguous chunks t*s//p,
+    each chunk's moment, combined as sum_s part_s * (t_s / t) in chunk order.
+    p = 1 is exactly `moment`.  (Across GPUs: see distributed.py.)"""
+    X = as_data_matrix(x)
+    t = X.shape[0]
+    if p < 1:
+        raise ValidationError(f"worker count must be >= 1, got {p}")
+    if p > t:
+        raise ValidationError(f"cannot split {t} rows into {p} non-empty chunks")
+    if p == 1:
+        return moment(X, m, b, engine)
+    chunks = _chunk_bounds(t, p)
+    parts = [moment(X[lo:hi], m, b, engine) for lo, hi in chunks]
+    total = parts[0].scale((chunks[0][1] - chunks[0][0]) / t)
+    for (lo, hi), part in zip(chunks[1:], parts[1:]):
+        total = total._axpby(1.0, (hi - lo) / t, part)  # total + part.scale(w), same roundings
+    return total
+
+
+def moment_parallel_blocks(x, m: int, b: int = 2, p: int = 1, engine: str = "auto") -> BlockSymTensor:
+    """Block-split moment (bc/moments.py:99-131): p disjoint key ranges
+    filling one packed buffer; bitwise identical to `moment`."""
+    X = as_data_matrix(x)
+    if p < 1:
+        raise ValidationError(f"worker count must be >= 1, got {p}")
+    if m == 1 or p == 1:
+        return moment(X, m, b, engine)
+    resolve_engine(engine)
+    torch = _native.torch_cuda()
+    t, n = X.shape
+    lay = layout(n, m, b)
+    out = torch.zeros(lay.size, dtype=torch.float64, device=X.device)
+    bounds = [lay.K * s // p for s in range(p + 1)]
+    for s in range(p):
+        if bounds[s] < bounds[s + 1]:
+            _moment_raw_into(X, m, b, out, key_range=(bounds[s], bounds[s + 1]))
+    _divide(out, t)
+    return BlockSymTensor(n, m, b, data=out)

@@ -1,0 +1,359 @@
+"""GPU parity: the sm_100a path against the reference's golden vectors and the
+CPU oracle, on the same seeded inputs (tolerances as the reference's own tests:
+moments rtol 1e-12 atol 1e-14, pkg/tests/test_moments.py:116-126; cumulants
+rtol 1e-9 atol 1e-12, pkg/tests/test_acceptance.py:44-66)."""
+
+import ctypes
+import itertools
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1701_05420_b200 as bcg  # noqa: E402
+from paper_1701_05420_b200 import _native  # noqa: E402
+from oracle import oracle as orc  # noqa: E402
+import workloads  # noqa: E402
+from conftest import random_sym_dense  # noqa: E402
+
+
+def packed(t):
+    return t.packed_host()
+
+
+# ---------------------------------------------------------------- moments
+
+
+def test_moments_match_reference_golden(golden):
+    g = golden("moments.npz")
+    n_cases = 0
+    for key in g.files:
+        if not key.startswith("shape_"):
+            continue
+        i = key.split("_")[1]
+        n, m, b, t = map(int, g[key])
+        got = bcg.moment(g[f"x_{i}"], m, b)
+        np.testing.assert_allclose(packed(got), g[f"m_{i}"], rtol=1e-12, atol=1e-14)
+        n_cases += 1
+    assert n_cases >= 11
+
+
+@pytest.mark.parametrize("n,m,b,t", [(4, 3, 2, 100), (5, 4, 2, 60), (5, 4, 3, 60), (3, 5, 2, 40),
+                                     (6, 2, 4, 200), (2, 6, 1, 30), (3, 3, 5, 50), (6, 6, 2, 300),
+                                     (13, 7, 3, 77), (11, 8, 5, 40), (1, 3, 1, 5), (100, 2, 7, 33),
+                                     (24, 4, 4, 5000), (17, 5, 4, 4097), (9, 3, 2, 1)])
+def test_moment_matches_oracle(n, m, b, t, rng):
+    x = rng.standard_normal((t, n))
+    got = bcg.moment(x, m, b)
+    want = orc.moment(x, m, b)
+    np.testing.assert_allclose(packed(got), want, rtol=1e-12, atol=1e-14)
+
+
+def test_moment_kat_two_sample():
+    # pkg/tests/test_moments.py:71-76
+    t = bcg.moment(np.array([[1.0, 2.0], [3.0, 4.0]]), 2, 2)
+    np.testing.assert_array_equal(t.blocks[(1, 1)], [[5.0, 7.0], [7.0, 10.0]])
+
+
+def test_moment_constant_and_ones():
+    assert bcg.moment(np.full((2, 1), 2.0), 3, 1).blocks[(1, 1, 1)][0, 0, 0] == 8.0
+    t = bcg.moment(np.ones((10, 4)), 2, 2)
+    np.testing.assert_array_equal(t.blocks[(1, 2)], np.ones((2, 2)))
+
+
+def test_moment_order1_is_means(rng):
+    x = rng.standard_normal((40, 5))
+    np.testing.assert_allclose(bcg.moment(x, 1, 2).to_dense(), x.mean(axis=0), rtol=1e-14)
+
+
+def test_moment_dense_against_oracle_dense(rng):
+    x = rng.standard_normal((120, 5))
+    np.testing.assert_allclose(bcg.moment(x, 4, 2).to_dense(), orc.dense_moment(x, 4), rtol=1e-12, atol=1e-15)
+
+
+def test_moment_deterministic_bitwise(rng):
+    x = rng.standard_normal((20000, 12))
+    a = packed(bcg.moment(x, 4, 3))
+    b = packed(bcg.moment(x, 4, 3))
+    np.testing.assert_array_equal(a, b)
+
+
+def test_moment_block_matches(rng):
+    x = rng.standard_normal((23, 5))
+    blk = bcg.moment_block(x, (1, 2), 2)
+    want = orc.moment(x, 2, 2)
+    lay = orc.block_layout(5, 2, 2)
+    k = lay[0].index((1, 2))
+    np.testing.assert_allclose(blk.ravel(), want[lay[3][k]:lay[3][k + 1]], rtol=1e-13)
+    with pytest.raises(bcg.ValidationError, match="not sorted"):
+        bcg.moment_block(x, (2, 1), 2)
+
+
+def test_moment_validation(rng):
+    with pytest.raises(bcg.ValidationError, match="row 2, column 1"):
+        bcg.as_data_matrix([[1.0, 2.0], [np.nan, 3.0]])
+    with pytest.raises(bcg.ValidationError, match="2-D"):
+        bcg.as_data_matrix([1.0, 2.0])
+    with pytest.raises(bcg.ValidationError):
+        bcg.moment(rng.standard_normal((5, 2)), 0)
+    with pytest.raises(bcg.ValidationError):
+        bcg.moment(rng.standard_normal((5, 2)), 2, 0)
+    with pytest.raises(bcg.ValidationError, match="unknown engine"):
+        bcg.moment(rng.standard_normal((5, 2)), 2, 2, engine="nope")
+    x = rng.standard_normal((50, 7))
+    x[31, 4] = np.inf
+    with pytest.raises(bcg.ValidationError, match="row 32, column 5"):
+        bcg.moment(x, 3, 2)
+
+
+def test_moment_torch_input_stays_on_device(rng):
+    x = torch.from_numpy(rng.standard_normal((300, 6))).cuda()
+    t = bcg.moment(x, 3, 2)
+    assert t.data.is_cuda
+    np.testing.assert_allclose(packed(t), orc.moment(x.cpu().numpy(), 3, 2), rtol=1e-12, atol=1e-14)
+
+
+def test_permutation_properties(rng):
+    # pkg/tests/test_moments.py:134-149
+    x = rng.standard_normal((80, 4))
+    a = bcg.moment(x, 3, 2).to_dense()
+    b = bcg.moment(x[rng.permutation(80)], 3, 2).to_dense()
+    np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-15)
+    perm = [2, 0, 3, 1]
+    c = bcg.moment(x[:, perm], 3, 2).to_dense()
+    np.testing.assert_allclose(c, a[np.ix_(perm, perm, perm)], rtol=1e-12, atol=1e-15)
+
+
+# ---------------------------------------------------------------- parallel
+
+
+def test_moment_parallel(rng):
+    x = rng.standard_normal((101, 4))
+    serial = bcg.moment(x, 4, 2)
+    np.testing.assert_array_equal(packed(bcg.moment_parallel(x, 4, 2, p=1)), packed(serial))
+    for p in (2, 3, 4, 7, 8):
+        np.testing.assert_allclose(packed(bcg.moment_parallel(x, 4, 2, p=p)), packed(serial),
+                                   rtol=1e-12, atol=1e-15)
+    with pytest.raises(bcg.ValidationError, match="non-empty"):
+        bcg.moment_parallel(rng.standard_normal((3, 2)), 2, 2, p=5)
+
+
+def test_moment_parallel_equal_chunks_bitwise(rng):
+    # pkg/tests/test_moments.py:171-184: equal chunks -> exactly (1/p) sum parts
+    x = rng.standard_normal((100, 3))
+    par = bcg.moment_parallel(x, 3, 2, p=4)
+    parts = [bcg.moment(x[lo:lo + 25], 3, 2) for lo in (0, 25, 50, 75)]
+    manual = parts[0].scale(0.25)
+    for part in parts[1:]:
+        manual = manual + part.scale(0.25)
+    np.testing.assert_array_equal(packed(par), packed(manual))
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 7])
+def test_moment_parallel_blocks_bitwise(p, rng):
+    x = rng.standard_normal((900, 9))
+    np.testing.assert_array_equal(packed(bcg.moment_parallel_blocks(x, 4, 2, p=p)), packed(bcg.moment(x, 4, 2)))
+
+
+# ---------------------------------------------------------------- drop-in ABI
+
+
+def test_dropin_moment_blocks_matches_oracle(rng):
+    """bcg_moment_blocks with the reference's own arguments (xt, col0, edges,
+    out, offs, k0, k1) and accumulate semantics (bc/_core.pyx:126-148)."""
+    lib = _native.lib()
+    n, m, b, t = 7, 4, 3, 513
+    x = rng.standard_normal((t, n))
+    keys, col0, edges, offs = orc.block_layout(n, m, b)
+    dxt = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+    dc0, de, do = (torch.from_numpy(a).cuda() for a in (col0, edges, offs))
+    out = torch.zeros(int(offs[-1]), dtype=torch.float64, device="cuda")
+    K = len(keys)
+    s = _native.stream_handle()
+    for k0, k1 in ((0, K // 3), (K // 3, K)):
+        _native.check(lib.bcg_moment_blocks(dxt.data_ptr(), n, t, dc0.data_ptr(), de.data_ptr(), m, K,
+                                            out.data_ptr(), do.data_ptr(), k0, k1, s))
+    want = orc.moment_raw_sums(x, m, b)
+    np.testing.assert_allclose(out.cpu().numpy(), want, rtol=1e-12, atol=1e-12)
+    # accumulate: a second full call doubles the sums (verified on the reference)
+    _native.check(lib.bcg_moment_blocks(dxt.data_ptr(), n, t, dc0.data_ptr(), de.data_ptr(), m, K,
+                                        out.data_ptr(), do.data_ptr(), 0, K, s))
+    np.testing.assert_allclose(out.cpu().numpy(), 2 * want, rtol=1e-12, atol=1e-12)
+    rc = lib.bcg_moment_blocks(dxt.data_ptr(), n, t, dc0.data_ptr(), de.data_ptr(), 17, K,
+                               out.data_ptr(), do.data_ptr(), 0, K, s)
+    assert rc == 1 and b"2 <= m <= 16" in lib.bcg_last_error()
+
+
+# ---------------------------------------------------------------- cumulants
+
+
+def test_cumulants_match_reference_golden(golden):
+    g = golden("cumulants.npz")
+    cases = 0
+    worst = 0.0
+    for key in g.files:
+        if not key.startswith("shape_"):
+            continue
+        i = key.split("_")[1]
+        n, t, m_max, b = map(int, g[key])
+        cs = bcg.cumulants_upto(g[f"x_{i}"], m_max, b=b)
+        np.testing.assert_allclose(cs[1], g[f"c1_{i}"], rtol=1e-12, atol=1e-15)
+        for k in range(2, m_max + 1):
+            got, want = packed(cs[k]), g[f"c{k}_{i}"]
+            np.testing.assert_allclose(got, want, rtol=1e-9, atol=1e-12)
+            worst = max(worst, float(np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-3))))
+        cases += 1
+    assert cases >= 24
+    print(f"worst floored relative deviation vs reference: {worst:.2e}")
+
+
+def test_cfg1_full_size_matches_reference(golden):
+    g = golden("configs.npz")
+    cfg = workloads.CONFIGS["cfg1"]
+    x = workloads.generate("cfg1")
+    np.testing.assert_allclose([x.sum(), (x * x).sum()], g["cfg1_xsum"], rtol=1e-12)
+    cs = bcg.cumulants_upto(x, cfg.m, b=cfg.b)
+    np.testing.assert_allclose(cs[1], g["cfg1_c1"], rtol=1e-12, atol=1e-15)
+    for k in range(2, cfg.m + 1):
+        flat = packed(cs[k])
+        np.testing.assert_allclose(flat[g[f"cfg1_c{k}_idx"]], g[f"cfg1_c{k}_val"], rtol=1e-9, atol=1e-12)
+        st = g[f"cfg1_c{k}_stats"]
+        assert flat.size == int(st[2])
+        np.testing.assert_allclose(flat.sum(), st[0], rtol=1e-9, atol=1e-9)
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4", "cfg5"])
+def test_config_shapes_match_reference(name, golden):
+    g = golden("configs.npz")
+    cfg = workloads.CONFIGS[name]
+    x = g[f"{name}_x"]
+    m_top = max(int(k.split("_")[1][1:]) for k in g.files if k.startswith(f"{name}_c") and k.endswith("_idx"))
+    cs = bcg.cumulants_upto(x, m_top, b=cfg.b)
+    np.testing.assert_allclose(cs[1], g[f"{name}_c1"], rtol=1e-12, atol=1e-15)
+    for k in range(2, m_top + 1):
+        flat = packed(cs[k])
+        assert flat.size == int(g[f"{name}_c{k}_stats"][2])
+        np.testing.assert_allclose(flat[g[f"{name}_c{k}_idx"]], g[f"{name}_c{k}_val"], rtol=1e-9, atol=1e-12)
+
+
+def test_cumulants_match_oracle_partial_edges(rng):
+    x = rng.exponential(1.0, size=(700, 7)) + rng.standard_normal((700, 7))
+    c1, want = orc.cumulants_upto(x, 6, 3)
+    cs = bcg.cumulants_upto(x, 6, b=3)
+    for k in range(2, 7):
+        np.testing.assert_allclose(packed(cs[k]), want[k], rtol=1e-9, atol=1e-12)
+
+
+def test_low_orders_bitwise_equal_central_moments(rng):
+    # acceptance criterion 3 (pkg/tests/test_acceptance.py:91-106)
+    data = rng.standard_normal((400, 5)) + rng.standard_normal(5)
+    cs = bcg.cumulants_upto(data, 4, b=2)
+    centered = bcg.center(data)
+    for m in (2, 3):
+        np.testing.assert_array_equal(packed(cs[m]), packed(bcg.moment(centered, m, b=2)))
+
+
+def test_order4_matches_direct_pairings(rng):
+    x = rng.standard_normal((500, 3)) ** 3
+    xc = x - x.mean(axis=0)
+    m4 = orc.dense_moment(xc, 4)
+    cov = xc.T @ xc / x.shape[0]
+    m4 -= np.einsum("ab,cd->abcd", cov, cov) + np.einsum("ac,bd->abcd", cov, cov) + np.einsum("ad,bc->abcd", cov, cov)
+    np.testing.assert_allclose(bcg.cumulants_upto(x, 4, b=2)[4].to_dense(), m4, rtol=1e-10, atol=1e-12)
+
+
+def test_constant_data_exact_zeros():
+    x = np.tile([2.0, -1.0, 0.5], (20, 1))
+    cs = bcg.cumulants_upto(x, 4, b=2)
+    np.testing.assert_array_equal(cs[1], [2.0, -1.0, 0.5])
+    for k in (2, 3, 4):
+        assert cs[k].max_abs() == 0.0
+
+
+def test_two_point_c4():
+    cs = bcg.cumulants_upto(np.array([[-1.0], [1.0]] * 5), 4, b=1)
+    assert cs[4].get((1, 1, 1, 1)) == pytest.approx(-2.0, rel=1e-14)
+
+
+def test_outer_prod_cum_identity_kat():
+    # pkg/tests/test_cumulants.py:35-41
+    c2 = bcg.BlockSymTensor.from_dense(np.eye(3), b=2)
+    out = bcg.outer_prod_cum(4, 2, [c2])
+    assert out.get((1, 1, 1, 1)) == 3.0
+    assert out.get((1, 1, 2, 2)) == 1.0
+    assert out.get((1, 2, 3, 3)) == 0.0
+    assert out.get((1, 2, 3, 1)) == 0.0
+
+
+@pytest.mark.parametrize("m", [4, 5, 6])
+def test_outer_prod_cum_matches_oracle(m, rng):
+    n, b = 5, 2
+    lower = {k: bcg.BlockSymTensor.from_dense(random_sym_dense(n, k, rng), b) for k in range(2, m - 1)}
+    flats = {k: t.packed_host() for k, t in lower.items()}
+    for sigma in range(2, m // 2 + 1):
+        got = bcg.outer_prod_cum(m, sigma, list(lower.values()))
+        # same float ops in the same order as the reference einsum loop
+        np.testing.assert_allclose(packed(got), orc.outer_prod_cum(m, sigma, flats, n, b), rtol=1e-14, atol=1e-15)
+
+
+def test_recursion_errors(rng):
+    x = bcg.center(rng.standard_normal((50, 3)))
+    with pytest.raises(bcg.ValidationError, match="missing lower cumulant"):
+        bcg.cumulant(x, 4, [], b=2)
+    with pytest.raises(bcg.ValidationError, match="not centered"):
+        bcg.cumulant(rng.standard_normal((50, 3)) + 5.0, 3, [], b=2)
+    c2 = bcg.BlockSymTensor.from_dense(random_sym_dense(2, 2, rng), b=2)
+    with pytest.raises(bcg.ValidationError, match="order 3"):
+        bcg.outer_prod_cum(6, 2, [c2])
+    with pytest.raises(bcg.ValidationError):
+        bcg.outer_prod_cum(4, 3, [c2])
+    with pytest.raises(bcg.ValidationError):
+        bcg.cumulants_upto(rng.standard_normal((30, 2)), 13)
+    with pytest.raises(bcg.ValidationError, match="two samples"):
+        bcg.cumulants_upto(np.ones((1, 3)), 2)
+
+
+def test_super_symmetry_of_results(rng):
+    x = rng.standard_normal((150, 4))
+    cs = bcg.cumulants_upto(x, 5, b=2)
+    for m in range(2, 6):
+        for _ in range(100):
+            index = tuple(rng.integers(1, 5, size=m))
+            permuted = tuple(index[q] for q in rng.permutation(m))
+            assert cs[m].get(index) == cs[m].get(permuted)
+
+
+def test_shift_invariance(rng):
+    x = rng.standard_normal((800, 3))
+    a = bcg.cumulants_upto(x, 5, b=2)
+    b = bcg.cumulants_upto(x + np.array([5.0, -3.0, 10.0]), 5, b=2)
+    for k in range(2, 6):
+        da, db = packed(a[k]), packed(b[k])
+        assert np.max(np.abs(da - db)) <= 1e-9 * max(np.max(np.abs(da)), 1e-12)
+
+
+def test_cumulants_deterministic(rng):
+    x = rng.standard_normal((5000, 10))
+    a = bcg.cumulants_upto(x, 5, b=3)
+    b = bcg.cumulants_upto(x, 5, b=3)
+    for k in range(2, 6):
+        np.testing.assert_array_equal(packed(a[k]), packed(b[k]))
+
+
+def test_blocksymtensor_device_arithmetic(rng):
+    u = bcg.BlockSymTensor.from_dense(random_sym_dense(5, 3, rng), 2)
+    v = bcg.BlockSymTensor.from_dense(random_sym_dense(5, 3, rng), 2)
+    np.testing.assert_array_equal((u + v).packed_host(), u.packed_host() + v.packed_host())
+    np.testing.assert_array_equal((u - v).packed_host(), u.packed_host() - v.packed_host())
+    np.testing.assert_array_equal(u.scale(0.3).packed_host(), u.packed_host() * 0.3)
+
+
+def test_native_launches_counted(rng):
+    before = _native.launch_count()
+    bcg.cumulants_upto(rng.standard_normal((100, 4)), 4, b=2)
+    assert _native.launch_count() > before

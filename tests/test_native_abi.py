@@ -1,0 +1,93 @@
+"""The C-ABI library on a CPU-only host: it loads, exports every symbol the
+header declares, and its host-built tables equal the reference's layout and
+map every stored element exactly once (no GPU compute here)."""
+
+import hashlib
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1701_05420_b200 import _native
+from oracle import oracle as orc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    with open(os.path.join(ROOT, "include", "bcgpu.h")) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"\b(bcg_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.lib()
+    syms = header_symbols()
+    assert len(syms) >= 18
+    for s in syms:
+        assert hasattr(lib, s), s
+    bound = {name for name, _, _ in _native.SIGNATURES}
+    assert set(syms) == bound, set(syms) ^ bound
+    assert lib.bcg_version() == 100
+
+
+def test_library_is_sm100a(tmp_path):
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+@pytest.mark.parametrize("n,m,b", [(5, 3, 2), (7, 4, 3), (3, 3, 5), (2, 6, 1), (6, 6, 2), (24, 4, 4),
+                                   (5, 2, 2), (9, 5, 4), (10, 1, 3)])
+def test_native_layout_matches_reference(n, m, b, golden):
+    g = golden("layout.npz")
+    tag = f"{n}_{m}_{b}"
+    plan = _native.Plan(n, m, b, host_only=True)
+    keys, col0, edges, offs = plan.layout(m)
+    np.testing.assert_array_equal(keys, g[f"keys_{tag}"])
+    np.testing.assert_array_equal(col0, g[f"col0_{tag}"])
+    np.testing.assert_array_equal(edges, g[f"edges_{tag}"])
+    np.testing.assert_array_equal(offs, g[f"offs_{tag}"])
+
+
+def test_native_layout_config_digests(golden):
+    digests = json.loads(str(golden("layout.npz")["digests"]))
+    plans = {}
+    for tag, want in digests.items():
+        n, m, b = map(int, tag.split("_"))
+        top = max(int(t.split("_")[1]) for t in digests if t.startswith(f"{n}_") and t.endswith(f"_{b}"))
+        plan = plans.setdefault((n, b), _native.Plan(n, top, b, host_only=True))
+        keys, col0, edges, offs = plan.layout(m)
+        h = hashlib.sha256()
+        for a in (keys, col0, edges, offs):
+            h.update(np.ascontiguousarray(a).tobytes())
+        assert h.hexdigest() == want, tag
+
+
+@pytest.mark.parametrize("n,m,b", [(4, 3, 2), (5, 4, 2), (5, 4, 3), (3, 5, 2), (6, 2, 4), (2, 6, 1),
+                                   (3, 3, 5), (6, 6, 2), (7, 4, 3), (24, 4, 4), (64, 4, 8), (48, 5, 4),
+                                   (36, 6, 3), (13, 7, 3), (11, 8, 5), (1, 3, 1), (100, 2, 7)])
+def test_gemm_mapping_selfcheck(n, m, b):
+    plan = _native.Plan(n, m, b, host_only=True)
+    _native.check(_native.lib().bcg_plan_selfcheck(plan.handle))
+
+
+def test_plan_errors():
+    from paper_1701_05420_b200 import ValidationError
+
+    with pytest.raises(ValidationError, match="2 <= m <= 16"):
+        _native.Plan(4, 17, 2, host_only=True)
+    with pytest.raises(ValidationError):
+        _native.Plan(0, 3, 2, host_only=True)
+
+
+def test_native_partitions_match_python():
+    # sub-key ranks: C++ multiset_rank vs Python key index, via the layout
+    plan = _native.Plan(9, 6, 2, host_only=True)
+    for k in range(2, 7):
+        keys, _, _, _ = plan.layout(k)
+        lay = orc.block_layout(9, k, 2)
+        assert [tuple(r) for r in keys.tolist()] == lay[0]
