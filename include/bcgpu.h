@@ -99,7 +99,9 @@ int bcg_moment_ws_bytes(const bcg_plan *plan, int64_t t, size_t *bytes);
  * ------------------------------------------------------------------------- */
 int bcg_colstats(const double *x, int64_t t, int64_t n, int64_t ldx,
                  double *sums, double *mean, double *sumsq, int64_t *first_bad,
-                 void *stream);
+                 void *ws, size_t ws_bytes, void *stream);
+/* Workspace bytes bcg_colstats needs (per-partition partial sums). */
+size_t bcg_colstats_ws_bytes(int64_t t, int64_t n);
 
 /* xc[l, c] = x[l, c] - mean[c]   (bc/moments.py:38-41). */
 int bcg_center(const double *x, int64_t t, int64_t n, int64_t ldx,
@@ -132,6 +134,13 @@ int bcg_moment_raw_range(const bcg_plan *plan, const double *x, int64_t t,
  * ------------------------------------------------------------------------- */
 int bcg_cumulant_recursion(const bcg_plan *plan, double *mk,
                            const double *const *lower, void *stream);
+
+/* Same, for output blocks [k0, k1) only: the block-list split of the
+ * recursion across GPUs (north_star; bc/moments.py:114-131 splits the same
+ * way across threads).  Only mk[offs[k0]:offs[k1]] is written. */
+int bcg_cumulant_recursion_range(const bcg_plan *plan, double *mk,
+                                 const double *const *lower, int64_t k0,
+                                 int64_t k1, void *stream);
 
 /* Same correction without the moment: out = B_sigma (bc/cumulants.py:53-84,
  * `outer_prod_cum(m, sigma, lower)`), out has S_m elements. */

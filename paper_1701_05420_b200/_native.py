@@ -36,11 +36,13 @@ SIGNATURES = [
     ("bcg_plan_sizes", ctypes.c_int, [_vp, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     ("bcg_plan_layout", ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp]),
     ("bcg_moment_ws_bytes", ctypes.c_int, [_vp, _i64, ctypes.POINTER(_sz)]),
-    ("bcg_colstats", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
+    ("bcg_colstats", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    ("bcg_colstats_ws_bytes", _sz, [_i64, _i64]),
     ("bcg_center", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     ("bcg_moment_raw", ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     ("bcg_moment_raw_range", ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _sz, _i64, _i64, _vp]),
     ("bcg_cumulant_recursion", ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    ("bcg_cumulant_recursion_range", ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
     ("bcg_outer_prod_cum", ctypes.c_int, [_vp, _i32, _vp, _vp, _vp]),
     ("bcg_axpby", ctypes.c_int, [_i64, _dbl, _vp, _dbl, _vp, _vp, _vp]),
     ("bcg_div", ctypes.c_int, [_i64, _vp, _dbl, _vp, _vp]),

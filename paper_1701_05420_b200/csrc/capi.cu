@@ -232,15 +232,20 @@ int bcg_moment_ws_bytes(const bcg_plan *plan, int64_t t, size_t *bytes) {
   return BCG_OK;
 }
 
+size_t bcg_colstats_ws_bytes(int64_t t, int64_t n) {
+  if (t < 1 || n < 1) return 0;
+  return (2 * (size_t)bcg::colstats_parts(t, n) * n + 1) * sizeof(double);
+}
+
 int bcg_colstats(const double *x, int64_t t, int64_t n, int64_t ldx, double *sums, double *mean, double *sumsq,
-                 int64_t *first_bad, void *stream) {
+                 int64_t *first_bad, void *ws, size_t ws_bytes, void *stream) {
   if (t < 1 || n < 1 || ldx < n) return fail(BCG_EINVAL, "data must be non-empty with ldx >= n");
+  if (!ws || ws_bytes < bcg_colstats_ws_bytes(t, n))
+    return fail(BCG_EINVAL, "workspace too small: need " + std::to_string(bcg_colstats_ws_bytes(t, n)) + " bytes");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int parts = bcg::colstats_parts(t, n);
-  double *scratch = nullptr;
-  CUDA_TRY(cudaMallocAsync(&scratch, (2 * (size_t)parts * n + 1) * sizeof(double), s), "colstats scratch");
-  cudaError_t e = bcg::launch_colstats(x, t, n, ldx, sums, mean, sumsq, first_bad, scratch, parts, s);
-  cudaFreeAsync(scratch, s);
+  cudaError_t e = bcg::launch_colstats(x, t, n, ldx, sums, mean, sumsq, first_bad, static_cast<double *>(ws),
+                                       parts, s);
   if (e != cudaSuccess) return cuda_fail(e, "colstats");
   return BCG_OK;
 }
@@ -312,6 +317,16 @@ int bcg_moment_blocks(const double *xt, int64_t n, int64_t t, const int64_t *col
   k0 = std::max<int64_t>(k0, 0);
   k1 = std::min<int64_t>(k1, K);
   if (k1 <= k0 || t <= 0) return BCG_OK;
+  // the reference's signature has no workspace: stream-ordered allocations
+  // from the device pool, kept mapped between calls (no trim at each sync)
+  {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   double *x = nullptr;
   void *ws = nullptr;
   const size_t wsb = ws_bytes_for(pl->p, choose_slicing(pl->p, t));
@@ -331,7 +346,7 @@ int bcg_moment_blocks(const double *xt, int64_t n, int64_t t, const int64_t *col
 }
 
 static int recursion_common(const bcg_plan *plan, double *mk, const double *const *lower, int mode, int sigma_lo,
-                            int sigma_hi, cudaStream_t s) {
+                            int sigma_hi, int64_t k0, int64_t k1, cudaStream_t s) {
   const bcg::Plan &p = plan->p;
   if (!p.d_offs) return fail(BCG_EINVAL, "host-only plan");
   bcg::RecursionArgs a{};
@@ -362,6 +377,8 @@ static int recursion_common(const bcg_plan *plan, double *mk, const double *cons
   }
   a.mk = mk;
   a.mode = mode;
+  a.k0 = std::max<int64_t>(0, k0);
+  a.k1 = std::min<int64_t>(a.K, k1);
   if ((size_t)p.nslots * 8 > 200 * 1024) return fail(BCG_EINVAL, "cumulant order too high for the recursion kernel");
   CUDA_TRY(bcg::launch_recursion(a, s), "recursion kernel");
   return BCG_OK;
@@ -370,7 +387,15 @@ static int recursion_common(const bcg_plan *plan, double *mk, const double *cons
 int bcg_cumulant_recursion(const bcg_plan *plan, double *mk, const double *const *lower, void *stream) {
   if (!plan) return fail(BCG_EINVAL, "plan is NULL");
   if (plan->p.m <= 3) return BCG_OK;
-  return recursion_common(plan, mk, lower, 0, 2, plan->p.m / 2, static_cast<cudaStream_t>(stream));
+  return recursion_common(plan, mk, lower, 0, 2, plan->p.m / 2, 0, plan->p.lay[plan->p.m].K,
+                          static_cast<cudaStream_t>(stream));
+}
+
+int bcg_cumulant_recursion_range(const bcg_plan *plan, double *mk, const double *const *lower, int64_t k0,
+                                 int64_t k1, void *stream) {
+  if (!plan) return fail(BCG_EINVAL, "plan is NULL");
+  if (plan->p.m <= 3) return BCG_OK;
+  return recursion_common(plan, mk, lower, 0, 2, plan->p.m / 2, k0, k1, static_cast<cudaStream_t>(stream));
 }
 
 int bcg_outer_prod_cum(const bcg_plan *plan, int32_t sigma, const double *const *lower, double *out, void *stream) {
@@ -378,7 +403,8 @@ int bcg_outer_prod_cum(const bcg_plan *plan, int32_t sigma, const double *const 
   if (sigma < 2 || sigma > plan->p.m / 2)
     return fail(BCG_EINVAL, "sigma must be in 2..m//2=" + std::to_string(plan->p.m / 2) + ", got " +
                                 std::to_string(sigma));
-  return recursion_common(plan, out, lower, 1, sigma, sigma, static_cast<cudaStream_t>(stream));
+  return recursion_common(plan, out, lower, 1, sigma, sigma, 0, plan->p.lay[plan->p.m].K,
+                          static_cast<cudaStream_t>(stream));
 }
 
 int bcg_axpby(int64_t len, double a, const double *x, double c, const double *y, double *out, void *stream) {

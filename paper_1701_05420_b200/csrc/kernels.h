@@ -55,6 +55,7 @@ struct RecursionArgs {
   const int32_t *part_mask; // per partition 8 masks
   int nslots;
   int p_begin, p_end;       // partitions [p_begin, p_end) processed
+  int64_t k0, k1;           // output blocks [k0, k1) processed
   int sigma_lo, sigma_hi;   // sigma range (for grouping into B_sigma)
   int sigma_first[12];       // sigma -> first partition (host copy)
   const int64_t *lower_offs[16];

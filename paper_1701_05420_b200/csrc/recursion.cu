@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) k_recursion(RecursionArgs a) {
   int64_t *slot_base = reinterpret_cast<int64_t *>(smem_raw);  // nslots
   __shared__ int edges[16];
   const int m = a.m;
-  const int64_t k = blockIdx.x;
+  const int64_t k = a.k0 + blockIdx.x;
   const int tid = threadIdx.x;
   const int32_t *key = a.keys + k * m;
   if (tid < m) {
@@ -97,7 +97,8 @@ cudaError_t launch_recursion(const RecursionArgs &args, cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(k_recursion, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (args.K <= 0) return cudaSuccess;
-  k_recursion<<<(unsigned)args.K, 256, smem, stream>>>(args);
+  if (args.k1 <= args.k0) return cudaSuccess;
+  k_recursion<<<(unsigned)(args.k1 - args.k0), 256, smem, stream>>>(args);
   g_launches++;
   return cudaGetLastError();
 }

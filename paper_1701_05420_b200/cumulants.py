@@ -155,13 +155,14 @@ class CumulantSet:
         return f"CumulantSet(n={self.n}, b={self.b}, orders=1..{self.max_order})"
 
 
-def cumulants_device(X, m_max: int, b: int, c1_host: bool = True):
+def cumulants_device(X, m_max: int, b: int, c1_host: bool = True, timer: dict | None = None):
     """Core of cumulants_upto on a device matrix: returns (c1, [C_2..C_m]).
 
     One colstats pass (means + finite scan), one centering pass, one
     centering check, then per order one moment GEMM and one in-place
     recursion -- the reference's sequence (bc/cumulants.py:182-193) without
-    its repeated validation scans.
+    its repeated validation scans.  ``timer`` (bench.py) collects CUDA events
+    around the top-order moment launch.
     """
     t, n = X.shape
     st = _colstats(X, mean=True, bad=True)
@@ -171,7 +172,13 @@ def cumulants_device(X, m_max: int, b: int, c1_host: bool = True):
         Xc = _center_device(X, st["mean"])
         _check_centered(Xc)
         for k in range(2, m_max + 1):
-            Mk = _moment_device(Xc, k, b)
+            if timer is not None and k == m_max:
+                torch = _native.torch_cuda()
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                timer.setdefault("moment_top", []).append(ev)
+                Mk = _moment_device(Xc, k, b, events=ev)
+            else:
+                Mk = _moment_device(Xc, k, b)
             if k >= 4:
                 _recursion_inplace(Mk, tensors)
             tensors.append(Mk)

@@ -60,10 +60,13 @@ def _colstats(X, sums=False, mean=False, sumsq=False, bad=False):
     for name, want in (("sums", sums), ("mean", mean), ("sumsq", sumsq)):
         outs[name] = torch.empty(n, dtype=torch.float64, device=X.device) if want else None
     outs["bad"] = torch.empty(1, dtype=torch.int64, device=X.device) if bad else None
+    lib = _native.lib()
+    wsb = lib.bcg_colstats_ws_bytes(t, n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=X.device)
     p = lambda v: v.data_ptr() if v is not None else None  # noqa: E731
-    _native.check(_native.lib().bcg_colstats(
+    _native.check(lib.bcg_colstats(
         X.data_ptr(), t, n, n, p(outs["sums"]), p(outs["mean"]), p(outs["sumsq"]), p(outs["bad"]),
-        _native.stream_handle()), "colstats")
+        ws.data_ptr(), wsb, _native.stream_handle()), "colstats")
     return outs
 
 
@@ -126,12 +129,17 @@ def _divide(buf, t: int) -> None:
                                         _native.stream_handle()), "scale")
 
 
-def _moment_device(X, m: int, b: int) -> BlockSymTensor:
-    """Order-m moment of a validated device matrix (m >= 2)."""
+def _moment_device(X, m: int, b: int, events=None) -> BlockSymTensor:
+    """Order-m moment of a validated device matrix (m >= 2).  ``events``:
+    optional (start, end) CUDA events recorded around the GEMM launch(es)."""
     torch = _native.torch_cuda()
     t, n = X.shape
     out = torch.zeros(layout(n, m, b).size, dtype=torch.float64, device=X.device)
+    if events is not None:
+        events[0].record()
     _moment_raw_into(X, m, b, out)
+    if events is not None:
+        events[1].record()
     _divide(out, t)  # the reference's `out /= t` (bc/_engines.py:99)
     return BlockSymTensor(n, m, b, data=out)
 
