@@ -71,6 +71,10 @@ int bcg_moment_blocks(const double *xt, int64_t n, int64_t t,
 typedef struct bcg_plan bcg_plan;
 
 int bcg_plan_create(int64_t n, int32_t m, int32_t b, bcg_plan **plan);
+/* Same with an explicit moment-kernel variant (-1 = default; 0 = v1 64x64
+ * all-warps kernel; 1..4 = warp-specialized tile shapes, K2). */
+int bcg_plan_create_ex(int64_t n, int32_t m, int32_t b, int32_t variant,
+                       bcg_plan **plan);
 /* Host-only plan (tables built, nothing uploaded): layout queries work
  * without a GPU; compute calls on it fail with BCG_EINVAL. */
 int bcg_plan_create_host(int64_t n, int32_t m, int32_t b, bcg_plan **plan);

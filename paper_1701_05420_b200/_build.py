@@ -11,8 +11,8 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbcgpu.so")
-SOURCES = ["plan.cu", "moment.cu", "elementwise.cu", "recursion.cu", "capi.cu"]
-HEADERS = ["plan.h", "kernels.h"]
+SOURCES = ["plan.cu", "moment.cu", "moment_ws.cu", "elementwise.cu", "recursion.cu", "capi.cu"]
+HEADERS = ["plan.h", "kernels.h", "kr.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -29,17 +29,41 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
+DEBUG_LIB = os.path.join(HERE, "libbcgpu_checks.so")
+
+
+def build(force: bool = False, verbose: bool = False, checks: bool = False) -> str:
+    """Compile the sources in parallel (one nvcc per .cu) and link libbcgpu.so.
+    ``checks`` builds libbcgpu_checks.so with device bounds checks
+    (-DBCG_CHECKS); select it at run time with BCG_LIB=checks."""
+    out = DEBUG_LIB if checks else LIB
+    if not force and not checks and not _stale():
+        return out
+    from concurrent.futures import ThreadPoolExecutor
+
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", *SOURCES]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.check_call(cmd, cwd=CSRC)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    extra = ["-DBCG_CHECKS"] if checks else []
+    tag = "chk" if checks else "rel"
+
+    def compile_one(src):
+        obj = os.path.join(CSRC, f".{src}.{tag}.o")
+        cmd = [nvcc, *NVCC_FLAGS[:-1], *extra, "-c", "-o", obj, src]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        subprocess.check_call(cmd, cwd=CSRC)
+        return obj
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    subprocess.check_call([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out + ".tmp", *objs],
+                          cwd=CSRC)
+    os.replace(out + ".tmp", out)
+    for o in objs:
+        os.remove(o)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import sys
+
+    print(build(force=True, verbose="-v" in sys.argv, checks="--checks" in sys.argv))

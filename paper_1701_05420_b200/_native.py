@@ -15,7 +15,9 @@ import numpy as np
 
 from .errors import NativeUnavailableError, ValidationError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbcgpu.so")
+_HERE = os.path.dirname(os.path.abspath(__file__))
+# BCG_LIB=checks selects the bounds-checked debug build (_build.py --checks)
+LIB_PATH = os.path.join(_HERE, "libbcgpu_checks.so" if os.environ.get("BCG_LIB") == "checks" else "libbcgpu.so")
 
 _i64 = ctypes.c_int64
 _i32 = ctypes.c_int32
@@ -30,6 +32,7 @@ SIGNATURES = [
     ("bcg_launch_count", _i64, []),
     ("bcg_moment_blocks", ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp]),
     ("bcg_plan_create", ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(_vp)]),
+    ("bcg_plan_create_ex", ctypes.c_int, [_i64, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
     ("bcg_plan_create_host", ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(_vp)]),
     ("bcg_plan_destroy", ctypes.c_int, [_vp]),
     ("bcg_plan_selfcheck", ctypes.c_int, [_vp]),
@@ -108,12 +111,15 @@ def ptr(tensor) -> int:
 class Plan:
     """Host-built index tables for one (n, m, b) (bcg_plan_create)."""
 
-    def __init__(self, n: int, m: int, b: int, host_only: bool = False):
+    def __init__(self, n: int, m: int, b: int, host_only: bool = False, variant: int = -1):
         self.n, self.m, self.b = int(n), int(m), int(b)
         self.host_only = host_only
+        self.variant = int(variant)
         h = _vp()
-        fn = lib().bcg_plan_create_host if host_only else lib().bcg_plan_create
-        check(fn(self.n, self.m, self.b, ctypes.byref(h)), "plan")
+        if host_only:
+            check(lib().bcg_plan_create_host(self.n, self.m, self.b, ctypes.byref(h)), "plan")
+        else:
+            check(lib().bcg_plan_create_ex(self.n, self.m, self.b, self.variant, ctypes.byref(h)), "plan")
         self._h = h
         self._lib = lib()
 
@@ -154,14 +160,21 @@ class Plan:
 _plans: dict = {}
 
 
+def moment_variant() -> int:
+    """Moment-kernel variant for new plans: $BCG_MOMENT_VARIANT or the
+    library default (-1)."""
+    v = os.environ.get("BCG_MOMENT_VARIANT", "")
+    return int(v) if v.strip() else -1
+
+
 def plan(n: int, m: int, b: int) -> Plan:
-    """Cached device plan for (n, m, b)."""
-    key = (int(n), int(m), int(b))
+    """Cached device plan for (n, m, b) and the current kernel variant."""
+    key = (int(n), int(m), int(b), moment_variant())
     with _lock:
         p = _plans.get(key)
         if p is None:
             torch_cuda()
-            p = _plans[key] = Plan(*key)
+            p = _plans[key] = Plan(key[0], key[1], key[2], variant=key[3])
         return p
 
 

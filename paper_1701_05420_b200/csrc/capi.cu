@@ -52,13 +52,34 @@ struct Slicing {
 Slicing choose_slicing(const bcg::Plan &p, int64_t t) {
   Slicing s{bcg::pick_kc((int)p.n), 1, t};
   if (s.KC == 0 || t <= 0) return s;
+  if (p.variant > 0) s.KC = 16;
   const int64_t ntiles = (int64_t)p.tiles.size();
-  const size_t smem = bcg::moment_smem_bytes(s.KC, (int)p.n);
-  int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / (int64_t)(smem + 1024)));
+  int64_t per_sm = 1;
+  if (p.variant > 0) {
+    int bps = 1;
+    bcg::MomentArgs probe{};
+    probe.n = (int)p.n;
+    probe.h = p.h;
+    probe.r = p.r;
+    if (bcg::launch_moment_ws(probe, p.variant, 0, nullptr, &bps) == cudaSuccess && bps > 0) per_sm = bps;
+  } else {
+    const size_t smem = bcg::moment_smem_bytes(s.KC, (int)p.n);
+    per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / (int64_t)(smem + 1024)));
+  }
   const int64_t concurrent = 148 * per_sm;
-  const int64_t target_units = 8 * concurrent;  // >= 8 waves keeps the tail small
-  int64_t ns = (target_units + ntiles - 1) / ntiles;
-  ns = std::min<int64_t>(ns, std::max<int64_t>(1, t / 1024));
+  // enough units for >= 8 waves, each slice >= 1024 samples; then the slice
+  // count (within +25%) whose last wave is fullest
+  const int64_t ns_max = std::max<int64_t>(1, t / 1024);
+  int64_t ns0 = std::min<int64_t>((8 * concurrent + ntiles - 1) / ntiles, ns_max);
+  int64_t ns = ns0;
+  if (ns0 > 1) {
+    double best = -1.0;
+    for (int64_t cand = ns0; cand <= std::min<int64_t>(ns_max, ns0 + ns0 / 4 + 1); ++cand) {
+      const int64_t units = cand * ntiles;
+      const double eff = (double)units / (double)(((units + concurrent - 1) / concurrent) * concurrent);
+      if (eff > best + 1e-9) { best = eff; ns = cand; }
+    }
+  }
   const int64_t S = p.lay[p.m].offs.back();
   const int64_t ws_cap = (int64_t)1 << 30;  // 1 GiB of split-K partials at most
   if (ns > 1) ns = std::max<int64_t>(1, std::min<int64_t>(ns, ws_cap / (S * 8)));
@@ -115,7 +136,10 @@ int run_moment(const bcg::Plan &p, const double *x, int64_t t, int64_t ldx, doub
   if (k0 == 0 && k1 >= p.lay[p.m].K) a.kmax_sel = INT32_MAX;
   const int64_t grid = (int64_t)a.ntiles * sl.nslices;
   if (grid > INT32_MAX) return fail(BCG_EINVAL, "moment grid too large");
-  CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream), "moment kernel");
+  if (p.variant > 0)
+    CUDA_TRY(bcg::launch_moment_ws(a, p.variant, (int)grid, stream), "moment kernel");
+  else
+    CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream), "moment kernel");
   bcg::g_launches++;
   if (sl.nslices > 1) {
     const auto &offs = p.lay[p.m].offs;
@@ -137,9 +161,14 @@ int bcg_version(void) { return 100; }
 int64_t bcg_launch_count(void) { return bcg::g_launches; }
 
 int bcg_plan_create(int64_t n, int32_t m, int32_t b, bcg_plan **plan) {
+  return bcg_plan_create_ex(n, m, b, -1, plan);
+}
+
+int bcg_plan_create_ex(int64_t n, int32_t m, int32_t b, int32_t variant, bcg_plan **plan) {
   if (!plan) return fail(BCG_EINVAL, "plan pointer is NULL");
+  if (variant > 4) return fail(BCG_EINVAL, "unknown moment kernel variant " + std::to_string(variant));
   auto pl = std::make_unique<bcg_plan>();
-  std::string err = bcg::build_plan(n, m, b, pl->p);
+  std::string err = bcg::build_plan(n, m, b, pl->p, variant);
   if (!err.empty()) return fail(BCG_EINVAL, err);
   err = bcg::upload_plan(pl->p);
   if (!err.empty()) {
@@ -167,8 +196,8 @@ int bcg_plan_selfcheck(const bcg_plan *plan) {
   const int64_t S = L.offs.back();
   std::vector<uint8_t> seen(S, 0);
   for (const bcg::Tile &tl : p.tiles) {
-    for (int64_t r = tl.row0; r < std::min<int64_t>(tl.row0 + bcg::kTM, p.R); ++r) {
-      for (int64_t c = tl.col0; c < std::min<int64_t>(tl.col0 + bcg::kTN, p.C); ++c) {
+    for (int64_t r = tl.row0; r < std::min<int64_t>(tl.row0 + p.tm, p.R); ++r) {
+      for (int64_t c = tl.col0; c < std::min<int64_t>(tl.col0 + p.tn, p.C); ++c) {
         if (c < p.row_cstart[r]) continue;
         const int64_t k = p.row_keybase[r] + p.col_rank[c];
         if (k < 0 || k >= L.K) return fail(BCG_EINVAL, "selfcheck: key index out of range");

@@ -31,6 +31,9 @@ struct MomentArgs {
 size_t moment_smem_bytes(int KC, int n);
 int pick_kc(int n);
 cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t stream);
+cudaError_t launch_moment_ws(const MomentArgs &args, int variant, int grid, cudaStream_t stream,
+                             int *blocks_per_sm = nullptr);
+void ws_tile_shape(int variant, int *tm, int *tn);
 cudaError_t launch_reduce_slices(const double *ws, int nslices, int64_t S, int64_t lo, int64_t hi,
                                  double *out, cudaStream_t stream);
 

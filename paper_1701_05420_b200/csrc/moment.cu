@@ -24,8 +24,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
+#include "kr.cuh"
 #include "plan.h"
 
 namespace bcg {
@@ -71,8 +73,9 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-template <int KC>
+template <int KC, int M>
 __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
+  constexpr int H = M / 2, R = M - M / 2;  // compile-time mode counts (0: runtime)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int n = a.n;
   double *xs = reinterpret_cast<double *>(smem_raw);                   // [2][KC*n]
@@ -149,18 +152,23 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
     // ---- build the chunk's Khatri-Rao factors ----
     double *ka = kra + st * KC * (kTM + kPad);
     double *kb = krb + st * KC * (kTN + kPad);
-#pragma unroll 4
-    for (int k = kk0; k < KC; k += 2) {
-      const double *xr = xst + k * n;
-      double pa = xr[colA[0]];
-      double pb = xr[colB[0]];
+    {
+      double *wa = ka + kk0 * (kTM + kPad) + ki;
+      double *wb = kb + kk0 * (kTN + kPad) + ki;
+      const double *xr = xst + kk0 * n;
 #pragma unroll
-      for (int q = 1; q < 8; ++q) {
-        if (q < a.h) pa *= xr[colA[q]];
-        if (q < a.r) pb *= xr[colB[q]];
+      for (int q = 0; q < 8; ++q) {
+        BCG_CHECK(colA[q] >= 0 && colA[q] < n, "colA", colA[q]);
+        BCG_CHECK(colB[q] >= 0 && colB[q] < n, "colB", colB[q]);
       }
-      ka[k * (kTM + kPad) + ki] = okA ? pa : 0.0;
-      kb[k * (kTN + kPad) + ki] = okB ? pb : 0.0;
+#pragma unroll
+      for (int k = 0; k < KC / 2; ++k) {
+        const double pa = kr_prod<H>(xr, colA, a.h);
+        const double pb = kr_prod<R>(xr, colB, a.r);
+        wa[2 * k * (kTM + kPad)] = okA ? pa : 0.0;
+        wb[2 * k * (kTN + kPad)] = okB ? pb : 0.0;
+        xr += 2 * n;
+      }
     }
     __syncthreads();
     // ---- DMMA over the chunk ----
@@ -197,6 +205,8 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
         const int32_t key = kb0 + a.col_rank[col];
         if (key < a.kmin_sel || key > a.kmax_sel) continue;
         const int64_t addr = a.offs[key] + (int64_t)ro * a.col_size[col] + a.col_olin[col];
+        BCG_CHECK(addr >= 0 && addr < a.S, "epilogue address", addr);
+        BCG_CHECK(key >= 0, "key", key);
         if (accumulate)
           dst[addr] += acc[i][j][e];
         else
@@ -230,29 +240,32 @@ int pick_kc(int n) {
   return 0;
 }
 
-cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t stream) {
+template <int KC, int M>
+static cudaError_t go_v1(const MomentArgs &args, int grid, cudaStream_t stream) {
   const size_t smem = moment_smem_bytes(KC, args.n);
-  cudaError_t e;
-  switch (KC) {
-    case 16:
-      e = cudaFuncSetAttribute(k_moment_dmma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      k_moment_dmma<16><<<grid, kThreads, smem, stream>>>(args);
-      break;
-    case 8:
-      e = cudaFuncSetAttribute(k_moment_dmma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      k_moment_dmma<8><<<grid, kThreads, smem, stream>>>(args);
-      break;
-    case 4:
-      e = cudaFuncSetAttribute(k_moment_dmma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      k_moment_dmma<4><<<grid, kThreads, smem, stream>>>(args);
-      break;
-    default:
-      return cudaErrorInvalidValue;
-  }
+  cudaError_t e = cudaFuncSetAttribute(k_moment_dmma<KC, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_moment_dmma<KC, M><<<grid, kThreads, smem, stream>>>(args);
   return cudaGetLastError();
+}
+
+cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t stream) {
+  static const bool generic = getenv("BCG_FORCE_GENERIC_M") != nullptr;  // debug knob
+  const int m = generic ? 0 : args.h + args.r;
+  cudaError_t e = cudaErrorInvalidValue;
+#define GO16(M, ...) e = go_v1<16, M>(args, grid, stream)
+#define GO8(M, ...) e = go_v1<8, M>(args, grid, stream)
+#define GO4(M, ...) e = go_v1<4, M>(args, grid, stream)
+  switch (KC) {
+    case 16: BCG_DISPATCH_M(m, GO16, 0) break;
+    case 8: BCG_DISPATCH_M(m, GO8, 0) break;
+    case 4: BCG_DISPATCH_M(m, GO4, 0) break;
+    default: break;
+  }
+#undef GO16
+#undef GO8
+#undef GO4
+  return e;
 }
 
 cudaError_t launch_reduce_slices(const double *ws, int nslices, int64_t S, int64_t lo, int64_t hi,

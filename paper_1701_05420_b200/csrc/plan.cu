@@ -5,7 +5,10 @@
 
 #include <cuda_runtime.h>
 
+#include "kernels.h"
+
 #include <algorithm>
+#include <cstdlib>
 #include <functional>
 #include <numeric>
 
@@ -99,8 +102,16 @@ std::vector<std::vector<std::vector<int>>> partitions_min2(int m, int sigma) {
   return out;
 }
 
-std::string build_plan(int64_t n, int m, int b, Plan &p) {
+int default_variant() {
+  const char *env = std::getenv("BCG_MOMENT_VARIANT");
+  if (env && *env) return std::atoi(env);
+  return 0;
+}
+
+std::string build_plan(int64_t n, int m, int b, Plan &p, int variant) {
   if (n < 1 || m < 1 || b < 1) return "n, m and b must all be >= 1";
+  p.variant = variant < 0 ? default_variant() : variant;
+  ws_tile_shape(p.variant, &p.tm, &p.tn);
   if (m > 16) return "kernel supports 2 <= m <= 16";
   p.n = n;
   p.m = m;
@@ -203,10 +214,10 @@ std::string build_plan(int64_t n, int m, int b, Plan &p) {
   p.tiles.clear();
   p.tile_kmin.clear();
   p.tile_kmax.clear();
-  for (int64_t r0 = 0; r0 < p.R; r0 += kTM) {
-    const int64_t r1 = std::min<int64_t>(r0 + kTM, p.R);
-    for (int64_t c0 = p.row_cstart[r0]; c0 < p.C; c0 += kTN) {
-      const int64_t c1 = std::min<int64_t>(c0 + kTN, p.C);
+  for (int64_t r0 = 0; r0 < p.R; r0 += p.tm) {
+    const int64_t r1 = std::min<int64_t>(r0 + p.tm, p.R);
+    for (int64_t c0 = p.row_cstart[r0]; c0 < p.C; c0 += p.tn) {
+      const int64_t c1 = std::min<int64_t>(c0 + p.tn, p.C);
       int64_t kmin = INT64_MAX, kmax = -1;
       for (int64_t rr = r0; rr < r1; ++rr) {
         int64_t cs = std::max<int64_t>(c0, p.row_cstart[rr]);

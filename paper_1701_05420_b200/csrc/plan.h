@@ -26,6 +26,8 @@ struct Tile {
 
 struct Plan {
   int64_t n = 0;
+  int variant = 0;          // moment kernel: 0 = v1 (64x64), >0 = warp-specialized shape
+  int tm = kTM, tn = kTN;   // CTA tile of the staircase GEMM
   int m = 0, b = 0;
   int64_t nbar = 0;
   std::vector<Layout> lay;  // index = order, 0..m (0 unused)
@@ -68,7 +70,8 @@ struct Plan {
 };
 
 // Builders (plan.cu).
-std::string build_plan(int64_t n, int m, int b, Plan &p);
+std::string build_plan(int64_t n, int m, int b, Plan &p, int variant = -1);
+int default_variant();
 std::string upload_plan(Plan &p);
 void free_plan(Plan &p);
 int64_t multiset_rank(const int64_t *key, int k, int64_t nbar);

@@ -357,3 +357,29 @@ def test_native_launches_counted(rng):
     before = _native.launch_count()
     bcg.cumulants_upto(rng.standard_normal((100, 4)), 4, b=2)
     assert _native.launch_count() > before
+
+
+# ---------------------------------------------------------------- kernel variants
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+def test_moment_kernel_variants_match_oracle(variant, monkeypatch, rng):
+    monkeypatch.setenv("BCG_MOMENT_VARIANT", str(variant))
+    for n, m, b, t in [(7, 4, 3, 1003), (13, 5, 2, 517), (9, 6, 2, 211), (24, 4, 4, 4099), (5, 2, 2, 70),
+                       (30, 3, 4, 333)]:
+        x = rng.standard_normal((t, n))
+        np.testing.assert_allclose(packed(bcg.moment(x, m, b)), orc.moment(x, m, b), rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_cumulants_variants_match_reference_golden(variant, monkeypatch, golden):
+    monkeypatch.setenv("BCG_MOMENT_VARIANT", str(variant))
+    g = golden("cumulants.npz")
+    for key in g.files:
+        if not key.startswith("shape_"):
+            continue
+        i = key.split("_")[1]
+        n, t, m_max, b = map(int, g[key])
+        cs = bcg.cumulants_upto(g[f"x_{i}"], m_max, b=b)
+        for k in range(2, m_max + 1):
+            np.testing.assert_allclose(packed(cs[k]), g[f"c{k}_{i}"], rtol=1e-9, atol=1e-12)
