@@ -1,0 +1,81 @@
+"""Multi-process (gloo, world size 2) test of the t-sharded cumulant path's
+collective logic (distributed.py).  The per-rank kernels are replaced by the
+CPU oracle, so this runs on a GPU-less host; the CUDA ops are covered by the
+GPU parity tests."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as orc
+from paper_1701_05420_b200.distributed import block_bounds, cumulants_upto_sharded, shard_bounds
+from paper_1701_05420_b200.layout import layout
+
+
+class OracleOps:
+    """Per-rank compute on the CPU oracle (test stand-in for CudaOps)."""
+
+    def matrix(self, x):
+        return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64))
+
+    def colstats(self, X):
+        a = X.numpy()
+        bad = np.argwhere(~np.isfinite(a))
+        first = int(bad[0][0] * a.shape[1] + bad[0][1]) if len(bad) else -1
+        return torch.as_tensor(a.sum(0)), torch.as_tensor((a * a).sum(0)), torch.tensor([first])
+
+    def center(self, X, mean):
+        return X - mean
+
+    def moment_raw(self, X, k, b):
+        return torch.as_tensor(orc.moment_raw_sums(X.numpy(), k, b))
+
+    def divide(self, buf, t):
+        buf /= t
+
+    def recursion_range(self, mk, n, k, b, lower, k0, k1):
+        full = orc.cumulant_from_moment(mk.numpy().copy(), k, {j: v.numpy() for j, v in lower.items()}, n, b)
+        lay = layout(n, k, b)
+        lo, hi = int(lay.offs[k0]), int(lay.offs[k1])
+        mk[lo:hi] = torch.as_tensor(full[lo:hi])
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, x, m_max, b, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = shard_bounds(x.shape[0], world, rank)
+    mean, tensors = cumulants_upto_sharded(x[lo:hi], m_max, b, ops=OracleOps())
+    np.savez(f"{out_path}_{rank}.npz", mean=mean.numpy(), **{f"c{k}": t.numpy() for k, t in enumerate(tensors, 2)})
+    dist.destroy_process_group()
+
+
+def test_shard_and_block_bounds():
+    assert [shard_bounds(101, 4, r) for r in range(4)] == [(0, 25), (25, 50), (50, 75), (75, 101)]
+    spans = [block_bounds(330, 8, r) for r in range(8)]
+    assert spans[0][0] == 0 and spans[-1][1] == 330
+    assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_cumulants_match_oracle(world, tmp_path, rng):
+    x = rng.exponential(1.0, size=(403, 5)) + rng.standard_normal((403, 5))
+    m_max, b = 6, 2
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, x, m_max, b, str(tmp_path / "out")), nprocs=world, join=True)
+    c1, want = orc.cumulants_upto(x, m_max, b)
+    for r in range(world):
+        got = np.load(tmp_path / f"out_{r}.npz")
+        np.testing.assert_allclose(got["mean"], c1, rtol=1e-13)
+        for k in range(2, m_max + 1):
+            np.testing.assert_allclose(got[f"c{k}"], want[k], rtol=1e-9, atol=1e-12)
