@@ -32,7 +32,7 @@
 
 namespace bcg {
 
-constexpr int kPad = 8;  // row stride (TM + 8) doubles == 64 mod 128 bytes: conflict-free fragment loads
+constexpr int kPad = 4;  // row stride (TM + 4) doubles == 32 mod 128 bytes: the 4 k-rows of an m8n8k4 fragment load hit 4 distinct bank quadrants (conflict-free)
 constexpr int kThreads = 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -132,13 +132,14 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  if (tid == 0 && nch > 0 && chunk_full(0)) issue(0);
-  for (int c = 0; c < nch; ++c) {
-    const int st = c & 1;
-    if (tid == 0 && c + 1 < nch && chunk_full(c + 1)) issue(c + 1);
-    double *xst = xs + st * KC * n;
+  // Software pipeline, one CTA barrier per chunk: while the warps issue the
+  // DMMAs of chunk c they also build the Khatri-Rao factors of chunk c+1 into
+  // the other KR buffer; the TMA copy of chunk c+2 is in flight meanwhile.
+  //   stage(x) = x & 1 for both the X ring and the KR double buffer.
+  auto load_x = [&](int c) {  // make chunk c's samples resident in xs[c & 1]
+    double *xst = xs + (c & 1) * KC * n;
     if (chunk_full(c)) {
-      mbar_wait(&bar[st], (uint32_t)((c >> 1) & 1));
+      mbar_wait(&bar[c & 1], (uint32_t)((c >> 1) & 1));
     } else {
       // ragged / strided chunk: plain loads, zero-filled past the slice end
       const int64_t s0 = sbeg + (int64_t)c * KC;
@@ -149,29 +150,44 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
       }
       __syncthreads();
     }
-    // ---- build the chunk's Khatri-Rao factors ----
-    double *ka = kra + st * KC * (kTM + kPad);
-    double *kb = krb + st * KC * (kTN + kPad);
-    {
-      double *wa = ka + kk0 * (kTM + kPad) + ki;
-      double *wb = kb + kk0 * (kTN + kPad) + ki;
-      const double *xr = xst + kk0 * n;
+  };
+  auto build = [&](int c) {  // Khatri-Rao factors of chunk c -> kra/krb[c & 1]
+    const double *xr = xs + (c & 1) * KC * n + kk0 * n;
+    double *wa = kra + (c & 1) * KC * (kTM + kPad) + kk0 * (kTM + kPad) + ki;
+    double *wb = krb + (c & 1) * KC * (kTN + kPad) + kk0 * (kTN + kPad) + ki;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        BCG_CHECK(colA[q] >= 0 && colA[q] < n, "colA", colA[q]);
-        BCG_CHECK(colB[q] >= 0 && colB[q] < n, "colB", colB[q]);
-      }
-#pragma unroll
-      for (int k = 0; k < KC / 2; ++k) {
-        const double pa = kr_prod<H>(xr, colA, a.h);
-        const double pb = kr_prod<R>(xr, colB, a.r);
-        wa[2 * k * (kTM + kPad)] = okA ? pa : 0.0;
-        wb[2 * k * (kTN + kPad)] = okB ? pb : 0.0;
-        xr += 2 * n;
-      }
+    for (int q = 0; q < 8; ++q) {
+      BCG_CHECK(colA[q] >= 0 && colA[q] < n, "colA", colA[q]);
+      BCG_CHECK(colB[q] >= 0 && colB[q] < n, "colB", colB[q]);
     }
+#pragma unroll
+    for (int k = 0; k < KC / 2; ++k) {
+      const double pa = kr_prod<H>(xr, colA, a.h);
+      const double pb = kr_prod<R>(xr, colB, a.r);
+      wa[2 * k * (kTM + kPad)] = okA ? pa : 0.0;
+      wb[2 * k * (kTN + kPad)] = okB ? pb : 0.0;
+      xr += 2 * n;
+    }
+  };
+
+  if (nch > 0) {
+    if (tid == 0) {
+      if (chunk_full(0)) issue(0);
+      if (nch > 1 && chunk_full(1)) issue(1);
+    }
+    load_x(0);
+    build(0);
     __syncthreads();
-    // ---- DMMA over the chunk ----
+    if (tid == 0 && nch > 2 && chunk_full(2)) issue(2);
+  }
+  for (int c = 0; c < nch; ++c) {
+    if (c + 1 < nch) {
+      load_x(c + 1);
+      build(c + 1);
+    }
+    // ---- DMMA over chunk c ----
+    const double *ka = kra + (c & 1) * KC * (kTM + kPad);
+    const double *kb = krb + (c & 1) * KC * (kTN + kPad);
 #pragma unroll
     for (int k = 0; k < KC; k += 4) {
       double fa[4], fb[4];
@@ -186,6 +202,8 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma884(acc[i][j], fa[i], fb[j]);
     }
+    __syncthreads();  // KR[c+1] complete, KR[c] and xs[(c+1) & 1] free
+    if (tid == 0 && c + 3 < nch && chunk_full(c + 3)) issue(c + 3);
   }
 
   // ---- epilogue: scatter to packed addresses ----

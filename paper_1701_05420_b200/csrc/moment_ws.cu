@@ -69,8 +69,8 @@ struct WsShape {
   static constexpr int NCONS = (TM / WM) * (TN / WN);
   static constexpr int NWARPS = 1 + NPROD + NCONS;
   static constexpr int NTHREADS = NWARPS * 32;
-  static constexpr int LDA = TM + 8;  // == 64 mod 128 bytes: 2-wavefront fragment loads
-  static constexpr int LDB = TN + 8;
+  static constexpr int LDA = TM + 4;  // == 32 mod 128 bytes: conflict-free fragment loads
+  static constexpr int LDB = TN + 4;
   static constexpr int MT = WM / 8, NT = WN / 8;
   static constexpr int JT = TM + TN;  // Khatri-Rao columns built per sample
   static constexpr int NPT = NPROD * 32;
