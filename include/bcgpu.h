@@ -75,6 +75,19 @@ int bcg_plan_create(int64_t n, int32_t m, int32_t b, bcg_plan **plan);
  * all-warps kernel; 1..4 = warp-specialized tile shapes, K2). */
 int bcg_plan_create_ex(int64_t n, int32_t m, int32_t b, int32_t variant,
                        bcg_plan **plan);
+/* Fused multi-order plan: ONE staircase GEMM over the block alphabet extended
+ * by a constant "ones" block yields the raw sums of every order 2..m (a key
+ * with z ones is the order-(m - z) key of its other entries) -- a single pass
+ * over X for cumulants_upto's moments (bc/cumulants.py:187-192 computes one
+ * moment per order).  bcg_moment_raw on it accumulates into a buffer of
+ * S_2 + ... + S_m elements, order o's packed tensor at order_base[o]
+ * (bcg_plan_output).  host_only != 0: tables only (layout / selfcheck). */
+int bcg_plan_create_fused(int64_t n, int32_t m, int32_t b, int32_t host_only,
+                          bcg_plan **plan);
+/* Output size of bcg_moment_raw on this plan (S_m, or S_2 + ... + S_m for a
+ * fused plan) and, if order_base != NULL (m + 2 entries), each order's start
+ * offset in it (fused plans; zeros otherwise, order_base[m + 1] = S_out). */
+int bcg_plan_output(const bcg_plan *plan, int64_t *S_out, int64_t *order_base);
 /* Host-only plan (tables built, nothing uploaded): layout queries work
  * without a GPU; compute calls on it fail with BCG_EINVAL. */
 int bcg_plan_create_host(int64_t n, int32_t m, int32_t b, bcg_plan **plan);

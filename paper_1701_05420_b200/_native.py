@@ -33,6 +33,8 @@ SIGNATURES = [
     ("bcg_moment_blocks", ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp]),
     ("bcg_plan_create", ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(_vp)]),
     ("bcg_plan_create_ex", ctypes.c_int, [_i64, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
+    ("bcg_plan_create_fused", ctypes.c_int, [_i64, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
+    ("bcg_plan_output", ctypes.c_int, [_vp, ctypes.POINTER(_i64), _vp]),
     ("bcg_plan_create_host", ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(_vp)]),
     ("bcg_plan_destroy", ctypes.c_int, [_vp]),
     ("bcg_plan_selfcheck", ctypes.c_int, [_vp]),
@@ -111,12 +113,16 @@ def ptr(tensor) -> int:
 class Plan:
     """Host-built index tables for one (n, m, b) (bcg_plan_create)."""
 
-    def __init__(self, n: int, m: int, b: int, host_only: bool = False, variant: int = -1):
+    def __init__(self, n: int, m: int, b: int, host_only: bool = False, variant: int = -1,
+                 fused: bool = False):
         self.n, self.m, self.b = int(n), int(m), int(b)
         self.host_only = host_only
         self.variant = int(variant)
+        self.fused = bool(fused)
         h = _vp()
-        if host_only:
+        if fused:
+            check(lib().bcg_plan_create_fused(self.n, self.m, self.b, int(host_only), ctypes.byref(h)), "plan")
+        elif host_only:
             check(lib().bcg_plan_create_host(self.n, self.m, self.b, ctypes.byref(h)), "plan")
         else:
             check(lib().bcg_plan_create_ex(self.n, self.m, self.b, self.variant, ctypes.byref(h)), "plan")
@@ -143,6 +149,14 @@ class Plan:
                                         edges.ctypes.data, offs.ctypes.data))
         return keys, col0, edges, offs
 
+    def output(self):
+        """(S_out, order_base): output size of bcg_moment_raw and, for a fused
+        plan, each order's offset in it."""
+        S = _i64()
+        base = np.zeros(self.m + 2, dtype=np.int64)
+        check(self._lib.bcg_plan_output(self._h, ctypes.byref(S), base.ctypes.data))
+        return S.value, base
+
     def ws_bytes(self, t: int) -> int:
         out = _sz()
         check(self._lib.bcg_moment_ws_bytes(self._h, int(t), ctypes.byref(out)))
@@ -167,14 +181,15 @@ def moment_variant() -> int:
     return int(v) if v.strip() else -1
 
 
-def plan(n: int, m: int, b: int) -> Plan:
-    """Cached device plan for (n, m, b) and the current kernel variant."""
-    key = (int(n), int(m), int(b), moment_variant())
+def plan(n: int, m: int, b: int, fused: bool = False) -> Plan:
+    """Cached device plan for (n, m, b), the current kernel variant and
+    whether it is the fused multi-order plan."""
+    key = (int(n), int(m), int(b), -1 if fused else moment_variant(), bool(fused))
     with _lock:
         p = _plans.get(key)
         if p is None:
             torch_cuda()
-            p = _plans[key] = Plan(key[0], key[1], key[2], variant=key[3])
+            p = _plans[key] = Plan(key[0], key[1], key[2], variant=key[3], fused=key[4])
         return p
 
 

@@ -42,57 +42,30 @@ int cuda_fail(cudaError_t e, const char *what) {
     if (_e != cudaSuccess) return cuda_fail(_e, what); \
   } while (0)
 
-// Split-K decision shared by bcg_moment_ws_bytes and bcg_moment_raw.
+// Split-K decision shared by bcg_moment_ws_bytes and bcg_moment_raw: fixed
+// kSliceLen-sample slices (association independent of the plan), launched in
+// groups whose partials fit the workspace cap.
 struct Slicing {
   int KC;
-  int nslices;
+  int nslices;   // total slices
+  int group;     // slices per launch
   int64_t slice_len;
 };
 
+constexpr int64_t kWsCap = (int64_t)2 << 30;  // 2 GiB of split-K partials at most
+
 Slicing choose_slicing(const bcg::Plan &p, int64_t t) {
-  Slicing s{bcg::pick_kc((int)p.n), 1, t};
-  if (s.KC == 0 || t <= 0) return s;
+  Slicing s{bcg::pick_kc((int)p.n), 1, 1, bcg::kSliceLen};
   if (p.variant > 0) s.KC = 16;
-  const int64_t ntiles = (int64_t)p.tiles.size();
-  int64_t per_sm = 1;
-  if (p.variant > 0) {
-    int bps = 1;
-    bcg::MomentArgs probe{};
-    probe.n = (int)p.n;
-    probe.h = p.h;
-    probe.r = p.r;
-    if (bcg::launch_moment_ws(probe, p.variant, 0, nullptr, &bps) == cudaSuccess && bps > 0) per_sm = bps;
-  } else {
-    const size_t smem = bcg::moment_smem_bytes(s.KC, (int)p.n);
-    per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / (int64_t)(smem + 1024)));
-  }
-  const int64_t concurrent = 148 * per_sm;
-  // enough units for >= 8 waves, each slice >= 1024 samples; then the slice
-  // count (within +25%) whose last wave is fullest
-  const int64_t ns_max = std::max<int64_t>(1, t / 1024);
-  int64_t ns0 = std::min<int64_t>((8 * concurrent + ntiles - 1) / ntiles, ns_max);
-  int64_t ns = ns0;
-  if (ns0 > 1) {
-    double best = -1.0;
-    for (int64_t cand = ns0; cand <= std::min<int64_t>(ns_max, ns0 + ns0 / 4 + 1); ++cand) {
-      const int64_t units = cand * ntiles;
-      const double eff = (double)units / (double)(((units + concurrent - 1) / concurrent) * concurrent);
-      if (eff > best + 1e-9) { best = eff; ns = cand; }
-    }
-  }
-  const int64_t S = p.lay[p.m].offs.back();
-  const int64_t ws_cap = (int64_t)1 << 30;  // 1 GiB of split-K partials at most
-  if (ns > 1) ns = std::max<int64_t>(1, std::min<int64_t>(ns, ws_cap / (S * 8)));
-  int64_t len = (t + ns - 1) / ns;
-  len = (len + s.KC - 1) / s.KC * s.KC;
-  ns = (t + len - 1) / len;
-  s.nslices = (int)ns;
-  s.slice_len = len;
+  if (s.KC == 0 || t <= 0) return s;
+  s.nslices = (int)((t + bcg::kSliceLen - 1) / bcg::kSliceLen);
+  const int64_t S = p.S_out;
+  s.group = (int)std::max<int64_t>(1, std::min<int64_t>(s.nslices, kWsCap / std::max<int64_t>(1, S * 8)));
   return s;
 }
 
 size_t ws_bytes_for(const bcg::Plan &p, const Slicing &s) {
-  return s.nslices > 1 ? (size_t)s.nslices * (size_t)p.lay[p.m].offs.back() * sizeof(double) : 0;
+  return s.nslices > 1 ? (size_t)s.group * (size_t)p.S_out * sizeof(double) : 0;
 }
 
 int run_moment(const bcg::Plan &p, const double *x, int64_t t, int64_t ldx, double *out, void *ws,
@@ -119,32 +92,39 @@ int run_moment(const bcg::Plan &p, const double *x, int64_t t, int64_t ldx, doub
   a.col_rank = p.d_col_rank;
   a.col_olin = p.d_col_olin;
   a.col_size = p.d_col_size;
-  a.offs = p.d_offs;
+  a.offs = p.d_koff;
+  a.ones = p.fused ? 1 : 0;
   a.tiles = p.d_tiles;
   a.tile_kmin = p.d_tile_kmin;
   a.tile_kmax = p.d_tile_kmax;
   a.ntiles = (int)p.tiles.size();
   a.R = p.R;
   a.C = p.C;
-  a.nslices = sl.nslices;
+  a.nslices_total = sl.nslices;
   a.slice_len = sl.slice_len;
   a.out = out;
   a.ws = static_cast<double *>(ws);
-  a.S = p.lay[p.m].offs.back();
+  a.S = p.S_out;
   a.kmin_sel = (int32_t)k0;
   a.kmax_sel = k1 - 1 >= INT32_MAX ? INT32_MAX : (int32_t)(k1 - 1);
   if (k0 == 0 && k1 >= p.lay[p.m].K) a.kmax_sel = INT32_MAX;
-  const int64_t grid = (int64_t)a.ntiles * sl.nslices;
-  if (grid > INT32_MAX) return fail(BCG_EINVAL, "moment grid too large");
-  if (p.variant > 0)
-    CUDA_TRY(bcg::launch_moment_ws(a, p.variant, (int)grid, stream), "moment kernel");
-  else
-    CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream), "moment kernel");
-  bcg::g_launches++;
-  if (sl.nslices > 1) {
-    const auto &offs = p.lay[p.m].offs;
-    CUDA_TRY(bcg::launch_reduce_slices(a.ws, sl.nslices, a.S, offs[k0], offs[k1], out, stream), "split-K reduce");
+  const auto &offs = p.lay[p.m].offs;
+  const int64_t lo = p.fused ? 0 : offs[k0], hi = p.fused ? p.S_out : offs[k1];
+  for (int g0 = 0; g0 < sl.nslices; g0 += sl.group) {
+    a.slice0 = g0;
+    a.nslices = std::min(sl.group, sl.nslices - g0);
+    const int64_t grid = (int64_t)a.ntiles * a.nslices;
+    if (grid > INT32_MAX) return fail(BCG_EINVAL, "moment grid too large");
+    if (p.variant > 0)
+      CUDA_TRY(bcg::launch_moment_ws(a, p.variant, (int)grid, stream), "moment kernel");
+    else
+      CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream), "moment kernel");
     bcg::g_launches++;
+    if (sl.nslices > 1) {
+      CUDA_TRY(bcg::launch_reduce_slices(a.ws, a.nslices, a.S, lo, hi, out, stream),
+               "split-K reduce");
+      bcg::g_launches++;
+    }
   }
   return BCG_OK;
 }
@@ -188,35 +168,75 @@ int bcg_plan_create_host(int64_t n, int32_t m, int32_t b, bcg_plan **plan) {
   return BCG_OK;
 }
 
+int bcg_plan_create_fused(int64_t n, int32_t m, int32_t b, int32_t host_only, bcg_plan **plan) {
+  if (!plan) return fail(BCG_EINVAL, "plan pointer is NULL");
+  if (m < 2 || m > 16) return fail(BCG_EINVAL, "kernel supports 2 <= m <= 16");
+  auto pl = std::make_unique<bcg_plan>();
+  std::string err = bcg::build_plan(n, m, b, pl->p, 0, true);
+  if (!err.empty()) return fail(BCG_EINVAL, err);
+  if (!host_only) {
+    err = bcg::upload_plan(pl->p);
+    if (!err.empty()) {
+      bcg::free_plan(pl->p);
+      return fail(BCG_ECUDA, err);
+    }
+  }
+  *plan = pl.release();
+  return BCG_OK;
+}
+
+int bcg_plan_output(const bcg_plan *plan, int64_t *S_out, int64_t *order_base) {
+  if (!plan) return fail(BCG_EINVAL, "plan is NULL");
+  const bcg::Plan &p = plan->p;
+  if (S_out) *S_out = p.S_out;
+  if (order_base)
+    for (int o = 0; o <= p.m + 1; ++o)
+      order_base[o] = p.fused ? (o < (int)p.order_base.size() ? p.order_base[o] : 0) : (o == p.m + 1 ? p.S_out : 0);
+  return BCG_OK;
+}
+
 int bcg_plan_selfcheck(const bcg_plan *plan) {
   if (!plan) return fail(BCG_EINVAL, "plan is NULL");
   const bcg::Plan &p = plan->p;
   if (p.m < 2) return BCG_OK;
-  const bcg::Layout &L = p.lay[p.m];
-  const int64_t S = L.offs.back();
+  const int64_t S = p.S_out;
   std::vector<uint8_t> seen(S, 0);
   for (const bcg::Tile &tl : p.tiles) {
     for (int64_t r = tl.row0; r < std::min<int64_t>(tl.row0 + p.tm, p.R); ++r) {
       for (int64_t c = tl.col0; c < std::min<int64_t>(tl.col0 + p.tn, p.C); ++c) {
         if (c < p.row_cstart[r]) continue;
-        const int64_t k = p.row_keybase[r] + p.col_rank[c];
-        if (k < 0 || k >= L.K) return fail(BCG_EINVAL, "selfcheck: key index out of range");
+        const int64_t kg = p.row_keybase[r] + p.col_rank[c];
+        if (kg < 0 || kg >= (int64_t)p.koff.size()) return fail(BCG_EINVAL, "selfcheck: key index out of range");
+        if (p.koff[kg] < 0) continue;  // fused: order 0 / 1 element
         const int64_t lin = (int64_t)p.row_olin[r] * p.col_size[c] + p.col_olin[c];
-        const int64_t addr = L.offs[k] + lin;
-        if (addr >= L.offs[k + 1]) return fail(BCG_EINVAL, "selfcheck: offset outside block");
+        const int64_t addr = p.koff[kg] + lin;
+        // locate (order, block) of addr and check the element's data columns
+        int o = p.m;
+        if (p.fused)
+          while (o > 2 && addr < p.order_base[o]) --o;
+        const bcg::Layout &L = p.lay[o];
+        const int64_t local = addr - (p.fused ? p.order_base[o] : 0);
+        const int64_t k = std::upper_bound(L.offs.begin(), L.offs.end(), local) - L.offs.begin() - 1;
+        if (k < 0 || k >= L.K || local >= L.offs[k + 1]) return fail(BCG_EINVAL, "selfcheck: offset outside block");
+        if (p.koff[kg] != (p.fused ? p.order_base[o] : 0) + L.offs[k])
+          return fail(BCG_EINVAL, "selfcheck: element outside its key's block");
         if (seen[addr]) return fail(BCG_EINVAL, "selfcheck: element produced twice");
         seen[addr] = 1;
-        // the element's data columns must be those of (key, offsets)
-        int64_t rem = lin, cols[16];
-        for (int q = p.m - 1; q >= 0; --q) {
-          const int64_t e = L.edges[k * p.m + q];
-          cols[q] = L.col0[k * p.m + q] + rem % e;
+        int64_t rem = local - L.offs[k], cols[16];
+        for (int q = o - 1; q >= 0; --q) {
+          const int64_t e = L.edges[k * o + q];
+          cols[q] = L.col0[k * o + q] + rem % e;
           rem /= e;
         }
+        // the GEMM element's columns, ones (-1) removed, must equal (key, offsets)'s
+        int64_t got[16], ng = 0;
         for (int q = 0; q < p.h; ++q)
-          if (p.rowcols[r * p.h + q] != cols[q]) return fail(BCG_EINVAL, "selfcheck: row column mismatch");
+          if (p.rowcols[r * p.h + q] >= 0) got[ng++] = p.rowcols[r * p.h + q];
         for (int q = 0; q < p.r; ++q)
-          if (p.colcols[c * p.r + q] != cols[p.h + q]) return fail(BCG_EINVAL, "selfcheck: col column mismatch");
+          if (p.colcols[c * p.r + q] >= 0) got[ng++] = p.colcols[c * p.r + q];
+        if (ng != o) return fail(BCG_EINVAL, "selfcheck: order mismatch");
+        for (int q = 0; q < o; ++q)
+          if (got[q] != cols[q]) return fail(BCG_EINVAL, "selfcheck: column mismatch");
       }
     }
   }

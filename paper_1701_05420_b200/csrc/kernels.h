@@ -13,21 +13,27 @@ struct MomentArgs {
   int64_t t, ldx;
   int n, h, r;
   int bulk_ok;  // rows contiguous and 16-byte aligned: TMA bulk staging
+  int ones;     // fused multi-order plan: column -1 is the constant-ones column
   const int16_t *rowcols, *colcols;
   const int32_t *row_keybase, *row_olin, *row_cstart;
   const int32_t *col_rank, *col_olin, *col_size;
-  const int64_t *offs;
+  const int64_t *offs;  // per GEMM key: output offset of its block, -1 = not produced
   const Tile *tiles;
   const int32_t *tile_kmin, *tile_kmax;
   int ntiles;
   int64_t R, C;
-  int nslices;
+  int nslices;        // slices in this launch (group)
+  int slice0;         // first slice of the group
+  int nslices_total;  // slices over the whole sample range
   int64_t slice_len;
   double *out, *ws;
   int64_t S;
   int32_t kmin_sel, kmax_sel;
 };
 
+// fixed split-K slice length (samples): the summation order of every element
+// depends on t only (see moment.cu)
+constexpr int64_t kSliceLen = 16384;
 size_t moment_smem_bytes(int KC, int n);
 int pick_kc(int n);
 cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t stream);

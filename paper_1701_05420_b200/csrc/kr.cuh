@@ -5,16 +5,28 @@
 
 namespace bcg {
 
-template <int NQ>
+// ONES: column index -1 denotes the constant-ones column of a fused
+// multi-order plan (factor 1.0; no load).
+template <bool ONES>
+__device__ __forceinline__ double kr_val(const double *xr, int c) {
+  if constexpr (ONES) {
+    const double v = xr[c < 0 ? 0 : c];
+    return c < 0 ? 1.0 : v;
+  } else {
+    return xr[c];
+  }
+}
+
+template <int NQ, bool ONES = false>
 __device__ __forceinline__ double kr_prod(const double *xr, const int (&cols)[8], int nq) {
-  double p = xr[cols[0]];
+  double p = kr_val<ONES>(xr, cols[0]);
   if constexpr (NQ > 0) {
 #pragma unroll
-    for (int q = 1; q < NQ; ++q) p *= xr[cols[q]];
+    for (int q = 1; q < NQ; ++q) p *= kr_val<ONES>(xr, cols[q]);
   } else {
 #pragma unroll
     for (int q = 1; q < 8; ++q)
-      if (q < nq) p *= xr[cols[q]];
+      if (q < nq) p *= kr_val<ONES>(xr, cols[q]);
   }
   return p;
 }

@@ -19,8 +19,11 @@
 //   4. the epilogue scatters each accumulator to its packed address
 //      offs[keybase[row] + rank[col]] + olin[row] * size[col] + olin[col],
 //      either accumulating into `out` (one K-slice) or writing a per-slice
-//      partial that k_reduce_slices sums in fixed order (deterministic split-K,
-//      no float atomics).
+//      partial that k_reduce_slices adds in slice order (deterministic split-K,
+//      no float atomics).  Slices have a fixed length (kSliceLen samples), so
+//      every element's summation order depends on t only -- not on the plan,
+//      tile shape, key range or launch grouping: moments from different plans
+//      (block-split, kernel variants) agree bitwise.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -73,7 +76,7 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-template <int KC, int M>
+template <int KC, int M, bool ONES>
 __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
   constexpr int H = M / 2, R = M - M / 2;  // compile-time mode counts (0: runtime)
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -85,8 +88,9 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
 
   const int tid = threadIdx.x;
   const int unit = blockIdx.x;
-  const int slice = unit / a.ntiles;
-  const int tile_id = unit - slice * a.ntiles;
+  const int sl_local = unit / a.ntiles;  // slice within this launch's group
+  const int tile_id = unit - sl_local * a.ntiles;
+  const int slice = a.slice0 + sl_local;
   if (a.kmin_sel > 0 || a.kmax_sel < INT32_MAX) {
     if (a.tile_kmax[tile_id] < a.kmin_sel || a.tile_kmin[tile_id] > a.kmax_sel) return;
   }
@@ -157,13 +161,13 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
     double *wb = krb + (c & 1) * KC * (kTN + kPad) + kk0 * (kTN + kPad) + ki;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      BCG_CHECK(colA[q] >= 0 && colA[q] < n, "colA", colA[q]);
-      BCG_CHECK(colB[q] >= 0 && colB[q] < n, "colB", colB[q]);
+      BCG_CHECK(colA[q] >= (ONES ? -1 : 0) && colA[q] < n, "colA", colA[q]);
+      BCG_CHECK(colB[q] >= (ONES ? -1 : 0) && colB[q] < n, "colB", colB[q]);
     }
 #pragma unroll
     for (int k = 0; k < KC / 2; ++k) {
-      const double pa = kr_prod<H>(xr, colA, a.h);
-      const double pb = kr_prod<R>(xr, colB, a.r);
+      const double pa = kr_prod<H, ONES>(xr, colA, a.h);
+      const double pb = kr_prod<R, ONES>(xr, colB, a.r);
       wa[2 * k * (kTM + kPad)] = okA ? pa : 0.0;
       wb[2 * k * (kTN + kPad)] = okB ? pb : 0.0;
       xr += 2 * n;
@@ -207,8 +211,8 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
   }
 
   // ---- epilogue: scatter to packed addresses ----
-  double *dst = a.nslices == 1 ? a.out : a.ws + (int64_t)slice * a.S;
-  const bool accumulate = a.nslices == 1;
+  double *dst = a.nslices_total == 1 ? a.out : a.ws + (int64_t)sl_local * a.S;
+  const bool accumulate = a.nslices_total == 1;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int64_t row = (int64_t)tile.row0 + wm * 32 + 8 * i + gid;
@@ -222,7 +226,9 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
         if (col >= a.C || col < cs) continue;
         const int32_t key = kb0 + a.col_rank[col];
         if (key < a.kmin_sel || key > a.kmax_sel) continue;
-        const int64_t addr = a.offs[key] + (int64_t)ro * a.col_size[col] + a.col_olin[col];
+        const int64_t base = a.offs[key];  // output offset of the key's block
+        if (base < 0) continue;            // fused plan: orders 0 / 1 are not produced
+        const int64_t addr = base + (int64_t)ro * a.col_size[col] + a.col_olin[col];
         BCG_CHECK(addr >= 0 && addr < a.S, "epilogue address", addr);
         BCG_CHECK(key >= 0, "key", key);
         if (accumulate)
@@ -234,14 +240,16 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
   }
 }
 
-// out[i] += sum_s ws[s * S + i]  for i in [lo, hi), slices summed in order.
+// out[i] = ((out[i] + ws[0][i]) + ws[1][i]) + ...  for i in [lo, hi): the
+// slices of one group added sequentially, so the association of the whole
+// split-K sum is the same for any grouping of the slices.
 __global__ void k_reduce_slices(const double *__restrict__ ws, int nslices, int64_t S, int64_t lo,
                                 int64_t hi, double *__restrict__ out) {
   for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi;
        i += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < nslices; ++k) s += ws[k * S + i];
-    out[i] += s;
+    double v = out[i];
+    for (int k = 0; k < nslices; ++k) v += ws[k * S + i];
+    out[i] = v;
   }
 }
 
@@ -261,9 +269,10 @@ int pick_kc(int n) {
 template <int KC, int M>
 static cudaError_t go_v1(const MomentArgs &args, int grid, cudaStream_t stream) {
   const size_t smem = moment_smem_bytes(KC, args.n);
-  cudaError_t e = cudaFuncSetAttribute(k_moment_dmma<KC, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = args.ones ? k_moment_dmma<KC, M, true> : k_moment_dmma<KC, M, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_moment_dmma<KC, M><<<grid, kThreads, smem, stream>>>(args);
+  kern<<<grid, kThreads, smem, stream>>>(args);
   return cudaGetLastError();
 }
 

@@ -96,8 +96,9 @@ __global__ void __launch_bounds__(WsShape<TM, TN, WM, WN, KC, NPROD, NXS, NKS>::
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int unit = blockIdx.x;
-  const int slice = unit / a.ntiles;
-  const int tile_id = unit - slice * a.ntiles;
+  const int sl_local = unit / a.ntiles;  // slice within this launch's group
+  const int tile_id = unit - sl_local * a.ntiles;
+  const int slice = a.slice0 + sl_local;
   if (a.kmin_sel > 0 || a.kmax_sel < INT32_MAX) {
     if (a.tile_kmax[tile_id] < a.kmin_sel || a.tile_kmin[tile_id] > a.kmax_sel) return;
   }
@@ -241,8 +242,8 @@ __global__ void __launch_bounds__(WsShape<TM, TN, WM, WN, KC, NPROD, NXS, NKS>::
       if (lane == 0) bar_arrive(&k_empty[sk]);
     }
     // epilogue: scatter to packed addresses
-    double *dst = a.nslices == 1 ? a.out : a.ws + (int64_t)slice * a.S;
-    const bool accumulate = a.nslices == 1;
+    double *dst = a.nslices_total == 1 ? a.out : a.ws + (int64_t)sl_local * a.S;
+    const bool accumulate = a.nslices_total == 1;
 #pragma unroll
     for (int i = 0; i < S::MT; ++i) {
       const int64_t row = (int64_t)tile.row0 + wm * WM + 8 * i + gid;
@@ -256,7 +257,9 @@ __global__ void __launch_bounds__(WsShape<TM, TN, WM, WN, KC, NPROD, NXS, NKS>::
           if (col >= a.C || col < cs) continue;
           const int32_t key = kb0 + a.col_rank[col];
           if (key < a.kmin_sel || key > a.kmax_sel) continue;
-          const int64_t addr = a.offs[key] + (int64_t)ro * a.col_size[col] + a.col_olin[col];
+          const int64_t base = a.offs[key];
+          if (base < 0) continue;
+          const int64_t addr = base + (int64_t)ro * a.col_size[col] + a.col_olin[col];
           if (accumulate)
             dst[addr] += acc[i][j][e];
           else

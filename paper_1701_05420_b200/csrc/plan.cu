@@ -108,8 +108,9 @@ int default_variant() {
   return 0;
 }
 
-std::string build_plan(int64_t n, int m, int b, Plan &p, int variant) {
+std::string build_plan(int64_t n, int m, int b, Plan &p, int variant, bool fused) {
   if (n < 1 || m < 1 || b < 1) return "n, m and b must all be >= 1";
+  p.fused = fused;
   p.variant = variant < 0 ? default_variant() : variant;
   ws_tile_shape(p.variant, &p.tm, &p.tn);
   if (m > 16) return "kernel supports 2 <= m <= 16";
@@ -125,14 +126,59 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant) {
   if (LM.K > INT32_MAX) return "too many blocks";
   if (m < 2) return "";
 
-  // ---- moment GEMM tables: rows = left h-tuples grouped by last entry ----
+  // ---- moment GEMM tables over a block alphabet ----
+  // Unfused: symbols 1..nbar are the data blocks.  Fused (single pass over all
+  // orders 2..m): symbol 1 is a "ones" block (edge 1, constant column), symbols
+  // 2..nbar+1 are the data blocks; a key with z ones is the order-(m - z) key
+  // of its remaining entries, so one staircase GEMM yields M_2..M_m.
+  std::vector<int64_t> sym_edge, sym_col0;  // 1-based
+  const int64_t N = p.fused ? p.nbar + 1 : p.nbar;
+  sym_edge.assign(N + 1, 0);
+  sym_col0.assign(N + 1, 0);
+  for (int64_t sidx = 1; sidx <= N; ++sidx) {
+    const int64_t j = p.fused ? sidx - 1 : sidx;  // data block, 0 = ones
+    sym_edge[sidx] = j == 0 ? 1 : edge_of(j, n, b);
+    sym_col0[sidx] = j == 0 ? -1 : (j - 1) * b;
+  }
+  // target offset of every GEMM key (m-tuple of symbols, lexicographic)
+  {
+    std::vector<int64_t> keys;
+    enum_sorted(N, m, keys);
+    const int64_t KG = (int64_t)keys.size() / m;
+    p.koff.assign(KG, -1);
+    p.order_base.assign(m + 2, 0);
+    if (p.fused) {
+      int64_t base = 0;
+      for (int o = 2; o <= m; ++o) {
+        p.order_base[o] = base;
+        base += p.lay[o].offs.back();
+      }
+      p.order_base[m + 1] = base;
+      p.S_out = base;
+    } else {
+      p.S_out = LM.offs.back();
+    }
+    for (int64_t k = 0; k < KG; ++k) {
+      const int64_t *key = &keys[k * m];
+      if (!p.fused) {
+        p.koff[k] = LM.offs[k];
+        continue;
+      }
+      int z = 0;
+      while (z < m && key[z] == 1) ++z;
+      const int o = m - z;
+      if (o < 2) continue;  // orders 0 and 1 are not produced
+      int64_t sub[16];
+      for (int q = 0; q < o; ++q) sub[q] = key[z + q] - 1;  // data block j
+      p.koff[k] = p.order_base[o] + p.lay[o].offs[multiset_rank(sub, o, p.nbar)];
+    }
+  }
   p.h = m / 2;
   p.r = m - p.h;
   const int h = p.h, r = p.r;
-  const int64_t nbar = p.nbar;
   std::vector<int64_t> lt, rt;
-  enum_sorted(nbar, h, lt);
-  enum_sorted(nbar, r, rt);
+  enum_sorted(N, h, lt);
+  enum_sorted(N, r, rt);
   const int64_t NL = (int64_t)lt.size() / h, NR = (int64_t)rt.size() / r;
   std::vector<int64_t> lorder(NL);
   std::iota(lorder.begin(), lorder.end(), 0);
@@ -144,7 +190,7 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant) {
   std::vector<int64_t> rstart(NR + 1, 0);
   for (int64_t i = 0; i < NR; ++i) {
     int64_t sz = 1;
-    for (int q = 0; q < r; ++q) sz *= edge_of(rt[i * r + q], n, b);
+    for (int q = 0; q < r; ++q) sz *= sym_edge[rt[i * r + q]];
     rstart[i + 1] = rstart[i] + sz;
   }
   p.C = rstart[NR];
@@ -155,12 +201,13 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant) {
   for (int64_t i = 0; i < NR; ++i) {
     const int64_t *R = &rt[i * r];
     int64_t e[16];
-    for (int q = 0; q < r; ++q) e[q] = edge_of(R[q], n, b);
+    for (int q = 0; q < r; ++q) e[q] = sym_edge[R[q]];
     int64_t sz = rstart[i + 1] - rstart[i];
     for (int64_t o = 0; o < sz; ++o) {
       int64_t c = rstart[i] + o, rem = o;
       for (int q = r - 1; q >= 0; --q) {
-        p.colcols[c * r + q] = (int16_t)((R[q] - 1) * b + rem % e[q]);
+        const int64_t c0 = sym_col0[R[q]];
+        p.colcols[c * r + q] = (int16_t)(c0 < 0 ? -1 : c0 + rem % e[q]);
         rem /= e[q];
       }
       p.col_rank[c] = (int32_t)i;
@@ -169,10 +216,10 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant) {
     }
   }
   // first column of the suffix {R : R[0] >= v}; (v, ..., v) is its first tuple
-  std::vector<int64_t> cstart_v(nbar + 2, p.C), rank_first_v(nbar + 2, NR);
-  for (int64_t v = 1; v <= nbar; ++v) {
+  std::vector<int64_t> cstart_v(N + 2, p.C), rank_first_v(N + 2, NR);
+  for (int64_t v = 1; v <= N; ++v) {
     std::vector<int64_t> vv(r, v);
-    int64_t rk = multiset_rank(vv.data(), r, nbar);
+    int64_t rk = multiset_rank(vv.data(), r, N);
     rank_first_v[v] = rk;
     cstart_v[v] = rstart[rk];
   }
@@ -180,7 +227,7 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant) {
   p.R = 0;
   for (int64_t i = 0; i < NL; ++i) {
     int64_t sz = 1;
-    for (int q = 0; q < h; ++q) sz *= edge_of(lt[lorder[i] * h + q], n, b);
+    for (int q = 0; q < h; ++q) sz *= sym_edge[lt[lorder[i] * h + q]];
     p.R += sz;
   }
   p.rowcols.resize(p.R * h);
@@ -194,13 +241,14 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant) {
     int64_t full[16], e[16];
     for (int q = 0; q < h; ++q) full[q] = L[q];
     for (int q = h; q < m; ++q) full[q] = v;
-    const int64_t kbase = multiset_rank(full, m, nbar) - rank_first_v[v];
+    const int64_t kbase = multiset_rank(full, m, N) - rank_first_v[v];
     int64_t sz = 1;
-    for (int q = 0; q < h; ++q) sz *= (e[q] = edge_of(L[q], n, b));
+    for (int q = 0; q < h; ++q) sz *= (e[q] = sym_edge[L[q]]);
     for (int64_t o = 0; o < sz; ++o, ++row) {
       int64_t rem = o;
       for (int q = h - 1; q >= 0; --q) {
-        p.rowcols[row * h + q] = (int16_t)((L[q] - 1) * b + rem % e[q]);
+        const int64_t c0 = sym_col0[L[q]];
+        p.rowcols[row * h + q] = (int16_t)(c0 < 0 ? -1 : c0 + rem % e[q]);
         rem /= e[q];
       }
       p.row_keybase[row] = (int32_t)kbase;
@@ -210,7 +258,7 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant) {
   }
   if (p.R > INT32_MAX || p.C > INT32_MAX) return "GEMM dimension overflow";
 
-  // staircase tiles
+  // staircase tiles (tiles whose elements all map to orders < 2 are dropped)
   p.tiles.clear();
   p.tile_kmin.clear();
   p.tile_kmax.clear();
@@ -219,13 +267,17 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant) {
     for (int64_t c0 = p.row_cstart[r0]; c0 < p.C; c0 += p.tn) {
       const int64_t c1 = std::min<int64_t>(c0 + p.tn, p.C);
       int64_t kmin = INT64_MAX, kmax = -1;
+      bool live = false;
       for (int64_t rr = r0; rr < r1; ++rr) {
         int64_t cs = std::max<int64_t>(c0, p.row_cstart[rr]);
         if (cs >= c1) continue;
-        kmin = std::min<int64_t>(kmin, p.row_keybase[rr] + p.col_rank[cs]);
-        kmax = std::max<int64_t>(kmax, p.row_keybase[rr] + p.col_rank[c1 - 1]);
+        const int64_t klo = p.row_keybase[rr] + p.col_rank[cs];
+        const int64_t khi = p.row_keybase[rr] + p.col_rank[c1 - 1];
+        kmin = std::min<int64_t>(kmin, klo);
+        kmax = std::max<int64_t>(kmax, khi);
+        for (int64_t kk = klo; kk <= khi && !live; ++kk) live = p.koff[kk] >= 0;
       }
-      if (kmax < 0) continue;  // tile entirely below the staircase
+      if (kmax < 0 || !live) continue;  // below the staircase / only orders 0, 1
       p.tiles.push_back(Tile{(int32_t)r0, (int32_t)c0});
       p.tile_kmin.push_back((int32_t)kmin);
       p.tile_kmax.push_back((int32_t)kmax);
@@ -264,7 +316,7 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant) {
         int64_t sub[16];
         int len = 0;
         for (int q : slot_modes[s]) sub[len++] = key[q];
-        p.sub_rank[(size_t)k * p.nslots + s] = (int32_t)multiset_rank(sub, len, nbar);
+        p.sub_rank[(size_t)k * p.nslots + s] = (int32_t)multiset_rank(sub, len, p.nbar);
       }
     }
   }
@@ -295,6 +347,7 @@ std::string upload_plan(Plan &p) {
   UP(d_tile_kmax, tile_kmax);
   UP(d_sub_rank, sub_rank);
   UP(d_part_mask, part_mask);
+  UP(d_koff, koff);
 #undef UP
   if (e == cudaSuccess) e = up(&p.d_offs, p.lay[p.m].offs);
   if (e == cudaSuccess && p.m >= 1) {
@@ -309,7 +362,7 @@ std::string upload_plan(Plan &p) {
 void free_plan(Plan &p) {
   void *ptrs[] = {p.d_rowcols, p.d_colcols, p.d_row_keybase, p.d_row_olin, p.d_row_cstart,
                   p.d_col_rank, p.d_col_olin, p.d_col_size, p.d_offs, p.d_tiles, p.d_tile_kmin, p.d_tile_kmax,
-                  p.d_keys32, p.d_sub_rank, p.d_part_mask};
+                  p.d_keys32, p.d_sub_rank, p.d_part_mask, p.d_koff};
   for (void *q : ptrs)
     if (q) cudaFree(q);
   for (auto &q : p.d_lower_offs)

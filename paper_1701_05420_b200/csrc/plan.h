@@ -27,6 +27,7 @@ struct Tile {
 struct Plan {
   int64_t n = 0;
   int variant = 0;          // moment kernel: 0 = v1 (64x64), >0 = warp-specialized shape
+  bool fused = false;       // one GEMM for all orders 2..m (ones block), output concatenated
   int tm = kTM, tn = kTN;   // CTA tile of the staircase GEMM
   int m = 0, b = 0;
   int64_t nbar = 0;
@@ -43,6 +44,9 @@ struct Plan {
   std::vector<int32_t> col_rank;        // lexicographic rank of R among r-tuples
   std::vector<int32_t> col_olin;        // within-block offset of R's modes
   std::vector<int32_t> col_size;        // |R| = prod edges(R)
+  std::vector<int64_t> koff;           // GEMM key -> output offset of its block (-1: not produced)
+  std::vector<int64_t> order_base;     // fused: order o's packed buffer starts at order_base[o]
+  int64_t S_out = 0;                   // output elements (S_m, or S_2 + ... + S_m fused)
   std::vector<Tile> tiles;
   std::vector<int32_t> tile_kmin, tile_kmax;  // key range a tile touches
 
@@ -66,11 +70,12 @@ struct Plan {
   int32_t *d_keys32 = nullptr;          // K_m x m keys (1-based)
   int32_t *d_sub_rank = nullptr;
   int32_t *d_part_mask = nullptr;
+  int64_t *d_koff = nullptr;
   int64_t *d_lower_offs[16] = {nullptr};  // offs of orders 2..m-2
 };
 
 // Builders (plan.cu).
-std::string build_plan(int64_t n, int m, int b, Plan &p, int variant = -1);
+std::string build_plan(int64_t n, int m, int b, Plan &p, int variant = -1, bool fused = false);
 int default_variant();
 std::string upload_plan(Plan &p);
 void free_plan(Plan &p);
