@@ -159,6 +159,21 @@ int bcg_cumulant_recursion_range(const bcg_plan *plan, double *mk,
                                  const double *const *lower, int64_t k0,
                                  int64_t k1, void *stream);
 
+/* Same, with the central moments of the complements: cmom[j] = packed
+ * central moment M_{j+2} (device) for j = 2 .. m-4 (orders 4 .. m-2; entries
+ * for orders 2, 3 are ignored: M_2 = C_2, M_3 = C_3).  Full blocks then use
+ * the factored, register-blocked kernel
+ *   C_m = M_m - sum_{S containing mode 1, 2 <= |S| <= m-2} C_|S|[S] M_{m-|S|}[rest]
+ * (algebraically the reference's partition sum grouped by the part holding
+ * mode 1; 25 products per element at m = 6 instead of 55), for 4 <= m <= 6
+ * and b <= 8; other blocks / orders fall back to the partition kernel.  Only
+ * blocks [k0, k1) are written.  bcg_cumulant_recursion(_range) use the
+ * factored kernel for m <= 5 (no central moments needed). */
+int bcg_cumulant_recursion_ex(const bcg_plan *plan, double *mk,
+                              const double *const *lower,
+                              const double *const *cmom, int64_t k0,
+                              int64_t k1, void *stream);
+
 /* Same correction without the moment: out = B_sigma (bc/cumulants.py:53-84,
  * `outer_prod_cum(m, sigma, lower)`), out has S_m elements. */
 int bcg_outer_prod_cum(const bcg_plan *plan, int32_t sigma,

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -395,7 +396,7 @@ int bcg_moment_blocks(const double *xt, int64_t n, int64_t t, const int64_t *col
 }
 
 static int recursion_common(const bcg_plan *plan, double *mk, const double *const *lower, int mode, int sigma_lo,
-                            int sigma_hi, int64_t k0, int64_t k1, cudaStream_t s) {
+                            int sigma_hi, int64_t k0, int64_t k1, cudaStream_t s, const int32_t *klist = nullptr) {
   const bcg::Plan &p = plan->p;
   if (!p.d_offs) return fail(BCG_EINVAL, "host-only plan");
   bcg::RecursionArgs a{};
@@ -428,23 +429,67 @@ static int recursion_common(const bcg_plan *plan, double *mk, const double *cons
   a.mode = mode;
   a.k0 = std::max<int64_t>(0, k0);
   a.k1 = std::min<int64_t>(a.K, k1);
+  a.klist = klist;
   if ((size_t)p.nslots * 8 > 200 * 1024) return fail(BCG_EINVAL, "cumulant order too high for the recursion kernel");
   CUDA_TRY(bcg::launch_recursion(a, s), "recursion kernel");
   return BCG_OK;
 }
 
+// Recursion dispatcher: the factored register-blocked kernel (recursion_fact.cu)
+// for full blocks when the plan supports it and the central moments it needs
+// are given; the partition-table kernel (recursion.cu) for everything else.
+static int recursion_dispatch(const bcg_plan *plan, double *mk, const double *const *lower,
+                              const double *const *cmom, int64_t k0, int64_t k1, cudaStream_t s) {
+  const bcg::Plan &p = plan->p;
+  if (p.m <= 3) return BCG_OK;
+  if (!p.d_offs) return fail(BCG_EINVAL, "host-only plan");
+  const int m = p.m;
+  k0 = std::max<int64_t>(0, k0);
+  k1 = std::min<int64_t>(p.lay[m].K, k1);
+  if (k1 <= k0) return BCG_OK;
+  static const bool force_partition = getenv("BCG_RECURSION_PARTITION") != nullptr;  // A/B knob
+  bool fact = p.fact_terms > 0 && lower && !force_partition;
+  for (int k = 4; fact && k <= m - 2; ++k) fact = cmom && cmom[k - 2];
+  if (!fact) return recursion_common(plan, mk, lower, 0, 2, m / 2, k0, k1, s);
+  for (int k = 2; k <= m - 2; ++k)
+    if (!lower[k - 2]) return fail(BCG_EINVAL, "missing lower cumulant of order " + std::to_string(k));
+  bcg::RecFactArgs a{};
+  a.offs = p.d_offs;
+  a.term_off = p.d_term_off;
+  for (int k = 2; k <= m - 2; ++k) {
+    a.cum[k] = lower[k - 2];
+    if (k >= 4) a.cmom[k] = cmom[k - 2];
+  }
+  a.mk = mk;
+  auto lo_f = std::lower_bound(p.full_keys.begin(), p.full_keys.end(), (int32_t)k0) - p.full_keys.begin();
+  auto hi_f = std::lower_bound(p.full_keys.begin(), p.full_keys.end(), (int32_t)k1) - p.full_keys.begin();
+  a.keys = p.d_full_keys + lo_f;
+  a.nkeys = hi_f - lo_f;
+  if (a.nkeys > 0) CUDA_TRY(bcg::launch_recursion_fact(a, m, p.b, s), "factored recursion kernel");
+  auto lo_p = std::lower_bound(p.partial_keys.begin(), p.partial_keys.end(), (int32_t)k0) - p.partial_keys.begin();
+  auto hi_p = std::lower_bound(p.partial_keys.begin(), p.partial_keys.end(), (int32_t)k1) - p.partial_keys.begin();
+  if (hi_p > lo_p) {
+    // partial-edge blocks: partition kernel over the explicit key list
+    return recursion_common(plan, mk, lower, 0, 2, m / 2, 0, hi_p - lo_p, s, p.d_partial_keys + lo_p);
+  }
+  return BCG_OK;
+}
+
 int bcg_cumulant_recursion(const bcg_plan *plan, double *mk, const double *const *lower, void *stream) {
   if (!plan) return fail(BCG_EINVAL, "plan is NULL");
-  if (plan->p.m <= 3) return BCG_OK;
-  return recursion_common(plan, mk, lower, 0, 2, plan->p.m / 2, 0, plan->p.lay[plan->p.m].K,
-                          static_cast<cudaStream_t>(stream));
+  return recursion_dispatch(plan, mk, lower, nullptr, 0, plan->p.lay[plan->p.m].K, static_cast<cudaStream_t>(stream));
 }
 
 int bcg_cumulant_recursion_range(const bcg_plan *plan, double *mk, const double *const *lower, int64_t k0,
                                  int64_t k1, void *stream) {
   if (!plan) return fail(BCG_EINVAL, "plan is NULL");
-  if (plan->p.m <= 3) return BCG_OK;
-  return recursion_common(plan, mk, lower, 0, 2, plan->p.m / 2, k0, k1, static_cast<cudaStream_t>(stream));
+  return recursion_dispatch(plan, mk, lower, nullptr, k0, k1, static_cast<cudaStream_t>(stream));
+}
+
+int bcg_cumulant_recursion_ex(const bcg_plan *plan, double *mk, const double *const *lower,
+                              const double *const *cmom, int64_t k0, int64_t k1, void *stream) {
+  if (!plan) return fail(BCG_EINVAL, "plan is NULL");
+  return recursion_dispatch(plan, mk, lower, cmom, k0, k1, static_cast<cudaStream_t>(stream));
 }
 
 int bcg_outer_prod_cum(const bcg_plan *plan, int32_t sigma, const double *const *lower, double *out, void *stream) {

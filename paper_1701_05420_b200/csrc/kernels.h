@@ -65,6 +65,7 @@ struct RecursionArgs {
   int nslots;
   int p_begin, p_end;       // partitions [p_begin, p_end) processed
   int64_t k0, k1;           // output blocks [k0, k1) processed
+  const int32_t *klist;     // if non-null: process klist[0 .. k1-k0) instead of the range
   int sigma_lo, sigma_hi;   // sigma range (for grouping into B_sigma)
   int sigma_first[12];       // sigma -> first partition (host copy)
   const int64_t *lower_offs[16];
@@ -73,6 +74,19 @@ struct RecursionArgs {
   int mode;                 // 0: mk = mk - sum_sigma B_sigma ; 1: mk = B_sigma (single sigma)
 };
 cudaError_t launch_recursion(const RecursionArgs &args, cudaStream_t stream);
+
+struct RecFactArgs {
+  const int32_t *keys;      // full output blocks to process (indices into the order-m layout)
+  int64_t nkeys;
+  const int64_t *offs;      // order-m block offsets
+  const int64_t *term_off;  // [K][nterms][2] element offsets of each term's factor blocks
+  const double *cum[16];    // packed C_k, k = 2 .. m-2
+  const double *cmom[16];   // packed central moments M_k, k = 4 .. m-2
+  double *mk;               // in: M_m, out: C_m
+};
+int recursion_fact_terms(int m);
+bool recursion_fact_supported(int m, int b);
+cudaError_t launch_recursion_fact(const RecFactArgs &a, int m, int b, cudaStream_t stream);
 
 extern int64_t g_launches;
 

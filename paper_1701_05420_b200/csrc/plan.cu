@@ -102,6 +102,8 @@ std::vector<std::vector<std::vector<int>>> partitions_min2(int m, int sigma) {
   return out;
 }
 
+static void build_fact_tables(Plan &p);
+
 int default_variant() {
   const char *env = std::getenv("BCG_MOMENT_VARIANT");
   if (env && *env) return std::atoi(env);
@@ -319,8 +321,48 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant, bool fused
         p.sub_rank[(size_t)k * p.nslots + s] = (int32_t)multiset_rank(sub, len, p.nbar);
       }
     }
+    build_fact_tables(p);
   }
   return "";
+}
+
+// factored-recursion tables (recursion_fact.cu): for every order-m key and
+// every subset S of modes containing mode 0 with 2 <= |S| <= m-2 (in mask
+// order, matching rf::term_mask), the element offsets of the factor blocks
+// C_|S|[key|S] and M_{m-|S|}[key|rest] in their packed buffers.
+static void build_fact_tables(Plan &p) {
+  const int m = p.m;
+  p.fact_terms = 0;
+  p.term_off.clear();
+  p.full_keys.clear();
+  p.partial_keys.clear();
+  const Layout &LM = p.lay[m];
+  for (int64_t k = 0; k < LM.K; ++k) {
+    bool full = true;
+    for (int q = 0; q < m; ++q) full = full && LM.edges[k * m + q] == p.b;
+    (full ? p.full_keys : p.partial_keys).push_back((int32_t)k);
+  }
+  if (!recursion_fact_supported(m, p.b)) return;
+  std::vector<int> masks;
+  for (int s = 1; s < (1 << m); s += 2) {
+    const int c = __builtin_popcount(s);
+    if (c >= 2 && c <= m - 2) masks.push_back(s);
+  }
+  p.fact_terms = (int)masks.size();
+  p.term_off.resize((size_t)LM.K * masks.size() * 2);
+  for (int64_t k = 0; k < LM.K; ++k) {
+    const int64_t *key = &LM.keys[k * m];
+    for (size_t t = 0; t < masks.size(); ++t) {
+      int64_t a[16], c[16];
+      int na = 0, nc = 0;
+      for (int q = 0; q < m; ++q) {
+        if (masks[t] & (1 << q)) a[na++] = key[q];
+        else c[nc++] = key[q];
+      }
+      p.term_off[(k * masks.size() + t) * 2] = p.lay[na].offs[multiset_rank(a, na, p.nbar)];
+      p.term_off[(k * masks.size() + t) * 2 + 1] = p.lay[nc].offs[multiset_rank(c, nc, p.nbar)];
+    }
+  }
 }
 
 template <typename T>
@@ -348,6 +390,9 @@ std::string upload_plan(Plan &p) {
   UP(d_sub_rank, sub_rank);
   UP(d_part_mask, part_mask);
   UP(d_koff, koff);
+  UP(d_term_off, term_off);
+  UP(d_full_keys, full_keys);
+  UP(d_partial_keys, partial_keys);
 #undef UP
   if (e == cudaSuccess) e = up(&p.d_offs, p.lay[p.m].offs);
   if (e == cudaSuccess && p.m >= 1) {
@@ -362,7 +407,8 @@ std::string upload_plan(Plan &p) {
 void free_plan(Plan &p) {
   void *ptrs[] = {p.d_rowcols, p.d_colcols, p.d_row_keybase, p.d_row_olin, p.d_row_cstart,
                   p.d_col_rank, p.d_col_olin, p.d_col_size, p.d_offs, p.d_tiles, p.d_tile_kmin, p.d_tile_kmax,
-                  p.d_keys32, p.d_sub_rank, p.d_part_mask, p.d_koff};
+                  p.d_keys32, p.d_sub_rank, p.d_part_mask, p.d_koff, p.d_term_off,
+                  p.d_full_keys, p.d_partial_keys};
   for (void *q : ptrs)
     if (q) cudaFree(q);
   for (auto &q : p.d_lower_offs)

@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) k_recursion(RecursionArgs a) {
   int64_t *slot_base = reinterpret_cast<int64_t *>(smem_raw);  // nslots
   __shared__ int edges[16];
   const int m = a.m;
-  const int64_t k = a.k0 + blockIdx.x;
+  const int64_t k = a.klist ? (int64_t)a.klist[blockIdx.x] : a.k0 + blockIdx.x;
   const int tid = threadIdx.x;
   const int32_t *key = a.keys + k * m;
   if (tid < m) {

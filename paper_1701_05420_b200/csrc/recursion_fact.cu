@@ -1,0 +1,190 @@
+// K3 (v2): cumulant recursion at memory rate, for full blocks (all edges = b).
+//
+// Uses the moment-cumulant relation of centered data expanded by the part
+// that contains mode 1 (PAPER.md:650-666 restated by subsets):
+//
+//   M(1..m) = sum_{S containing 1} C(S) * M(rest),   M(empty) = 1, M(single) = 0
+//   =>  C_m = M_m - sum_{S containing 1, 2 <= |S| <= m-2} C_|S|[key|S] * M_{m-|S|}[key|rest]
+//
+// which is algebraically the reference's partition sum (bc/cumulants.py:53-136:
+// grouping the partitions by the part holding mode 1 turns the sum over the
+// other parts into the central moment of the complement).  m = 6: 25 products
+// instead of 40 partitions / 55 multiplications.  M_2 = C_2 and M_3 = C_3; the
+// central moments M_4.. of the complement are kept by the caller.
+//
+// Every sub-key of a sorted key is sorted, so each factor is an element of a
+// stored lower-order block (bc/cumulants.py:9-12); the host precomputes the
+// element offset of each term's two factor blocks per output block.
+//
+// Register blocking: a thread owns one trailing index of the output block and
+// the B^(m-CT) elements sharing it in registers.  The term list, the factor
+// strides and the row offsets are compile-time (template on m and B), so every
+// factor access is a per-thread base plus an immediate offset; lanes cover
+// consecutive elements, so M_m is read and C_m written coalesced (HBM-bound:
+// 16 bytes per element).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <utility>
+
+#include "kernels.h"
+
+namespace bcg {
+
+namespace rf {
+
+__host__ __device__ constexpr int popc(int x) { return x == 0 ? 0 : (x & 1) + popc(x >> 1); }
+__host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+
+// terms: subsets S of {0..M-1} containing mode 0, 2 <= |S| <= M-2, by mask order
+__host__ __device__ constexpr int term_count(int M) {
+  int c = 0;
+  for (int s = 1; s < (1 << M); s += 2)
+    if (popc(s) >= 2 && popc(s) <= M - 2) ++c;
+  return c;
+}
+__host__ __device__ constexpr int term_mask(int M, int t) {
+  for (int s = 1; s < (1 << M); s += 2)
+    if (popc(s) >= 2 && popc(s) <= M - 2) {
+      if (t == 0) return s;
+      --t;
+    }
+  return 0;
+}
+// row-major stride of mode q inside the factor block over the modes in `mask`
+__host__ __device__ constexpr int stride_in(int mask, int q, int B) {
+  int later = 0;
+  for (int p = q + 1; p < 16; ++p)
+    if (mask & (1 << p)) ++later;
+  return ipow(B, later);
+}
+// compile-time offset contributed by the leading (register row) modes
+// 0..M-CT-1 for row index `row` (row-major)
+__host__ __device__ constexpr int head_offset(int mask, int M, int CT, int B, int row) {
+  int off = 0;
+  for (int q = M - CT - 1; q >= 0; --q) {
+    const int digit = row % B;
+    row /= B;
+    if (mask & (1 << q)) off += digit * stride_in(mask, q, B);
+  }
+  return off;
+}
+
+}  // namespace rf
+
+// Thread <-> (output block, trailing index c): the block is viewed as ROWS x W
+// with the leading M-CT modes as rows and the trailing CT modes as columns.
+// Lanes take consecutive columns (coalesced M_m / C_m traffic; factor loads are
+// broadcast or contiguous across the warp), each thread keeps its ROWS
+// elements in registers, and the row offsets into every factor are
+// compile-time immediates.
+template <int M, int B, int CT, int T>
+__device__ __forceinline__ void apply_term(double (&acc)[rf::ipow(B, M - CT)], const int (&dig)[M],
+                                           const RecFactArgs &a, const int64_t *toff) {
+  constexpr int S = rf::term_mask(M, T);
+  constexpr int FULL = (1 << M) - 1;
+  constexpr int REST = FULL & ~S;
+  constexpr int s = rf::popc(S), r = M - s;
+  constexpr int ROWS = rf::ipow(B, M - CT);
+  // runtime part: the thread's trailing digits
+  int o1 = 0, o2 = 0;
+#pragma unroll
+  for (int q = M - CT; q < M; ++q) {
+    if (S & (1 << q)) o1 += dig[q] * rf::stride_in(S, q, B);
+    if (REST & (1 << q)) o2 += dig[q] * rf::stride_in(REST, q, B);
+  }
+  const double *f1 = a.cum[s] + toff[2 * T] + o1;
+  const double *f2 = (r <= 3 ? a.cum[r] : a.cmom[r]) + toff[2 * T + 1] + o2;
+#pragma unroll
+  for (int row = 0; row < ROWS; ++row) {
+    const double u = __ldg(f1 + rf::head_offset(S, M, CT, B, row));
+    const double v = __ldg(f2 + rf::head_offset(REST, M, CT, B, row));
+    acc[row] = fma(-u, v, acc[row]);
+  }
+}
+
+template <int M, int B, int CT, int... Ts>
+__device__ __forceinline__ void apply_terms(double (&acc)[rf::ipow(B, M - CT)], const int (&dig)[M],
+                                            const RecFactArgs &a, const int64_t *toff,
+                                            std::integer_sequence<int, Ts...>) {
+  (apply_term<M, B, CT, Ts>(acc, dig, a, toff), ...);
+}
+
+template <int M, int B, int CT>
+__global__ void __launch_bounds__(256) k_recursion_fact(RecFactArgs a) {
+  constexpr int NT = rf::term_count(M);
+  constexpr int ROWS = rf::ipow(B, M - CT);  // elements per thread (registers)
+  constexpr int W = rf::ipow(B, CT);         // threads per block
+  const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t kb = item / W;
+  if (kb >= a.nkeys) return;
+  const int c = (int)(item - kb * W);
+  const int32_t key = a.keys[kb];
+  const int64_t *toff = a.term_off + (int64_t)key * 2 * NT;
+  int dig[M];
+#pragma unroll
+  for (int q = 0; q < M; ++q) dig[q] = 0;
+  {
+    int rem = c;
+#pragma unroll
+    for (int q = M - 1; q >= M - CT; --q) {
+      dig[q] = rem % B;
+      rem /= B;
+    }
+  }
+  double *blk = a.mk + a.offs[key] + c;
+  double acc[ROWS];
+#pragma unroll
+  for (int row = 0; row < ROWS; ++row) acc[row] = blk[(int64_t)row * W];
+  apply_terms<M, B, CT>(acc, dig, a, toff, std::make_integer_sequence<int, NT>{});
+#pragma unroll
+  for (int row = 0; row < ROWS; ++row) blk[(int64_t)row * W] = acc[row];
+}
+
+// trailing (thread) modes: the fewest that leave <= 32 register rows
+__host__ __device__ constexpr int ct_for(int M, int B) {
+  int c = 0;
+  while (c < M && rf::ipow(B, M - c) > 32) ++c;
+  return c;
+}
+
+template <int M, int B>
+static cudaError_t go_fact(const RecFactArgs &a, cudaStream_t stream) {
+  constexpr int CT = ct_for(M, B);
+  constexpr int W = rf::ipow(B, CT);
+  const int64_t items = a.nkeys * W;
+  const int threads = 256;
+  const int64_t blocks = (items + threads - 1) / threads;
+  if (blocks <= 0) return cudaSuccess;
+  k_recursion_fact<M, B, CT><<<(unsigned)blocks, threads, 0, stream>>>(a);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+int recursion_fact_terms(int m) { return rf::term_count(m); }
+
+bool recursion_fact_supported(int m, int b) { return m >= 4 && m <= 6 && b >= 1 && b <= 8; }
+
+cudaError_t launch_recursion_fact(const RecFactArgs &a, int m, int b, cudaStream_t stream) {
+#define RF_B(M)                                    \
+  switch (b) {                                     \
+    case 1: return go_fact<M, 1>(a, stream);       \
+    case 2: return go_fact<M, 2>(a, stream);       \
+    case 3: return go_fact<M, 3>(a, stream);       \
+    case 4: return go_fact<M, 4>(a, stream);       \
+    case 5: return go_fact<M, 5>(a, stream);       \
+    case 6: return go_fact<M, 6>(a, stream);       \
+    case 7: return go_fact<M, 7>(a, stream);       \
+    case 8: return go_fact<M, 8>(a, stream);       \
+    default: return cudaErrorInvalidValue;         \
+  }
+  switch (m) {
+    case 4: RF_B(4)
+    case 5: RF_B(5)
+    case 6: RF_B(6)
+    default: return cudaErrorInvalidValue;
+  }
+#undef RF_B
+}
+
+}  // namespace bcg

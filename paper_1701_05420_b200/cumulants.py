@@ -97,13 +97,21 @@ def outer_prod_cum(m: int, sigma: int, lower: Sequence[BlockSymTensor],
     return BlockSymTensor(n, m, b, data=out)
 
 
-def _recursion_inplace(result: BlockSymTensor, lower: Sequence[BlockSymTensor]) -> None:
+def _recursion_inplace(result: BlockSymTensor, lower: Sequence[BlockSymTensor],
+                       central: dict | None = None) -> None:
+    """C_m in place on the packed M_m.  ``central`` (order -> packed central
+    moment tensor, orders 4..m-2) enables the factored kernel at m = 6."""
     m, n, b = result.m, result.n, result.b
     by_order = _lower_by_order(lower, range(2, m - 1))
     plan = _native.plan(n, m, b)
     arr, keep = _lower_array(by_order, m, n, b)
-    _native.check(_native.lib().bcg_cumulant_recursion(plan.handle, result.data.data_ptr(), arr,
-                                                       _native.stream_handle()), "cumulant recursion")
+    cm = (ctypes.c_void_p * 15)()
+    for k, t in (central or {}).items():
+        if 4 <= k <= m - 2:
+            cm[k - 2] = t.data_ptr()
+    _native.check(_native.lib().bcg_cumulant_recursion_ex(
+        plan.handle, result.data.data_ptr(), arr, cm, 0, layout(n, m, b).K,
+        _native.stream_handle()), "cumulant recursion")
     del keep
 
 
@@ -171,6 +179,7 @@ def cumulants_device(X, m_max: int, b: int, c1_host: bool = True, timer: dict | 
     if m_max >= 2:
         Xc = _center_device(X, st["mean"])
         _check_centered(Xc)
+        central: dict = {}  # central moments M_4.. kept for the factored recursion
         for k in range(2, m_max + 1):
             if timer is not None and k == m_max:
                 torch = _native.torch_cuda()
@@ -179,8 +188,10 @@ def cumulants_device(X, m_max: int, b: int, c1_host: bool = True, timer: dict | 
                 Mk = _moment_device(Xc, k, b, events=ev)
             else:
                 Mk = _moment_device(Xc, k, b)
+            if 4 <= k <= m_max - 2:
+                central[k] = Mk.data.clone()
             if k >= 4:
-                _recursion_inplace(Mk, tensors)
+                _recursion_inplace(Mk, tensors, central)
             tensors.append(Mk)
     c1 = st["mean"].cpu().numpy() if c1_host else st["mean"]
     return c1, tensors
