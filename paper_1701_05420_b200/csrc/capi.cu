@@ -60,13 +60,22 @@ Slicing choose_slicing(const bcg::Plan &p, int64_t t) {
   if (p.variant > 0) s.KC = 16;
   if (s.KC == 0 || t <= 0) return s;
   s.nslices = (int)((t + bcg::kSliceLen - 1) / bcg::kSliceLen);
+  // slices per launch: as many as the workspace cap allows (fewest launches,
+  // no small tail launch), balanced across launches; a plan with enough tiles
+  // to fill the GPU by itself (>= 8 waves) runs one slice per launch and
+  // accumulates straight into `out` (no workspace, no reduce pass).
+  const int64_t ntiles = std::max<int64_t>(1, (int64_t)p.tiles.size());
   const int64_t S = p.S_out;
-  s.group = (int)std::max<int64_t>(1, std::min<int64_t>(s.nslices, kWsCap / std::max<int64_t>(1, S * 8)));
+  int64_t cap = kWsCap / std::max<int64_t>(1, S * 8);
+  if (ntiles >= 8 * 148 * 4) cap = 1;
+  cap = std::max<int64_t>(1, std::min<int64_t>(cap, s.nslices));
+  const int64_t ngroups = (s.nslices + cap - 1) / cap;
+  s.group = (int)((s.nslices + ngroups - 1) / ngroups);
   return s;
 }
 
 size_t ws_bytes_for(const bcg::Plan &p, const Slicing &s) {
-  return s.nslices > 1 ? (size_t)s.group * (size_t)p.S_out * sizeof(double) : 0;
+  return s.group > 1 ? (size_t)s.group * (size_t)p.S_out * sizeof(double) : 0;
 }
 
 int run_moment(const bcg::Plan &p, const double *x, int64_t t, int64_t ldx, double *out, void *ws,
@@ -121,7 +130,7 @@ int run_moment(const bcg::Plan &p, const double *x, int64_t t, int64_t ldx, doub
     else
       CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream), "moment kernel");
     bcg::g_launches++;
-    if (sl.nslices > 1) {
+    if (a.nslices > 1) {
       CUDA_TRY(bcg::launch_reduce_slices(a.ws, a.nslices, a.S, lo, hi, out, stream),
                "split-K reduce");
       bcg::g_launches++;

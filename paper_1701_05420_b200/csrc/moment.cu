@@ -211,8 +211,8 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
   }
 
   // ---- epilogue: scatter to packed addresses ----
-  double *dst = a.nslices_total == 1 ? a.out : a.ws + (int64_t)sl_local * a.S;
-  const bool accumulate = a.nslices_total == 1;
+  double *dst = a.nslices == 1 ? a.out : a.ws + (int64_t)sl_local * a.S;
+  const bool accumulate = a.nslices == 1;  // group of one slice: out += partial, in slice order
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int64_t row = (int64_t)tile.row0 + wm * 32 + 8 * i + gid;

@@ -242,8 +242,8 @@ __global__ void __launch_bounds__(WsShape<TM, TN, WM, WN, KC, NPROD, NXS, NKS>::
       if (lane == 0) bar_arrive(&k_empty[sk]);
     }
     // epilogue: scatter to packed addresses
-    double *dst = a.nslices_total == 1 ? a.out : a.ws + (int64_t)sl_local * a.S;
-    const bool accumulate = a.nslices_total == 1;
+    double *dst = a.nslices == 1 ? a.out : a.ws + (int64_t)sl_local * a.S;
+    const bool accumulate = a.nslices == 1;  // group of one slice: out += partial, in slice order
 #pragma unroll
     for (int i = 0; i < S::MT; ++i) {
       const int64_t row = (int64_t)tile.row0 + wm * WM + 8 * i + gid;
