@@ -84,6 +84,10 @@ int bcg_plan_create_ex(int64_t n, int32_t m, int32_t b, int32_t variant,
  * (bcg_plan_output).  host_only != 0: tables only (layout / selfcheck). */
 int bcg_plan_create_fused(int64_t n, int32_t m, int32_t b, int32_t host_only,
                           bcg_plan **plan);
+/* Moment-kernel choice of the plan: variant (0 = v1), CTA tile tm x tn
+ * (picked per plan by the staircase tile model) and the number of tiles. */
+int bcg_plan_kernel(const bcg_plan *plan, int32_t *variant, int32_t *tm,
+                    int32_t *tn, int64_t *ntiles);
 /* Output size of bcg_moment_raw on this plan (S_m, or S_2 + ... + S_m for a
  * fused plan) and, if order_base != NULL (m + 2 entries), each order's start
  * offset in it (fused plans; zeros otherwise, order_base[m + 1] = S_out). */

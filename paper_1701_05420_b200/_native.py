@@ -35,6 +35,8 @@ SIGNATURES = [
     ("bcg_plan_create_ex", ctypes.c_int, [_i64, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
     ("bcg_plan_create_fused", ctypes.c_int, [_i64, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
     ("bcg_plan_output", ctypes.c_int, [_vp, ctypes.POINTER(_i64), _vp]),
+    ("bcg_plan_kernel", ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
+                                       ctypes.POINTER(_i64)]),
     ("bcg_plan_create_host", ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(_vp)]),
     ("bcg_plan_destroy", ctypes.c_int, [_vp]),
     ("bcg_plan_selfcheck", ctypes.c_int, [_vp]),
@@ -158,6 +160,13 @@ class Plan:
         check(self._lib.bcg_plan_output(self._h, ctypes.byref(S), base.ctypes.data))
         return S.value, base
 
+    def kernel(self):
+        """(variant, tm, tn, ntiles) of the moment GEMM this plan launches."""
+        v, tm, tn, nt = _i32(), _i32(), _i32(), _i64()
+        check(self._lib.bcg_plan_kernel(self._h, ctypes.byref(v), ctypes.byref(tm), ctypes.byref(tn),
+                                        ctypes.byref(nt)))
+        return v.value, tm.value, tn.value, nt.value
+
     def ws_bytes(self, t: int) -> int:
         out = _sz()
         check(self._lib.bcg_moment_ws_bytes(self._h, int(t), ctypes.byref(out)))
@@ -185,7 +194,8 @@ def moment_variant() -> int:
 def plan(n: int, m: int, b: int, fused: bool = False) -> Plan:
     """Cached device plan for (n, m, b), the current kernel variant and
     whether it is the fused multi-order plan."""
-    key = (int(n), int(m), int(b), -1 if fused else moment_variant(), bool(fused))
+    key = (int(n), int(m), int(b), -1 if fused else moment_variant(), bool(fused),
+           os.environ.get("BCG_TILE", ""))
     with _lock:
         p = _plans.get(key)
         if p is None:

@@ -57,7 +57,7 @@ constexpr int64_t kWsCap = (int64_t)2 << 30;  // 2 GiB of split-K partials at mo
 
 Slicing choose_slicing(const bcg::Plan &p, int64_t t) {
   Slicing s{bcg::pick_kc((int)p.n), 1, 1, bcg::kSliceLen};
-  if (p.variant > 0) s.KC = 16;
+  if (p.variant > 0 || !(p.tm == 64 && p.tn == 64)) s.KC = 16;
   if (s.KC == 0 || t <= 0) return s;
   s.nslices = (int)((t + bcg::kSliceLen - 1) / bcg::kSliceLen);
   // slices per launch: as many as the workspace cap allows (fewest launches,
@@ -128,7 +128,7 @@ int run_moment(const bcg::Plan &p, const double *x, int64_t t, int64_t ldx, doub
     if (p.variant > 0)
       CUDA_TRY(bcg::launch_moment_ws(a, p.variant, (int)grid, stream), "moment kernel");
     else
-      CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream), "moment kernel");
+      CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream, p.tm, p.tn), "moment kernel");
     bcg::g_launches++;
     if (a.nslices > 1) {
       CUDA_TRY(bcg::launch_reduce_slices(a.ws, a.nslices, a.S, lo, hi, out, stream),
@@ -192,6 +192,15 @@ int bcg_plan_create_fused(int64_t n, int32_t m, int32_t b, int32_t host_only, bc
     }
   }
   *plan = pl.release();
+  return BCG_OK;
+}
+
+int bcg_plan_kernel(const bcg_plan *plan, int32_t *variant, int32_t *tm, int32_t *tn, int64_t *ntiles) {
+  if (!plan) return fail(BCG_EINVAL, "plan is NULL");
+  if (variant) *variant = plan->p.variant;
+  if (tm) *tm = plan->p.tm;
+  if (tn) *tn = plan->p.tn;
+  if (ntiles) *ntiles = (int64_t)plan->p.tiles.size();
   return BCG_OK;
 }
 

@@ -34,9 +34,10 @@ struct MomentArgs {
 // fixed split-K slice length (samples): the summation order of every element
 // depends on t only (see moment.cu)
 constexpr int64_t kSliceLen = 16384;
-size_t moment_smem_bytes(int KC, int n);
+size_t moment_smem_bytes(int KC, int n, int tm = 64, int tn = 64);
 int pick_kc(int n);
-cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t stream);
+bool v1_shape_supported(int KC, int m, int tm, int tn);
+cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t stream, int tm = 64, int tn = 64);
 cudaError_t launch_moment_ws(const MomentArgs &args, int variant, int grid, cudaStream_t stream,
                              int *blocks_per_sm = nullptr);
 void ws_tile_shape(int variant, int *tm, int *tn);

@@ -76,15 +76,35 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-template <int KC, int M, bool ONES>
+// CTA tile TM x TN, 4 warps in a WGM x WGN grid (warp tile WM x WN of 8x8
+// DMMA sub-tiles).  Khatri-Rao work split: TM rows x KC samples of A and
+// TN columns x KC samples of B over 128 threads, each thread a fixed row
+// (column) and an interleaved set of samples, so its X column indices stay in
+// registers.
+template <int TM, int TN>
+struct V1Shape {
+  static constexpr int WGN = TN >= 4 * TM ? 4 : (TN >= TM ? 2 : 1);
+  static constexpr int WGM = 4 / WGN;
+  static constexpr int WM = TM / WGM, WN = TN / WGN;
+  static constexpr int MT = WM / 8, NT = WN / 8;
+  static constexpr int LDA = TM + kPad, LDB = TN + kPad;
+  static_assert(WM % 8 == 0 && WN % 8 == 0, "warp tile must be a multiple of 8");
+  static_assert(kThreads % TM == 0 && kThreads % TN == 0, "TM, TN must divide 128");
+};
+
+template <int KC, int M, bool ONES, int TM, int TN>
 __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
+  using SH = V1Shape<TM, TN>;
   constexpr int H = M / 2, R = M - M / 2;  // compile-time mode counts (0: runtime)
+  constexpr int LDA = SH::LDA, LDB = SH::LDB, MT = SH::MT, NT = SH::NT;
+  constexpr int PA = kThreads / TM, PB = kThreads / TN;  // sample phases per row / col
+  static_assert(KC % PA == 0 && KC % PB == 0, "KC must be a multiple of the sample phases");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int n = a.n;
-  double *xs = reinterpret_cast<double *>(smem_raw);                   // [2][KC*n]
-  double *kra = xs + 2 * KC * n;                                       // [2][KC][TM+pad]
-  double *krb = kra + 2 * KC * (kTM + kPad);                           // [2][KC][TN+pad]
-  uint64_t *bar = reinterpret_cast<uint64_t *>(krb + 2 * KC * (kTN + kPad));
+  double *xs = reinterpret_cast<double *>(smem_raw);   // [2][KC*n]
+  double *kra = xs + 2 * KC * n;                       // [2][KC][LDA]
+  double *krb = kra + 2 * KC * LDA;                    // [2][KC][LDB]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(krb + 2 * KC * LDB);
 
   const int tid = threadIdx.x;
   const int unit = blockIdx.x;
@@ -100,12 +120,12 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
   const int64_t slen = send - sbeg;
   const int nch = (int)((slen + KC - 1) / KC);
 
-  // ---- per-thread Khatri-Rao assignment: one row (A) and one col (B), KC/2 samples each ----
-  const int ki = tid & 63;       // row / col within the tile
-  const int kk0 = tid >> 6;      // sample phase 0..1
+  // ---- per-thread Khatri-Rao assignment ----
+  const int ia = tid % TM, pa0 = tid / TM;  // A row, first sample phase (step PA)
+  const int ib = tid % TN, pb0 = tid / TN;  // B col, first sample phase (step PB)
   int colA[8], colB[8];
-  const int64_t grow = (int64_t)tile.row0 + ki;
-  const int64_t gcol = (int64_t)tile.col0 + ki;
+  const int64_t grow = (int64_t)tile.row0 + ia;
+  const int64_t gcol = (int64_t)tile.col0 + ib;
   const bool okA = grow < a.R, okB = gcol < a.C;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
@@ -129,12 +149,12 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
 
   const int warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;
-  double acc[4][4][2];
+  const int wm = warp % SH::WGM, wn = warp / SH::WGM;
+  double acc[MT][NT][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   // Software pipeline, one CTA barrier per chunk: while the warps issue the
   // DMMAs of chunk c they also build the Khatri-Rao factors of chunk c+1 into
@@ -156,21 +176,31 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
     }
   };
   auto build = [&](int c) {  // Khatri-Rao factors of chunk c -> kra/krb[c & 1]
-    const double *xr = xs + (c & 1) * KC * n + kk0 * n;
-    double *wa = kra + (c & 1) * KC * (kTM + kPad) + kk0 * (kTM + kPad) + ki;
-    double *wb = krb + (c & 1) * KC * (kTN + kPad) + kk0 * (kTN + kPad) + ki;
+    const double *xst = xs + (c & 1) * KC * n;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       BCG_CHECK(colA[q] >= (ONES ? -1 : 0) && colA[q] < n, "colA", colA[q]);
       BCG_CHECK(colB[q] >= (ONES ? -1 : 0) && colB[q] < n, "colB", colB[q]);
     }
+    {
+      double *wa = kra + (c & 1) * KC * LDA + pa0 * LDA + ia;
+      const double *xr = xst + pa0 * n;
 #pragma unroll
-    for (int k = 0; k < KC / 2; ++k) {
-      const double pa = kr_prod<H, ONES>(xr, colA, a.h);
-      const double pb = kr_prod<R, ONES>(xr, colB, a.r);
-      wa[2 * k * (kTM + kPad)] = okA ? pa : 0.0;
-      wb[2 * k * (kTN + kPad)] = okB ? pb : 0.0;
-      xr += 2 * n;
+      for (int k = 0; k < KC / PA; ++k) {
+        const double p = kr_prod<H, ONES>(xr, colA, a.h);
+        wa[k * PA * LDA] = okA ? p : 0.0;
+        xr += PA * n;
+      }
+    }
+    {
+      double *wb = krb + (c & 1) * KC * LDB + pb0 * LDB + ib;
+      const double *xr = xst + pb0 * n;
+#pragma unroll
+      for (int k = 0; k < KC / PB; ++k) {
+        const double p = kr_prod<R, ONES>(xr, colB, a.r);
+        wb[k * PB * LDB] = okB ? p : 0.0;
+        xr += PB * n;
+      }
     }
   };
 
@@ -190,21 +220,21 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
       build(c + 1);
     }
     // ---- DMMA over chunk c ----
-    const double *ka = kra + (c & 1) * KC * (kTM + kPad);
-    const double *kb = krb + (c & 1) * KC * (kTN + kPad);
+    const double *ka = kra + (c & 1) * KC * LDA;
+    const double *kb = krb + (c & 1) * KC * LDB;
 #pragma unroll
     for (int k = 0; k < KC; k += 4) {
-      double fa[4], fb[4];
-      const double *pa = ka + (k + tig) * (kTM + kPad) + wm * 32 + gid;
-      const double *pb = kb + (k + tig) * (kTN + kPad) + wn * 32 + gid;
+      double fa[MT], fb[NT];
+      const double *pa = ka + (k + tig) * LDA + wm * SH::WM + gid;
+      const double *pb = kb + (k + tig) * LDB + wn * SH::WN + gid;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) fa[i] = pa[8 * i];
+      for (int i = 0; i < MT; ++i) fa[i] = pa[8 * i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) fb[j] = pb[8 * j];
+      for (int j = 0; j < NT; ++j) fb[j] = pb[8 * j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(acc[i][j], fa[i], fb[j]);
+        for (int j = 0; j < NT; ++j) dmma884(acc[i][j], fa[i], fb[j]);
     }
     __syncthreads();  // KR[c+1] complete, KR[c] and xs[(c+1) & 1] free
     if (tid == 0 && c + 3 < nch && chunk_full(c + 3)) issue(c + 3);
@@ -214,15 +244,15 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
   double *dst = a.nslices == 1 ? a.out : a.ws + (int64_t)sl_local * a.S;
   const bool accumulate = a.nslices == 1;  // group of one slice: out += partial, in slice order
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t row = (int64_t)tile.row0 + wm * 32 + 8 * i + gid;
+  for (int i = 0; i < MT; ++i) {
+    const int64_t row = (int64_t)tile.row0 + wm * SH::WM + 8 * i + gid;
     if (row >= a.R) continue;
     const int32_t kb0 = a.row_keybase[row], ro = a.row_olin[row], cs = a.row_cstart[row];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NT; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int64_t col = (int64_t)tile.col0 + wn * 32 + 8 * j + 2 * tig + e;
+        const int64_t col = (int64_t)tile.col0 + wn * SH::WN + 8 * j + 2 * tig + e;
         if (col >= a.C || col < cs) continue;
         const int32_t key = kb0 + a.col_rank[col];
         if (key < a.kmin_sel || key > a.kmax_sel) continue;
@@ -253,12 +283,12 @@ __global__ void k_reduce_slices(const double *__restrict__ ws, int nslices, int6
   }
 }
 
-size_t moment_smem_bytes(int KC, int n) {
-  return sizeof(double) * (2 * (size_t)KC * n + 2 * (size_t)KC * (kTM + kPad) + 2 * (size_t)KC * (kTN + kPad)) +
+size_t moment_smem_bytes(int KC, int n, int tm, int tn) {
+  return sizeof(double) * (2 * (size_t)KC * n + 2 * (size_t)KC * (tm + kPad) + 2 * (size_t)KC * (tn + kPad)) +
          2 * sizeof(uint64_t);
 }
 
-int pick_kc(int n) {
+int pick_kc(int n) {  // sample-chunk length for the 64x64 tile
   // keep the double-buffered sample stage <= 96 KB so >= 2 CTAs fit per SM
   if (2 * 16 * (size_t)n * 8 <= 96 * 1024) return 16;
   if (2 * 8 * (size_t)n * 8 <= 96 * 1024) return 8;
@@ -266,23 +296,59 @@ int pick_kc(int n) {
   return 0;
 }
 
-template <int KC, int M>
+template <int KC, int M, int TM, int TN>
 static cudaError_t go_v1(const MomentArgs &args, int grid, cudaStream_t stream) {
-  const size_t smem = moment_smem_bytes(KC, args.n);
-  auto kern = args.ones ? k_moment_dmma<KC, M, true> : k_moment_dmma<KC, M, false>;
+  const size_t smem = moment_smem_bytes(KC, args.n, TM, TN);
+  auto kern = args.ones ? k_moment_dmma<KC, M, true, TM, TN> : k_moment_dmma<KC, M, false, TM, TN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, kThreads, smem, stream>>>(args);
   return cudaGetLastError();
 }
 
-cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t stream) {
+// v1 tile shapes: 64x64 for every KC / order; the thin / small shapes
+// (staircase-friendly, chosen per plan by the tile model) for KC = 16 and
+// orders 2..8.
+bool v1_shape_supported(int KC, int m, int tm, int tn) {
+  if (tm == 64 && tn == 64) return true;
+  if (KC != 16 || m < 2 || m > 8) return false;
+  return (tm == 16 && tn == 128) || (tm == 128 && tn == 16) || (tm == 32 && tn == 64) ||
+         (tm == 64 && tn == 32) || (tm == 32 && tn == 32);
+}
+
+cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t stream, int tm, int tn) {
   static const bool generic = getenv("BCG_FORCE_GENERIC_M") != nullptr;  // debug knob
   const int m = generic ? 0 : args.h + args.r;
   cudaError_t e = cudaErrorInvalidValue;
-#define GO16(M, ...) e = go_v1<16, M>(args, grid, stream)
-#define GO8(M, ...) e = go_v1<8, M>(args, grid, stream)
-#define GO4(M, ...) e = go_v1<4, M>(args, grid, stream)
+  if (!(tm == 64 && tn == 64)) {
+    if (!v1_shape_supported(KC, m, tm, tn)) return cudaErrorInvalidValue;
+#define GOS(M, TMV, TNV) e = go_v1<16, M, TMV, TNV>(args, grid, stream)
+#define SHAPE(TMV, TNV)                                   \
+  if (tm == TMV && tn == TNV) {                           \
+    switch (m) {                                          \
+      case 2: GOS(2, TMV, TNV); break;                    \
+      case 3: GOS(3, TMV, TNV); break;                    \
+      case 4: GOS(4, TMV, TNV); break;                    \
+      case 5: GOS(5, TMV, TNV); break;                    \
+      case 6: GOS(6, TMV, TNV); break;                    \
+      case 7: GOS(7, TMV, TNV); break;                    \
+      case 8: GOS(8, TMV, TNV); break;                    \
+      default: break;                                     \
+    }                                                     \
+    return e;                                             \
+  }
+    SHAPE(16, 128)
+    SHAPE(128, 16)
+    SHAPE(32, 64)
+    SHAPE(64, 32)
+    SHAPE(32, 32)
+#undef SHAPE
+#undef GOS
+    return e;
+  }
+#define GO16(M, ...) e = go_v1<16, M, 64, 64>(args, grid, stream)
+#define GO8(M, ...) e = go_v1<8, M, 64, 64>(args, grid, stream)
+#define GO4(M, ...) e = go_v1<4, M, 64, 64>(args, grid, stream)
   switch (KC) {
     case 16: BCG_DISPATCH_M(m, GO16, 0) break;
     case 8: BCG_DISPATCH_M(m, GO8, 0) break;

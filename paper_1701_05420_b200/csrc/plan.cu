@@ -8,6 +8,7 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <functional>
 #include <numeric>
@@ -108,6 +109,76 @@ int default_variant() {
   const char *env = std::getenv("BCG_MOMENT_VARIANT");
   if (env && *env) return std::atoi(env);
   return 0;
+}
+
+// Staircase tile list for a tm x tn CTA tile (tiles whose elements all map to
+// orders < 2 are dropped).  Returns the number of useful elements covered.
+static int64_t build_tiles(const Plan &p, int tm, int tn, std::vector<Tile> *tiles, std::vector<int32_t> *kmin_out,
+                           std::vector<int32_t> *kmax_out) {
+  if (tiles) tiles->clear();
+  if (kmin_out) kmin_out->clear();
+  if (kmax_out) kmax_out->clear();
+  int64_t ntiles = 0;
+  for (int64_t r0 = 0; r0 < p.R; r0 += tm) {
+    const int64_t r1 = std::min<int64_t>(r0 + tm, p.R);
+    for (int64_t c0 = p.row_cstart[r0]; c0 < p.C; c0 += tn) {
+      const int64_t c1 = std::min<int64_t>(c0 + tn, p.C);
+      int64_t kmin = INT64_MAX, kmax = -1;
+      bool live = false;
+      for (int64_t rr = r0; rr < r1; ++rr) {
+        int64_t cs = std::max<int64_t>(c0, p.row_cstart[rr]);
+        if (cs >= c1) continue;
+        const int64_t klo = p.row_keybase[rr] + p.col_rank[cs];
+        const int64_t khi = p.row_keybase[rr] + p.col_rank[c1 - 1];
+        kmin = std::min<int64_t>(kmin, klo);
+        kmax = std::max<int64_t>(kmax, khi);
+        for (int64_t kk = klo; kk <= khi && !live; ++kk) live = p.koff[kk] >= 0;
+      }
+      if (kmax < 0 || !live) continue;  // below the staircase / only orders 0, 1
+      ++ntiles;
+      if (tiles) tiles->push_back(Tile{(int32_t)r0, (int32_t)c0});
+      if (kmin_out) kmin_out->push_back((int32_t)kmin);
+      if (kmax_out) kmax_out->push_back((int32_t)kmax);
+    }
+  }
+  return ntiles;
+}
+
+// Modeled cost per useful FMA of a v1 tile shape: tiled area / useful area
+// (staircase waste) x (1 + 10 * Khatri-Rao products per FMA).  The weight of
+// a KR product (its X loads, DMULs on the shared FP64 pipe, the smem store,
+// ~10 FMA-equivalents) and the negligible effect of fragment-load pressure
+// are fitted to the shape sweep in profiles/r01_tile_shapes.log.
+static double v1_shape_cost(const Plan &p, int tm, int tn, int64_t useful) {
+  const int64_t ntiles = build_tiles(p, tm, tn, nullptr, nullptr, nullptr);
+  const double waste = (double)ntiles * tm * tn / (double)std::max<int64_t>(1, useful);
+  const double kr = 1.0 / tn + 1.0 / tm;
+  return waste * (1.0 + 10.0 * kr);
+}
+
+static void choose_v1_shape(Plan &p) {
+  p.tm = 64;
+  p.tn = 64;
+  const char *env = std::getenv("BCG_TILE");
+  int etm = 0, etn = 0;
+  if (env && std::sscanf(env, "%dx%d", &etm, &etn) == 2 && v1_shape_supported(pick_kc((int)p.n), p.m, etm, etn)) {
+    p.tm = etm;
+    p.tn = etn;
+    return;
+  }
+  if (pick_kc((int)p.n) != 16 || p.m < 2 || p.m > 8) return;
+  int64_t useful = 0;
+  for (int64_t r = 0; r < p.R; ++r) useful += p.C - p.row_cstart[r];
+  static const int shapes[][2] = {{64, 64}, {16, 128}, {128, 16}, {32, 64}, {64, 32}, {32, 32}};
+  double best = v1_shape_cost(p, 64, 64, useful);
+  for (const auto &sh : shapes) {
+    const double c = v1_shape_cost(p, sh[0], sh[1], useful);
+    if (c < best * 0.97) {  // switch only for a clear modeled gain
+      best = c;
+      p.tm = sh[0];
+      p.tn = sh[1];
+    }
+  }
 }
 
 std::string build_plan(int64_t n, int m, int b, Plan &p, int variant, bool fused) {
@@ -260,31 +331,9 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant, bool fused
   }
   if (p.R > INT32_MAX || p.C > INT32_MAX) return "GEMM dimension overflow";
 
-  // staircase tiles (tiles whose elements all map to orders < 2 are dropped)
-  p.tiles.clear();
-  p.tile_kmin.clear();
-  p.tile_kmax.clear();
-  for (int64_t r0 = 0; r0 < p.R; r0 += p.tm) {
-    const int64_t r1 = std::min<int64_t>(r0 + p.tm, p.R);
-    for (int64_t c0 = p.row_cstart[r0]; c0 < p.C; c0 += p.tn) {
-      const int64_t c1 = std::min<int64_t>(c0 + p.tn, p.C);
-      int64_t kmin = INT64_MAX, kmax = -1;
-      bool live = false;
-      for (int64_t rr = r0; rr < r1; ++rr) {
-        int64_t cs = std::max<int64_t>(c0, p.row_cstart[rr]);
-        if (cs >= c1) continue;
-        const int64_t klo = p.row_keybase[rr] + p.col_rank[cs];
-        const int64_t khi = p.row_keybase[rr] + p.col_rank[c1 - 1];
-        kmin = std::min<int64_t>(kmin, klo);
-        kmax = std::max<int64_t>(kmax, khi);
-        for (int64_t kk = klo; kk <= khi && !live; ++kk) live = p.koff[kk] >= 0;
-      }
-      if (kmax < 0 || !live) continue;  // below the staircase / only orders 0, 1
-      p.tiles.push_back(Tile{(int32_t)r0, (int32_t)c0});
-      p.tile_kmin.push_back((int32_t)kmin);
-      p.tile_kmax.push_back((int32_t)kmax);
-    }
-  }
+  // staircase tiles; v1 plans pick the CTA tile shape by the tile model
+  if (p.variant == 0) choose_v1_shape(p);
+  build_tiles(p, p.tm, p.tn, &p.tiles, &p.tile_kmin, &p.tile_kmax);
 
   // ---- recursion tables ----
   p.part_mask.clear();

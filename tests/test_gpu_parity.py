@@ -409,3 +409,19 @@ def test_factored_recursion_matches_partition_sum(n, m, b, t, rng, monkeypatch):
     _, want = orc.cumulants_upto(x, m, b)
     for k in range(2, m + 1):
         np.testing.assert_allclose(packed(fact[k]), want[k], rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("tile", ["64x64", "16x128", "128x16", "32x64", "64x32", "32x32"])
+def test_v1_tile_shapes_match_oracle_and_each_other(tile, monkeypatch, rng):
+    """Every v1 CTA tile shape (BCG_TILE override of the plan's model choice)
+    gives the oracle's moments and bitwise-identical results."""
+    x = rng.standard_normal((20000, 13))
+    monkeypatch.setenv("BCG_TILE", "64x64")
+    ref = {m: packed(bcg.moment(x, m, 2)) for m in (2, 3, 4, 5)}
+    monkeypatch.setenv("BCG_TILE", tile)
+    for m in (2, 3, 4, 5):
+        got = packed(bcg.moment(x, m, 2))
+        np.testing.assert_array_equal(got, ref[m])
+    for n, m, b, t in [(7, 4, 3, 1003), (13, 5, 2, 517), (9, 6, 2, 211), (30, 3, 4, 333)]:
+        x2 = rng.standard_normal((t, n))
+        np.testing.assert_allclose(packed(bcg.moment(x2, m, b)), orc.moment(x2, m, b), rtol=1e-12, atol=1e-14)
