@@ -36,13 +36,13 @@ def build(force: bool = False, verbose: bool = False, checks: bool = False) -> s
     """Compile the sources in parallel (one nvcc per .cu) and link libbcgpu.so.
     ``checks`` builds libbcgpu_checks.so with device bounds checks
     (-DBCG_CHECKS); select it at run time with BCG_LIB=checks."""
-    out = DEBUG_LIB if checks else LIB
+    out = DEBUG_LIB if checks else os.environ.get("BCG_BUILD_OUT", LIB)
     if not force and not checks and not _stale():
         return out
     from concurrent.futures import ThreadPoolExecutor
 
     nvcc = os.environ.get("NVCC", "nvcc")
-    extra = ["-DBCG_CHECKS"] if checks else []
+    extra = (["-DBCG_CHECKS"] if checks else []) + os.environ.get("BCG_NVCC_EXTRA", "").split()
     tag = "chk" if checks else "rel"
 
     def compile_one(src):

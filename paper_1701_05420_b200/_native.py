@@ -17,7 +17,9 @@ from .errors import NativeUnavailableError, ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # BCG_LIB=checks selects the bounds-checked debug build (_build.py --checks)
-LIB_PATH = os.path.join(_HERE, "libbcgpu_checks.so" if os.environ.get("BCG_LIB") == "checks" else "libbcgpu.so")
+_LIB_ENV = os.environ.get("BCG_LIB", "")
+LIB_PATH = (os.path.join(_HERE, "libbcgpu_checks.so") if _LIB_ENV == "checks"
+            else _LIB_ENV if _LIB_ENV.endswith(".so") else os.path.join(_HERE, "libbcgpu.so"))
 
 _i64 = ctypes.c_int64
 _i32 = ctypes.c_int32

@@ -80,7 +80,7 @@ struct RecFactArgs {
   const int32_t *keys;      // full output blocks to process (indices into the order-m layout)
   int64_t nkeys;
   const int64_t *offs;      // order-m block offsets
-  const int64_t *term_off;  // [K][nterms][2] element offsets of each term's factor blocks
+  const int32_t *term_off;  // [K][nterms][2] element offsets of each term's factor blocks
   const double *cum[16];    // packed C_k, k = 2 .. m-2
   const double *cmom[16];   // packed central moments M_k, k = 4 .. m-2
   double *mk;               // in: M_m, out: C_m

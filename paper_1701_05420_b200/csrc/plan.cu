@@ -392,6 +392,8 @@ static void build_fact_tables(Plan &p) {
     (full ? p.full_keys : p.partial_keys).push_back((int32_t)k);
   }
   if (!recursion_fact_supported(m, p.b)) return;
+  for (int k = 2; k <= m - 2; ++k)
+    if (p.lay[k].offs.back() > INT32_MAX) return;  // offsets kept as int32
   std::vector<int> masks;
   for (int s = 1; s < (1 << m); s += 2) {
     const int c = __builtin_popcount(s);
@@ -408,8 +410,8 @@ static void build_fact_tables(Plan &p) {
         if (masks[t] & (1 << q)) a[na++] = key[q];
         else c[nc++] = key[q];
       }
-      p.term_off[(k * masks.size() + t) * 2] = p.lay[na].offs[multiset_rank(a, na, p.nbar)];
-      p.term_off[(k * masks.size() + t) * 2 + 1] = p.lay[nc].offs[multiset_rank(c, nc, p.nbar)];
+      p.term_off[(k * masks.size() + t) * 2] = (int32_t)p.lay[na].offs[multiset_rank(a, na, p.nbar)];
+      p.term_off[(k * masks.size() + t) * 2 + 1] = (int32_t)p.lay[nc].offs[multiset_rank(c, nc, p.nbar)];
     }
   }
 }

@@ -25,6 +25,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
+#include <cstdlib>
 #include <utility>
 
 #include "kernels.h"
@@ -80,7 +82,7 @@ __host__ __device__ constexpr int head_offset(int mask, int M, int CT, int B, in
 // compile-time immediates.
 template <int M, int B, int CT, int T>
 __device__ __forceinline__ void apply_term(double (&acc)[rf::ipow(B, M - CT)], const int (&dig)[M],
-                                           const RecFactArgs &a, const int64_t *toff) {
+                                           const RecFactArgs &a, const int32_t *toff) {
   constexpr int S = rf::term_mask(M, T);
   constexpr int FULL = (1 << M) - 1;
   constexpr int REST = FULL & ~S;
@@ -105,46 +107,71 @@ __device__ __forceinline__ void apply_term(double (&acc)[rf::ipow(B, M - CT)], c
 
 template <int M, int B, int CT, int... Ts>
 __device__ __forceinline__ void apply_terms(double (&acc)[rf::ipow(B, M - CT)], const int (&dig)[M],
-                                            const RecFactArgs &a, const int64_t *toff,
+                                            const RecFactArgs &a, const int32_t *toff,
                                             std::integer_sequence<int, Ts...>) {
   (apply_term<M, B, CT, Ts>(acc, dig, a, toff), ...);
 }
 
+constexpr int kRfThreads = 128;
+
 template <int M, int B, int CT>
-__global__ void __launch_bounds__(256) k_recursion_fact(RecFactArgs a) {
+__global__ void __launch_bounds__(kRfThreads, 4) k_recursion_fact(RecFactArgs a) {
   constexpr int NT = rf::term_count(M);
   constexpr int ROWS = rf::ipow(B, M - CT);  // elements per thread (registers)
   constexpr int W = rf::ipow(B, CT);         // threads per block
-  const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t kb = item / W;
-  if (kb >= a.nkeys) return;
-  const int c = (int)(item - kb * W);
-  const int32_t key = a.keys[kb];
-  const int64_t *toff = a.term_off + (int64_t)key * 2 * NT;
-  int dig[M];
-#pragma unroll
-  for (int q = 0; q < M; ++q) dig[q] = 0;
-  {
-    int rem = c;
-#pragma unroll
-    for (int q = M - 1; q >= M - CT; --q) {
-      dig[q] = rem % B;
-      rem /= B;
+  constexpr int KPC = (kRfThreads + W - 1) / W + 1;  // max output blocks per step
+  __shared__ int32_t s_toff[KPC * 2 * NT];
+  // each CTA walks a contiguous run of steps (128 items each): consecutive
+  // output blocks share most factor blocks, which then stay in this SM's L1
+  const int64_t nsteps = (a.nkeys * W + kRfThreads - 1) / kRfThreads;
+  const int64_t per = (nsteps + gridDim.x - 1) / gridDim.x;
+  const int64_t s_begin = (int64_t)blockIdx.x * per;
+  const int64_t s_end = min(nsteps, s_begin + per);
+  for (int64_t step = s_begin; step < s_end; ++step) {
+    const int64_t item0 = step * kRfThreads;
+    const int64_t kb0 = item0 / W;
+    __syncthreads();  // previous step done with s_toff
+    // stage the term-offset tables of this step's output blocks (coalesced),
+    // so every factor address below is a shared-memory read away
+    for (int i = threadIdx.x; i < KPC * 2 * NT; i += kRfThreads) {
+      const int64_t kb = kb0 + i / (2 * NT);
+      if (kb < a.nkeys) s_toff[i] = a.term_off[(int64_t)a.keys[kb] * 2 * NT + i % (2 * NT)];
     }
+    __syncthreads();
+    const int64_t item = item0 + threadIdx.x;
+    const int64_t kb = item / W;
+    if (kb >= a.nkeys) continue;
+    const int c = (int)(item - kb * W);
+    const int32_t key = a.keys[kb];
+    const int32_t *toff = s_toff + (kb - kb0) * 2 * NT;
+    int dig[M];
+#pragma unroll
+    for (int q = 0; q < M; ++q) dig[q] = 0;
+    {
+      int rem = c;
+#pragma unroll
+      for (int q = M - 1; q >= M - CT; --q) {
+        dig[q] = rem % B;
+        rem /= B;
+      }
+    }
+    double *blk = a.mk + a.offs[key] + c;
+    double acc[ROWS];
+#pragma unroll
+    for (int row = 0; row < ROWS; ++row) acc[row] = blk[(int64_t)row * W];
+    apply_terms<M, B, CT>(acc, dig, a, toff, std::make_integer_sequence<int, NT>{});
+#pragma unroll
+    for (int row = 0; row < ROWS; ++row) blk[(int64_t)row * W] = acc[row];
   }
-  double *blk = a.mk + a.offs[key] + c;
-  double acc[ROWS];
-#pragma unroll
-  for (int row = 0; row < ROWS; ++row) acc[row] = blk[(int64_t)row * W];
-  apply_terms<M, B, CT>(acc, dig, a, toff, std::make_integer_sequence<int, NT>{});
-#pragma unroll
-  for (int row = 0; row < ROWS; ++row) blk[(int64_t)row * W] = acc[row];
 }
 
-// trailing (thread) modes: the fewest that leave <= 32 register rows
+// trailing (thread) modes: the fewest that leave <= kRfRows register rows
+#ifndef BCG_RF_ROWS
+#define BCG_RF_ROWS 32
+#endif
 __host__ __device__ constexpr int ct_for(int M, int B) {
   int c = 0;
-  while (c < M && rf::ipow(B, M - c) > 32) ++c;
+  while (c < M && rf::ipow(B, M - c) > BCG_RF_ROWS) ++c;
   return c;
 }
 
@@ -153,9 +180,11 @@ static cudaError_t go_fact(const RecFactArgs &a, cudaStream_t stream) {
   constexpr int CT = ct_for(M, B);
   constexpr int W = rf::ipow(B, CT);
   const int64_t items = a.nkeys * W;
-  const int threads = 256;
-  const int64_t blocks = (items + threads - 1) / threads;
-  if (blocks <= 0) return cudaSuccess;
+  const int threads = kRfThreads;
+  const int64_t steps = (items + threads - 1) / threads;
+  if (steps <= 0) return cudaSuccess;
+  static const int per_cta = getenv("BCG_RF_STEPS") ? atoi(getenv("BCG_RF_STEPS")) : 1;  // tuning knob
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(steps, (steps + per_cta - 1) / per_cta));
   k_recursion_fact<M, B, CT><<<(unsigned)blocks, threads, 0, stream>>>(a);
   g_launches++;
   return cudaGetLastError();
