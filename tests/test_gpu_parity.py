@@ -425,3 +425,39 @@ def test_v1_tile_shapes_match_oracle_and_each_other(tile, monkeypatch, rng):
     for n, m, b, t in [(7, 4, 3, 1003), (13, 5, 2, 517), (9, 6, 2, 211), (30, 3, 4, 333)]:
         x2 = rng.standard_normal((t, n))
         np.testing.assert_allclose(packed(bcg.moment(x2, m, b)), orc.moment(x2, m, b), rtol=1e-12, atol=1e-14)
+
+
+def _nccl_worker(rank, world, port, x, m, b, out):
+    import os
+
+    import torch.distributed as dist
+
+    from paper_1701_05420_b200.distributed import cumulants_upto_sharded, shard_bounds
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    lo, hi = shard_bounds(x.shape[0], world, rank)
+    mean, ts = cumulants_upto_sharded(torch.from_numpy(x[lo:hi]).cuda(), m, b)
+    np.savez(out, mean=mean.cpu().numpy(), **{f"c{k}": t.cpu().numpy() for k, t in enumerate(ts, 2)})
+    dist.destroy_process_group()
+
+
+def test_sharded_path_over_nccl_single_rank(tmp_path, rng):
+    """distributed.py on the real CUDA ops + NCCL (world size 1 on this 1-GPU
+    box; the 2-rank collective logic is covered with gloo in test_distributed)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    x = rng.exponential(1.0, size=(3001, 9)) + rng.standard_normal((3001, 9))
+    out = str(tmp_path / "r0.npz")
+    mp.spawn(_nccl_worker, args=(1, port, x, 6, 2, out), nprocs=1, join=True)
+    got = np.load(out)
+    c1, want = orc.cumulants_upto(x, 6, 2)
+    np.testing.assert_allclose(got["mean"], c1, rtol=1e-13)
+    for k in range(2, 7):
+        np.testing.assert_allclose(got[f"c{k}"], want[k], rtol=1e-9, atol=1e-12)
