@@ -175,8 +175,133 @@ __host__ __device__ constexpr int ct_for(int M, int B) {
   return c;
 }
 
+// ---------------------------------------------------------------------------
+// v3: one CTA per output block, every factor sub-block of the block staged in
+// shared memory first (sizes and offsets compile-time), then the same
+// register-blocked evaluation reading shared memory only.  Used when the
+// staged factors fit in 48 KB; otherwise v2 above (factors through L1).
+namespace rf {
+// doubles of factor storage for terms < T (both factors of each term)
+__host__ __device__ constexpr int seg_before(int M, int B, int T) {
+  int off = 0;
+  for (int t = 0; t < T; ++t) {
+    const int sz = popc(term_mask(M, t));
+    off += ipow(B, sz) + ipow(B, M - sz);
+  }
+  return off;
+}
+// staged thread modes: at least 64 threads, at most 32 register rows
+__host__ __device__ constexpr int ct_staged(int M, int B) {
+  int c1 = 0;
+  while (c1 < M - 1 && ipow(B, c1) < 64) ++c1;
+  int c2 = 0;
+  while (c2 < M && ipow(B, M - c2) > 32) ++c2;
+  return c1 > c2 ? c1 : c2;
+}
+}  // namespace rf
+
+template <int M, int B>
+struct Staged {
+  static constexpr int NT = rf::term_count(M);
+  static constexpr int CT = rf::ct_staged(M, B);
+  static constexpr int W = rf::ipow(B, CT);
+  static constexpr int ROWS = rf::ipow(B, M - CT);
+  static constexpr int NTH = (W + 31) / 32 * 32;
+  static constexpr int SEG = rf::seg_before(M, B, NT);
+  // staging pays off when the factor sub-blocks are no larger than the
+  // output block itself (cfg2, cfg3; cfg4's 25 terms stage 2.6x the block)
+  static constexpr bool ok = SEG * 8 <= 48 * 1024 && NTH <= 1024 && ROWS <= 32 && SEG <= rf::ipow(B, M);
+};
+
+template <int M, int B, int T>
+__device__ __forceinline__ void stage_term(double *sm, const RecFactArgs &a, const int32_t *toff, int tid) {
+  constexpr int S = rf::term_mask(M, T);
+  constexpr int s = rf::popc(S), r = M - s;
+  constexpr int L1 = rf::ipow(B, s), L2 = rf::ipow(B, r);
+  constexpr int O1 = rf::seg_before(M, B, T), O2 = O1 + L1;
+  constexpr int NTH = Staged<M, B>::NTH;
+  const double *src1 = a.cum[s] + toff[2 * T];
+  const double *src2 = (r <= 3 ? a.cum[r] : a.cmom[r]) + toff[2 * T + 1];
+  for (int i = tid; i < L1; i += NTH) sm[O1 + i] = __ldg(src1 + i);
+  for (int i = tid; i < L2; i += NTH) sm[O2 + i] = __ldg(src2 + i);
+}
+
+template <int M, int B, int T>
+__device__ __forceinline__ void apply_term_staged(double (&acc)[Staged<M, B>::ROWS], const int (&dig)[M],
+                                                  const double *sm) {
+  constexpr int CT = Staged<M, B>::CT, ROWS = Staged<M, B>::ROWS;
+  constexpr int S = rf::term_mask(M, T);
+  constexpr int REST = ((1 << M) - 1) & ~S;
+  constexpr int s = rf::popc(S);
+  constexpr int O1 = rf::seg_before(M, B, T), O2 = O1 + rf::ipow(B, s);
+  int o1 = 0, o2 = 0;
+#pragma unroll
+  for (int q = M - CT; q < M; ++q) {
+    if (S & (1 << q)) o1 += dig[q] * rf::stride_in(S, q, B);
+    if (REST & (1 << q)) o2 += dig[q] * rf::stride_in(REST, q, B);
+  }
+  const double *f1 = sm + O1 + o1;
+  const double *f2 = sm + O2 + o2;
+#pragma unroll
+  for (int row = 0; row < ROWS; ++row) {
+    const double u = f1[rf::head_offset(S, M, CT, B, row)];
+    const double v = f2[rf::head_offset(REST, M, CT, B, row)];
+    acc[row] = fma(-u, v, acc[row]);
+  }
+}
+
+template <int M, int B, int... Ts>
+__device__ __forceinline__ void staged_all(double *sm, double (&acc)[Staged<M, B>::ROWS], const int (&dig)[M],
+                                           const RecFactArgs &a, const int32_t *toff, int tid, bool active,
+                                           std::integer_sequence<int, Ts...>) {
+  (stage_term<M, B, Ts>(sm, a, toff, tid), ...);
+  __syncthreads();
+  if (active) (apply_term_staged<M, B, Ts>(acc, dig, sm), ...);
+}
+
+template <int M, int B>
+__global__ void __launch_bounds__(Staged<M, B>::NTH) k_recursion_staged(RecFactArgs a) {
+  using ST = Staged<M, B>;
+  __shared__ double sm[ST::SEG];
+  const int tid = threadIdx.x;
+  const int32_t key = a.keys[blockIdx.x];
+  const int32_t *toff = a.term_off + (int64_t)key * 2 * ST::NT;
+  const bool active = tid < ST::W;
+  const int c = active ? tid : 0;
+  int dig[M];
+#pragma unroll
+  for (int q = 0; q < M; ++q) dig[q] = 0;
+  {
+    int rem = c;
+#pragma unroll
+    for (int q = M - 1; q >= M - ST::CT; --q) {
+      dig[q] = rem % B;
+      rem /= B;
+    }
+  }
+  double *blk = a.mk + a.offs[key] + c;
+  double acc[ST::ROWS];
+  // M_m first: its HBM latency overlaps the factor staging
+#pragma unroll
+  for (int row = 0; row < ST::ROWS; ++row) acc[row] = active ? blk[(int64_t)row * ST::W] : 0.0;
+  staged_all<M, B>(sm, acc, dig, a, toff, tid, active, std::make_integer_sequence<int, ST::NT>{});
+  if (active) {
+#pragma unroll
+    for (int row = 0; row < ST::ROWS; ++row) blk[(int64_t)row * ST::W] = acc[row];
+  }
+}
+
 template <int M, int B>
 static cudaError_t go_fact(const RecFactArgs &a, cudaStream_t stream) {
+  static const bool no_staged = getenv("BCG_RF_NO_STAGED") != nullptr;  // A/B knob
+  if constexpr (Staged<M, B>::ok) {
+    if (!no_staged) {
+      if (a.nkeys <= 0) return cudaSuccess;
+      k_recursion_staged<M, B><<<(unsigned)a.nkeys, Staged<M, B>::NTH, 0, stream>>>(a);
+      g_launches++;
+      return cudaGetLastError();
+    }
+  }
   constexpr int CT = ct_for(M, B);
   constexpr int W = rf::ipow(B, CT);
   const int64_t items = a.nkeys * W;
