@@ -71,8 +71,8 @@ int bcg_moment_blocks(const double *xt, int64_t n, int64_t t,
 typedef struct bcg_plan bcg_plan;
 
 int bcg_plan_create(int64_t n, int32_t m, int32_t b, bcg_plan **plan);
-/* Same with an explicit moment-kernel variant (-1 = default; 0 = v1 64x64
- * all-warps kernel; 1..4 = warp-specialized tile shapes, K2). */
+/* Same with an explicit moment-kernel variant (-1 = default, 0 = the DMMA
+ * kernel of DESIGN.md K2; other values are rejected). */
 int bcg_plan_create_ex(int64_t n, int32_t m, int32_t b, int32_t variant,
                        bcg_plan **plan);
 /* Fused multi-order plan: ONE staircase GEMM over the block alphabet extended
@@ -131,12 +131,31 @@ int bcg_center(const double *x, int64_t t, int64_t n, int64_t ldx,
 /* ---------------------------------------------------------------------------
  * Order-m packed RAW moment sums of x (t x n row-major, ldx >= n), ACCUMULATED
  * into out[S_m] (same semantics as bcg_moment_blocks over all blocks).  The
- * Khatri-Rao-staged FP64 DMMA GEMM.  `ws` must hold
- * bcg_moment_ws_bytes(plan, t) bytes (may be NULL when that is 0).
+ * Khatri-Rao-staged FP64 DMMA GEMM; x is first transposed
+ * into the workspace.  `ws` must hold bcg_moment_ws_bytes(plan, t) bytes.
  * ------------------------------------------------------------------------- */
 int bcg_moment_raw(const bcg_plan *plan, const double *x, int64_t t,
                    int64_t ldx, double *out, void *ws, size_t ws_bytes,
                    void *stream);
+/* Same from the TRANSPOSED layout the reference's own kernel takes
+ * (bc/_engines.py:95): xt has n rows of stride ldt (even, >= bcg_padded_t(t)),
+ * 16-byte aligned, zero-padded in [t, ldt).  No transpose pass; `ws` needs
+ * only the split-K part (bcg_moment_ws_bytes is always enough). */
+int bcg_moment_raw_t(const bcg_plan *plan, const double *xt, int64_t t,
+                     int64_t ldt, double *out, void *ws, size_t ws_bytes,
+                     void *stream);
+/* t rounded up to the moment kernel's 16-sample chunk. */
+int64_t bcg_padded_t(int64_t t);
+/* xt[c, l] = x[l, c] - mean[c] (mean may be NULL) for l < t, 0 for
+ * t <= l < ldt: centering (bc/moments.py:38-41) fused with the transpose
+ * into the layout bcg_moment_raw_t reads. */
+int bcg_transpose_pad(const double *x, int64_t t, int64_t n, int64_t ldx,
+                      const double *mean, double *xt, int64_t ldt, void *stream);
+/* Per-row sums / sums of squares of xt (n x ldt, first t entries): the
+ * column statistics of the transposed data (_check_centered,
+ * bc/cumulants.py:31-39).  Deterministic. */
+int bcg_rowstats(const double *xt, int64_t n, int64_t t, int64_t ldt,
+                 double *sums, double *sumsq, void *stream);
 /* Same, restricted to blocks [k0, k1) (only out[offs[k0]:offs[k1]] is
  * touched; bitwise identical to the full call on those blocks) -- the
  * block-split path of moment_parallel_blocks (bc/moments.py:99-131). */

@@ -11,7 +11,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbcgpu.so")
-SOURCES = ["plan.cu", "moment.cu", "moment_ws.cu", "elementwise.cu", "recursion.cu", "recursion_fact.cu", "capi.cu"]
+SOURCES = ["plan.cu", "moment.cu", "elementwise.cu", "recursion.cu", "recursion_fact.cu", "capi.cu"]
 HEADERS = ["plan.h", "kernels.h", "kr.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -57,7 +57,7 @@ constexpr int64_t kWsCap = (int64_t)2 << 30;  // 2 GiB of split-K partials at mo
 
 Slicing choose_slicing(const bcg::Plan &p, int64_t t) {
   Slicing s{bcg::pick_kc((int)p.n), 1, 1, bcg::kSliceLen};
-  if (p.variant > 0 || !(p.tm == 64 && p.tn == 64)) s.KC = 16;
+  if (s.KC != 0 && !(p.tm == 64 && p.tn == 64)) s.KC = 16;
   if (s.KC == 0 || t <= 0) return s;
   s.nslices = (int)((t + bcg::kSliceLen - 1) / bcg::kSliceLen);
   // slices per launch: as many as the workspace cap allows (fewest launches,
@@ -74,26 +74,34 @@ Slicing choose_slicing(const bcg::Plan &p, int64_t t) {
   return s;
 }
 
+// split-K partials (the transposed-input entries)
 size_t ws_bytes_for(const bcg::Plan &p, const Slicing &s) {
   return s.group > 1 ? (size_t)s.group * (size_t)p.S_out * sizeof(double) : 0;
 }
 
-int run_moment(const bcg::Plan &p, const double *x, int64_t t, int64_t ldx, double *out, void *ws,
+// the row-major entries also transpose x into the workspace first
+size_t xt_bytes_for(const bcg::Plan &p, int64_t t) {
+  return ((size_t)p.n * (size_t)bcg::padded_t(t) * sizeof(double) + 255) / 256 * 256;
+}
+
+// xt: transposed data, n rows of stride ldt >= padded_t(t), zero-padded past t
+int run_moment(const bcg::Plan &p, const double *xt, int64_t t, int64_t ldt, double *out, void *ws,
                size_t ws_bytes, int64_t k0, int64_t k1, cudaStream_t stream) {
   if (t <= 0) return BCG_OK;
   const Slicing sl = choose_slicing(p, t);
   if (sl.KC == 0) return fail(BCG_EINVAL, "too many columns for the moment kernel's shared-memory stage");
+  if (ldt < bcg::padded_t(t) || (ldt & 1) || (reinterpret_cast<uintptr_t>(xt) & 15))
+    return fail(BCG_EINVAL, "xt must be 16-byte aligned with an even row stride >= t rounded up to 16");
   const size_t need = ws_bytes_for(p, sl);
   if (need > ws_bytes || (need && !ws))
     return fail(BCG_EINVAL, "workspace too small: need " + std::to_string(need) + " bytes");
   bcg::MomentArgs a{};
-  a.x = x;
+  a.x = xt;
   a.t = t;
-  a.ldx = ldx;
+  a.ldx = ldt;
   a.n = (int)p.n;
   a.h = p.h;
   a.r = p.r;
-  a.bulk_ok = (ldx == p.n) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && ((sl.KC * p.n * 8) % 16 == 0);
   a.rowcols = p.d_rowcols;
   a.colcols = p.d_colcols;
   a.row_keybase = p.d_row_keybase;
@@ -125,10 +133,7 @@ int run_moment(const bcg::Plan &p, const double *x, int64_t t, int64_t ldx, doub
     a.nslices = std::min(sl.group, sl.nslices - g0);
     const int64_t grid = (int64_t)a.ntiles * a.nslices;
     if (grid > INT32_MAX) return fail(BCG_EINVAL, "moment grid too large");
-    if (p.variant > 0)
-      CUDA_TRY(bcg::launch_moment_ws(a, p.variant, (int)grid, stream), "moment kernel");
-    else
-      CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream, p.tm, p.tn), "moment kernel");
+    CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream, p.tm, p.tn), "moment kernel");
     bcg::g_launches++;
     if (a.nslices > 1) {
       CUDA_TRY(bcg::launch_reduce_slices(a.ws, a.nslices, a.S, lo, hi, out, stream),
@@ -156,7 +161,7 @@ int bcg_plan_create(int64_t n, int32_t m, int32_t b, bcg_plan **plan) {
 
 int bcg_plan_create_ex(int64_t n, int32_t m, int32_t b, int32_t variant, bcg_plan **plan) {
   if (!plan) return fail(BCG_EINVAL, "plan pointer is NULL");
-  if (variant > 4) return fail(BCG_EINVAL, "unknown moment kernel variant " + std::to_string(variant));
+  if (variant > 0) return fail(BCG_EINVAL, "unknown moment kernel variant " + std::to_string(variant));
   auto pl = std::make_unique<bcg_plan>();
   std::string err = bcg::build_plan(n, m, b, pl->p, variant);
   if (!err.empty()) return fail(BCG_EINVAL, err);
@@ -296,7 +301,7 @@ int bcg_moment_ws_bytes(const bcg_plan *plan, int64_t t, size_t *bytes) {
     *bytes = 0;
     return BCG_OK;
   }
-  *bytes = ws_bytes_for(plan->p, choose_slicing(plan->p, t));
+  *bytes = xt_bytes_for(plan->p, t) + ws_bytes_for(plan->p, choose_slicing(plan->p, t));
   return BCG_OK;
 }
 
@@ -324,6 +329,19 @@ int bcg_center(const double *x, int64_t t, int64_t n, int64_t ldx, const double 
   return BCG_OK;
 }
 
+// row-major x (t x n, ldx): transpose (zero-padded) into the workspace, then
+// the transposed-input GEMM on the rest of the workspace
+static int moment_rowmajor(const bcg::Plan &p, const double *x, int64_t t, int64_t ldx, double *out, void *ws,
+                           size_t ws_bytes, int64_t k0, int64_t k1, cudaStream_t s) {
+  if (t <= 0) return BCG_OK;
+  const size_t xtb = xt_bytes_for(p, t);
+  if (!ws || ws_bytes < xtb) return fail(BCG_EINVAL, "workspace too small: need at least " + std::to_string(xtb) + " bytes");
+  double *xt = static_cast<double *>(ws);
+  const int64_t ldt = bcg::padded_t(t);
+  CUDA_TRY(bcg::launch_transpose_pad(x, t, p.n, ldx, nullptr, xt, ldt, s), "transpose");
+  return run_moment(p, xt, t, ldt, out, static_cast<char *>(ws) + xtb, ws_bytes - xtb, k0, k1, s);
+}
+
 int bcg_moment_raw(const bcg_plan *plan, const double *x, int64_t t, int64_t ldx, double *out, void *ws,
                    size_t ws_bytes, void *stream) {
   if (!plan) return fail(BCG_EINVAL, "plan is NULL");
@@ -331,7 +349,16 @@ int bcg_moment_raw(const bcg_plan *plan, const double *x, int64_t t, int64_t ldx
   if (p.m < 2 || p.m > 16) return fail(BCG_EINVAL, "kernel supports 2 <= m <= 16");
   if (ldx < p.n) return fail(BCG_EINVAL, "ldx < n");
   if (!p.d_tiles) return fail(BCG_EINVAL, "host-only plan");
-  return run_moment(p, x, t, ldx, out, ws, ws_bytes, 0, p.lay[p.m].K, static_cast<cudaStream_t>(stream));
+  return moment_rowmajor(p, x, t, ldx, out, ws, ws_bytes, 0, p.lay[p.m].K, static_cast<cudaStream_t>(stream));
+}
+
+int bcg_moment_raw_t(const bcg_plan *plan, const double *xt, int64_t t, int64_t ldt, double *out, void *ws,
+                     size_t ws_bytes, void *stream) {
+  if (!plan) return fail(BCG_EINVAL, "plan is NULL");
+  const bcg::Plan &p = plan->p;
+  if (p.m < 2 || p.m > 16) return fail(BCG_EINVAL, "kernel supports 2 <= m <= 16");
+  if (!p.d_tiles) return fail(BCG_EINVAL, "host-only plan");
+  return run_moment(p, xt, t, ldt, out, ws, ws_bytes, 0, p.lay[p.m].K, static_cast<cudaStream_t>(stream));
 }
 
 int bcg_moment_raw_range(const bcg_plan *plan, const double *x, int64_t t, int64_t ldx, double *out, void *ws,
@@ -344,7 +371,22 @@ int bcg_moment_raw_range(const bcg_plan *plan, const double *x, int64_t t, int64
   k0 = std::max<int64_t>(k0, 0);
   k1 = std::min<int64_t>(k1, p.lay[p.m].K);
   if (k1 <= k0) return BCG_OK;
-  return run_moment(p, x, t, ldx, out, ws, ws_bytes, k0, k1, static_cast<cudaStream_t>(stream));
+  return moment_rowmajor(p, x, t, ldx, out, ws, ws_bytes, k0, k1, static_cast<cudaStream_t>(stream));
+}
+
+int bcg_transpose_pad(const double *x, int64_t t, int64_t n, int64_t ldx, const double *mean, double *xt, int64_t ldt,
+                      void *stream) {
+  if (t < 1 || n < 1 || ldx < n || ldt < t) return fail(BCG_EINVAL, "bad transpose shape");
+  CUDA_TRY(bcg::launch_transpose_pad(x, t, n, ldx, mean, xt, ldt, static_cast<cudaStream_t>(stream)), "transpose");
+  return BCG_OK;
+}
+
+int64_t bcg_padded_t(int64_t t) { return bcg::padded_t(t); }
+
+int bcg_rowstats(const double *xt, int64_t n, int64_t t, int64_t ldt, double *sums, double *sumsq, void *stream) {
+  if (t < 1 || n < 1 || ldt < t) return fail(BCG_EINVAL, "bad shape");
+  CUDA_TRY(bcg::launch_rowstats(xt, n, t, ldt, sums, sumsq, static_cast<cudaStream_t>(stream)), "rowstats");
+  return BCG_OK;
 }
 
 int bcg_moment_blocks(const double *xt, int64_t n, int64_t t, const int64_t *col0, const int64_t *edges, int64_t m,
@@ -398,7 +440,8 @@ int bcg_moment_blocks(const double *xt, int64_t n, int64_t t, const int64_t *col
   double *x = nullptr;
   void *ws = nullptr;
   const size_t wsb = ws_bytes_for(pl->p, choose_slicing(pl->p, t));
-  CUDA_TRY(cudaMallocAsync(&x, (size_t)t * n * sizeof(double), s), "transpose buffer");
+  const int64_t ldt = bcg::padded_t(t);
+  CUDA_TRY(cudaMallocAsync(&x, (size_t)ldt * n * sizeof(double), s), "padded copy");
   if (wsb) {
     cudaError_t e = cudaMallocAsync(&ws, wsb, s);
     if (e != cudaSuccess) {
@@ -406,8 +449,9 @@ int bcg_moment_blocks(const double *xt, int64_t n, int64_t t, const int64_t *col
       return cuda_fail(e, "workspace");
     }
   }
-  cudaError_t e = bcg::launch_transpose(xt, n, t, x, s);
-  int rc = e == cudaSuccess ? run_moment(pl->p, x, t, n, out, ws, wsb, k0, k1, s) : cuda_fail(e, "transpose");
+  // the reference's xt is already the transposed layout; pad its rows to ldt
+  cudaError_t e = bcg::launch_pad_rows(xt, n, t, t, x, ldt, s);
+  int rc = e == cudaSuccess ? run_moment(pl->p, x, t, ldt, out, ws, wsb, k0, k1, s) : cuda_fail(e, "pad copy");
   cudaFreeAsync(x, s);
   if (ws) cudaFreeAsync(ws, s);
   return rc;

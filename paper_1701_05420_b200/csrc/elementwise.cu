@@ -174,4 +174,86 @@ cudaError_t launch_div(int64_t len, const double *x, double d, double *out, cuda
   return cudaGetLastError();
 }
 
+// xt[c, l] = x[l, c] - (mean ? mean[c] : 0) for l < t, 0 for t <= l < ldt:
+// the padded transposed layout the moment kernel stages (32 x 32 smem tiles,
+// coalesced on both sides).
+__global__ void k_transpose_pad(const double *__restrict__ x, int64_t t, int64_t n, int64_t ldx,
+                                const double *__restrict__ mean, double *__restrict__ xt, int64_t ldt) {
+  __shared__ double tile[32][33];
+  const int64_t l0 = blockIdx.x * 32LL, c0 = blockIdx.y * 32LL;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t l = l0 + i, c = c0 + threadIdx.x;
+    double v = 0.0;
+    if (l < t && c < n) v = x[l * ldx + c] - (mean ? mean[c] : 0.0);
+    tile[i][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, l = l0 + threadIdx.x;
+    if (c < n && l < ldt) xt[c * ldt + l] = tile[threadIdx.x][i];
+  }
+}
+
+cudaError_t launch_transpose_pad(const double *x, int64_t t, int64_t n, int64_t ldx, const double *mean, double *xt,
+                                 int64_t ldt, cudaStream_t stream) {
+  dim3 grid((unsigned)((ldt + 31) / 32), (unsigned)((n + 31) / 32));
+  k_transpose_pad<<<grid, dim3(32, 8), 0, stream>>>(x, t, n, ldx, mean, xt, ldt);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+// dst[c, l] = src[c, l] for l < t (src row stride lds), 0 up to ldt
+__global__ void k_pad_rows(const double *__restrict__ src, int64_t n, int64_t t, int64_t lds, double *__restrict__ dst,
+                           int64_t ldt) {
+  const int64_t total = n * ldt;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / ldt, l = i - c * ldt;
+    dst[i] = l < t ? src[c * lds + l] : 0.0;
+  }
+}
+
+cudaError_t launch_pad_rows(const double *src, int64_t n, int64_t t, int64_t lds, double *dst, int64_t ldt,
+                            cudaStream_t stream) {
+  int64_t blocks = (n * ldt + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  k_pad_rows<<<(int)blocks, 256, 0, stream>>>(src, n, t, lds, dst, ldt);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+// per row c of xt (n x ldt): sums[c] = sum_{l<t} xt[c, l], sumsq[c] = sum xt^2
+// (one CTA per row, fixed-order tree: deterministic)
+__global__ void k_rowstats(const double *__restrict__ xt, int64_t t, int64_t ldt, double *sums, double *sumsq) {
+  __shared__ double rs[256], rq[256];
+  const int64_t c = blockIdx.x;
+  double s = 0.0, q = 0.0;
+  for (int64_t l = threadIdx.x; l < t; l += 256) {
+    const double v = xt[c * ldt + l];
+    s += v;
+    q += v * v;
+  }
+  rs[threadIdx.x] = s;
+  rq[threadIdx.x] = q;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      rs[threadIdx.x] += rs[threadIdx.x + w];
+      rq[threadIdx.x] += rq[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (sums) sums[c] = rs[0];
+    if (sumsq) sumsq[c] = rq[0];
+  }
+}
+
+cudaError_t launch_rowstats(const double *xt, int64_t n, int64_t t, int64_t ldt, double *sums, double *sumsq,
+                            cudaStream_t stream) {
+  k_rowstats<<<(unsigned)n, 256, 0, stream>>>(xt, t, ldt, sums, sumsq);
+  g_launches++;
+  return cudaGetLastError();
+}
+
 }  // namespace bcg

@@ -14,6 +14,7 @@ struct MomentArgs {
   int n, h, r;
   int bulk_ok;  // rows contiguous and 16-byte aligned: TMA bulk staging
   int ones;     // fused multi-order plan: column -1 is the constant-ones column
+  // x is the TRANSPOSED data (n rows, row stride ldx >= padded_t(t)), zero-padded past t
   const int16_t *rowcols, *colcols;
   const int32_t *row_keybase, *row_olin, *row_cstart;
   const int32_t *col_rank, *col_olin, *col_size;
@@ -38,9 +39,6 @@ size_t moment_smem_bytes(int KC, int n, int tm = 64, int tn = 64);
 int pick_kc(int n);
 bool v1_shape_supported(int KC, int m, int tm, int tn);
 cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t stream, int tm = 64, int tn = 64);
-cudaError_t launch_moment_ws(const MomentArgs &args, int variant, int grid, cudaStream_t stream,
-                             int *blocks_per_sm = nullptr);
-void ws_tile_shape(int variant, int *tm, int *tn);
 cudaError_t launch_reduce_slices(const double *ws, int nslices, int64_t S, int64_t lo, int64_t hi,
                                  double *out, cudaStream_t stream);
 
@@ -51,6 +49,14 @@ int colstats_parts(int64_t t, int64_t n);
 cudaError_t launch_center(const double *x, int64_t t, int64_t n, int64_t ldx, const double *mean, double *xc,
                           cudaStream_t stream);
 cudaError_t launch_transpose(const double *xt, int64_t n, int64_t t, double *x, cudaStream_t stream);
+cudaError_t launch_transpose_pad(const double *x, int64_t t, int64_t n, int64_t ldx, const double *mean, double *xt,
+                                 int64_t ldt, cudaStream_t stream);
+cudaError_t launch_pad_rows(const double *src, int64_t n, int64_t t, int64_t lds, double *dst, int64_t ldt,
+                            cudaStream_t stream);
+cudaError_t launch_rowstats(const double *xt, int64_t n, int64_t t, int64_t ldt, double *sums, double *sumsq,
+                            cudaStream_t stream);
+// padded sample count of the transposed layout the moment kernel reads
+inline int64_t padded_t(int64_t t) { return (t + 15) / 16 * 16; }
 cudaError_t launch_div(int64_t len, const double *x, double d, double *out, cudaStream_t stream);
 cudaError_t launch_axpby(int64_t len, double a, const double *x, double c, const double *y, double *out,
                          cudaStream_t stream);

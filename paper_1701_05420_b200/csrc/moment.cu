@@ -7,27 +7,37 @@
 // {row group v = L[-1], col R with R[0] >= v} so nothing outside S_m is formed
 // except ragged tile edges.
 //
-// Per CTA (64 x 64 output tile, 4 warps of 32 x 32):
-//   1. a contiguous sample chunk X[s:s+KC, :] is staged into shared memory by
-//      a 1-D TMA bulk copy (cp.async.bulk, mbarrier complete_tx), double
-//      buffered;
-//   2. the chunk's Khatri-Rao factors  A[k][i] = prod_q X[s+k, rowcols[i][q]]
-//      and B[k][j] = prod_q X[s+k, colcols[j][q]] are built in shared memory
-//      (never in HBM), double buffered;
-//   3. warps run mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4) over the chunk, FP64
-//      accumulators in registers;
+// Input: the TRANSPOSED data xt (n rows x ldt, one contiguous row per
+// variable -- the layout the reference's own kernel takes, bc/_engines.py:95),
+// zero-padded to a multiple of 16 samples.
+//
+// Per CTA (TM x TN output tile, 4 warps):
+//   1. a sample chunk xt[:, s:s+16] is staged into shared memory by ONE 2-D TMA
+//      tensor copy (cp.async.bulk.tensor, box 16 samples x n variables, SASS
+//      UTMALDG) with 128-byte swizzle (8 consecutive rows at the same sample
+//      pair hit 8 distinct 16-byte bank groups), double buffered, on an
+//      mbarrier; a constant row of ones follows the n data rows (the "ones"
+//      column of fused multi-order plans);
+//   2. the chunk's Khatri-Rao factors A[i][k] = prod_q X[s+k, rowcols[i][q]]
+//      and B[j][k] are built in shared memory (never in HBM), two samples per
+//      LDS.128 / DMUL pair / STS.128, at compile-time offsets;
+//   3. warps run mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4) over the chunk into FP64
+//      register tiles; the loop is software-pipelined (the factors of chunk c+1
+//      are built while chunk c's DMMAs issue, one CTA barrier per chunk);
 //   4. the epilogue scatters each accumulator to its packed address
-//      offs[keybase[row] + rank[col]] + olin[row] * size[col] + olin[col],
-//      either accumulating into `out` (one K-slice) or writing a per-slice
-//      partial that k_reduce_slices adds in slice order (deterministic split-K,
-//      no float atomics).  Slices have a fixed length (kSliceLen samples), so
-//      every element's summation order depends on t only -- not on the plan,
-//      tile shape, key range or launch grouping: moments from different plans
-//      (block-split, kernel variants) agree bitwise.
+//      koff[keybase[row] + rank[col]] + olin[row] * size[col] + olin[col],
+//      either accumulating into `out` (one K-slice per launch) or writing a
+//      per-slice partial that k_reduce_slices adds in slice order
+//      (deterministic split-K, no float atomics).  Slices have a fixed length
+//      (kSliceLen samples), so every element's summation order depends on t
+//      only -- not on the plan, tile shape, key range or launch grouping.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 
 #include "kernels.h"
 #include "kr.cuh"
@@ -35,7 +45,6 @@
 
 namespace bcg {
 
-constexpr int kPad = 4;  // row stride (TM + 4) doubles == 32 mod 128 bytes: the 4 k-rows of an m8n8k4 fragment load hit 4 distinct bank quadrants (conflict-free)
 constexpr int kThreads = 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -56,55 +65,89 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "bra.uni LAB_WAIT;\n"
       "DONE:\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity));
+      "r"(parity)
+      : "memory");
 }
 
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+__device__ __forceinline__ void mbar_expect(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
           smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
 
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
 }
 
 // CTA tile TM x TN, 4 warps in a WGM x WGN grid (warp tile WM x WN of 8x8
-// DMMA sub-tiles).  Khatri-Rao work split: TM rows x KC samples of A and
-// TN columns x KC samples of B over 128 threads, each thread a fixed row
-// (column) and an interleaved set of samples, so its X column indices stay in
-// registers.
-template <int TM, int TN>
+// DMMA sub-tiles).  Factor storage [row][k], 16 doubles per row, sample index
+// XOR-swizzled by ((row & 3) << 2): an m8n8k4 fragment load (rows gid, samples
+// k0 + tig) and a paired STS.128 (samples 2j, 2j+1) are both conflict-free.
+template <int KC, int TM, int TN>
 struct V1Shape {
   static constexpr int WGN = TN >= 4 * TM ? 4 : (TN >= TM ? 2 : 1);
   static constexpr int WGM = 4 / WGN;
   static constexpr int WM = TM / WGM, WN = TN / WGN;
   static constexpr int MT = WM / 8, NT = WN / 8;
-  static constexpr int LDA = TM + kPad, LDB = TN + kPad;
+  static constexpr int LDK = KC;       // factor row stride (doubles), swizzled
+  static_assert(KC == 16, "the TMA box is one 128-byte swizzle span of samples");
+  static constexpr int PA = kThreads / TM, PB = kThreads / TN;  // threads per factor row
+  static constexpr int NPAIR = KC / 2;                          // sample pairs per chunk
   static_assert(WM % 8 == 0 && WN % 8 == 0, "warp tile must be a multiple of 8");
   static_assert(kThreads % TM == 0 && kThreads % TN == 0, "TM, TN must divide 128");
+  static_assert(NPAIR % PA == 0 && NPAIR % PB == 0, "sample pairs must split evenly");
 };
 
-template <int KC, int M, bool ONES, int TM, int TN>
-__global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
-  using SH = V1Shape<TM, TN>;
+// samples (2j, 2j+1) of staged row r: 128-byte swizzle, 16-byte chunk j of
+// row r lives at chunk j ^ (r & 7)
+__device__ __forceinline__ double2 xs_pair(const double *row, int sw, int j) {
+  return *reinterpret_cast<const double2 *>(row + 2 * (j ^ sw));
+}
+
+template <int NQ>
+__device__ __forceinline__ double2 kr_pair(const double *const (&row)[8], const int (&sw)[8], int nq, int j) {
+  double2 p = xs_pair(row[0], sw[0], j);
+  if constexpr (NQ > 0) {
+#pragma unroll
+    for (int q = 1; q < NQ; ++q) {
+      const double2 v = xs_pair(row[q], sw[q], j);
+      p.x *= v.x;
+      p.y *= v.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 1; q < 8; ++q)
+      if (q < nq) {
+        const double2 v = xs_pair(row[q], sw[q], j);
+        p.x *= v.x;
+        p.y *= v.y;
+      }
+  }
+  return p;
+}
+
+template <int KC, int M, int TM, int TN>
+__global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant__ CUtensorMap tmap, MomentArgs a) {
+  using SH = V1Shape<KC, TM, TN>;
   constexpr int H = M / 2, R = M - M / 2;  // compile-time mode counts (0: runtime)
-  constexpr int LDA = SH::LDA, LDB = SH::LDB, MT = SH::MT, NT = SH::NT;
-  constexpr int PA = kThreads / TM, PB = kThreads / TN;  // sample phases per row / col
-  static_assert(KC % PA == 0 && KC % PB == 0, "KC must be a multiple of the sample phases");
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int LDX = KC;                  // staged row: 16 doubles = one 128-byte swizzle span
+  constexpr int LDK = SH::LDK, MT = SH::MT, NT = SH::NT;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int n = a.n;
-  double *xs = reinterpret_cast<double *>(smem_raw);   // [2][KC*n]
-  double *kra = xs + 2 * KC * n;                       // [2][KC][LDA]
-  double *krb = kra + 2 * KC * LDA;                    // [2][KC][LDB]
-  uint64_t *bar = reinterpret_cast<uint64_t *>(krb + 2 * KC * LDB);
+  const int xrows = (n + 1 + 7) / 8 * 8;               // n variables + the ones row, 1024-byte stages
+  double *xs = reinterpret_cast<double *>(smem_raw);   // [2][xrows][16], swizzled
+  double *kra = xs + 2 * xrows * LDX;                  // [2][TM][LDK]
+  double *krb = kra + 2 * TM * LDK;                    // [2][TN][LDK]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(krb + 2 * TN * LDK);
 
   const int tid = threadIdx.x;
   const int unit = blockIdx.x;
@@ -117,20 +160,27 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
   const Tile tile = a.tiles[tile_id];
   const int64_t sbeg = (int64_t)slice * a.slice_len;
   const int64_t send = min(a.t, sbeg + a.slice_len);
-  const int64_t slen = send - sbeg;
-  const int nch = (int)((slen + KC - 1) / KC);
+  const int nch = (int)((send - sbeg + KC - 1) / KC);  // xt is zero-padded past t
 
-  // ---- per-thread Khatri-Rao assignment ----
-  const int ia = tid % TM, pa0 = tid / TM;  // A row, first sample phase (step PA)
-  const int ib = tid % TN, pb0 = tid / TN;  // B col, first sample phase (step PB)
+  // ---- per-thread Khatri-Rao assignment: a fixed factor row (A) and column
+  // (B), an interleaved set of sample pairs.  Rows past R / C keep column 0:
+  // their products feed only accumulators the epilogue discards. ----
+  const int ia = tid % TM, pa0 = tid / TM;
+  const int ib = tid % TN, pb0 = tid / TN;
   int colA[8], colB[8];
-  const int64_t grow = (int64_t)tile.row0 + ia;
-  const int64_t gcol = (int64_t)tile.col0 + ib;
-  const bool okA = grow < a.R, okB = gcol < a.C;
+  {
+    const int64_t grow = (int64_t)tile.row0 + ia;
+    const int64_t gcol = (int64_t)tile.col0 + ib;
+    const bool okA = grow < a.R, okB = gcol < a.C;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    colA[q] = (okA && q < a.h) ? a.rowcols[grow * a.h + q] : 0;
-    colB[q] = (okB && q < a.r) ? a.colcols[gcol * a.r + q] : 0;
+    for (int q = 0; q < 8; ++q) {
+      int ca = (okA && q < a.h) ? a.rowcols[grow * a.h + q] : 0;
+      int cb = (okB && q < a.r) ? a.colcols[gcol * a.r + q] : 0;
+      colA[q] = ca < 0 ? n : ca;  // -1: the ones row
+      colB[q] = cb < 0 ? n : cb;
+      BCG_CHECK(colA[q] >= 0 && colA[q] <= n, "colA", colA[q]);
+      BCG_CHECK(colB[q] >= 0 && colB[q] <= n, "colB", colB[q]);
+    }
   }
 
   if (tid == 0) {
@@ -138,13 +188,19 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  // the ones rows of both stages (all ones: the swizzle does not matter)
+  for (int k = tid; k < 2 * LDX; k += kThreads) xs[(k / LDX) * xrows * LDX + n * LDX + (k % LDX)] = 1.0;
   __syncthreads();
 
-  const uint32_t full_bytes = (uint32_t)(KC * n * sizeof(double));
-  auto chunk_full = [&](int c) { return (int64_t)(c + 1) * KC <= slen && a.bulk_ok; };
+  // thread 0 stages chunk c: one 2-D tensor copy per 256 variables
   auto issue = [&](int c) {
-    const double *src = a.x + (sbeg + (int64_t)c * KC) * a.ldx;
-    bulk_g2s(xs + (c & 1) * KC * n, src, full_bytes, &bar[c & 1]);
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_expect(&bar[c & 1], (uint32_t)(n * KC * sizeof(double)));
+      double *dst = xs + (c & 1) * xrows * LDX;
+      const int s0 = (int)(sbeg + (int64_t)c * KC);
+      for (int v0 = 0; v0 < n; v0 += 256) tma_load_2d(dst + v0 * LDX, &tmap, s0, v0, &bar[c & 1]);
+    }
   };
 
   const int warp = tid >> 5, lane = tid & 31;
@@ -156,88 +212,74 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // Software pipeline, one CTA barrier per chunk: while the warps issue the
-  // DMMAs of chunk c they also build the Khatri-Rao factors of chunk c+1 into
-  // the other KR buffer; the TMA copy of chunk c+2 is in flight meanwhile.
-  //   stage(x) = x & 1 for both the X ring and the KR double buffer.
-  auto load_x = [&](int c) {  // make chunk c's samples resident in xs[c & 1]
-    double *xst = xs + (c & 1) * KC * n;
-    if (chunk_full(c)) {
-      mbar_wait(&bar[c & 1], (uint32_t)((c >> 1) & 1));
-    } else {
-      // ragged / strided chunk: plain loads, zero-filled past the slice end
-      const int64_t s0 = sbeg + (int64_t)c * KC;
-      const int rows = (int)(send - s0 < KC ? send - s0 : KC);
-      for (int idx = tid; idx < KC * n; idx += kThreads) {
-        const int rr = idx / n, cc = idx - rr * n;
-        xst[idx] = rr < rows ? a.x[(s0 + rr) * a.ldx + cc] : 0.0;
-      }
-      __syncthreads();
-    }
-  };
   auto build = [&](int c) {  // Khatri-Rao factors of chunk c -> kra/krb[c & 1]
-    const double *xst = xs + (c & 1) * KC * n;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      BCG_CHECK(colA[q] >= (ONES ? -1 : 0) && colA[q] < n, "colA", colA[q]);
-      BCG_CHECK(colB[q] >= (ONES ? -1 : 0) && colB[q] < n, "colB", colB[q]);
-    }
+    mbar_wait(&bar[c & 1], (uint32_t)((c >> 1) & 1));
+    const double *xst = xs + (c & 1) * xrows * LDX;
     {
-      double *wa = kra + (c & 1) * KC * LDA + pa0 * LDA + ia;
-      const double *xr = xst + pa0 * n;
+      const double *ra[8];
+      int sa[8];
 #pragma unroll
-      for (int k = 0; k < KC / PA; ++k) {
-        const double p = kr_prod<H, ONES>(xr, colA, a.h);
-        wa[k * PA * LDA] = okA ? p : 0.0;
-        xr += PA * n;
+      for (int q = 0; q < 8; ++q) {
+        ra[q] = xst + colA[q] * LDX;
+        sa[q] = colA[q] & 7;
+      }
+      double *wa = kra + (c & 1) * TM * LDK + ia * LDK;
+      const int swa = (ia & 3) << 2;
+#pragma unroll
+      for (int i = 0; i < SH::NPAIR / SH::PA; ++i) {
+        const int j = pa0 + SH::PA * i;
+        const double2 p = kr_pair<H>(ra, sa, a.h, j);
+        *reinterpret_cast<double2 *>(wa + ((2 * j) ^ swa)) = p;
       }
     }
     {
-      double *wb = krb + (c & 1) * KC * LDB + pb0 * LDB + ib;
-      const double *xr = xst + pb0 * n;
+      const double *rb[8];
+      int sb[8];
 #pragma unroll
-      for (int k = 0; k < KC / PB; ++k) {
-        const double p = kr_prod<R, ONES>(xr, colB, a.r);
-        wb[k * PB * LDB] = okB ? p : 0.0;
-        xr += PB * n;
+      for (int q = 0; q < 8; ++q) {
+        rb[q] = xst + colB[q] * LDX;
+        sb[q] = colB[q] & 7;
+      }
+      double *wb = krb + (c & 1) * TN * LDK + ib * LDK;
+      const int swb = (ib & 3) << 2;
+#pragma unroll
+      for (int i = 0; i < SH::NPAIR / SH::PB; ++i) {
+        const int j = pb0 + SH::PB * i;
+        const double2 p = kr_pair<R>(rb, sb, a.r, j);
+        *reinterpret_cast<double2 *>(wb + ((2 * j) ^ swb)) = p;
       }
     }
   };
 
   if (nch > 0) {
-    if (tid == 0) {
-      if (chunk_full(0)) issue(0);
-      if (nch > 1 && chunk_full(1)) issue(1);
-    }
-    load_x(0);
+    issue(0);
+    if (nch > 1) issue(1);
     build(0);
-    __syncthreads();
-    if (tid == 0 && nch > 2 && chunk_full(2)) issue(2);
+    __syncthreads();  // KR[0] complete, xs[0] free
+    if (nch > 2) issue(2);
   }
   for (int c = 0; c < nch; ++c) {
-    if (c + 1 < nch) {
-      load_x(c + 1);
-      build(c + 1);
-    }
+    if (c + 1 < nch) build(c + 1);
     // ---- DMMA over chunk c ----
-    const double *ka = kra + (c & 1) * KC * LDA;
-    const double *kb = krb + (c & 1) * KC * LDB;
+    // fragment rows = gid (mod 4 after the 8-row and warp offsets): swizzle (gid & 3) << 2
+    const int swf = (gid & 3) << 2;
+    const double *ka = kra + (c & 1) * TM * LDK + (wm * SH::WM + gid) * LDK + tig;
+    const double *kb = krb + (c & 1) * TN * LDK + (wn * SH::WN + gid) * LDK + tig;
 #pragma unroll
     for (int k = 0; k < KC; k += 4) {
       double fa[MT], fb[NT];
-      const double *pa = ka + (k + tig) * LDA + wm * SH::WM + gid;
-      const double *pb = kb + (k + tig) * LDB + wn * SH::WN + gid;
+      const int ks = k ^ swf;
 #pragma unroll
-      for (int i = 0; i < MT; ++i) fa[i] = pa[8 * i];
+      for (int i = 0; i < MT; ++i) fa[i] = ka[8 * i * LDK + ks];
 #pragma unroll
-      for (int j = 0; j < NT; ++j) fb[j] = pb[8 * j];
+      for (int j = 0; j < NT; ++j) fb[j] = kb[8 * j * LDK + ks];
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int j = 0; j < NT; ++j) dmma884(acc[i][j], fa[i], fb[j]);
     }
     __syncthreads();  // KR[c+1] complete, KR[c] and xs[(c+1) & 1] free
-    if (tid == 0 && c + 3 < nch && chunk_full(c + 3)) issue(c + 3);
+    if (c + 3 < nch) issue(c + 3);
   }
 
   // ---- epilogue: scatter to packed addresses ----
@@ -260,7 +302,6 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(MomentArgs a) {
         if (base < 0) continue;            // fused plan: orders 0 / 1 are not produced
         const int64_t addr = base + (int64_t)ro * a.col_size[col] + a.col_olin[col];
         BCG_CHECK(addr >= 0 && addr < a.S, "epilogue address", addr);
-        BCG_CHECK(key >= 0, "key", key);
         if (accumulate)
           dst[addr] += acc[i][j][e];
         else
@@ -284,32 +325,62 @@ __global__ void k_reduce_slices(const double *__restrict__ ws, int nslices, int6
 }
 
 size_t moment_smem_bytes(int KC, int n, int tm, int tn) {
-  return sizeof(double) * (2 * (size_t)KC * n + 2 * (size_t)KC * (tm + kPad) + 2 * (size_t)KC * (tn + kPad)) +
-         2 * sizeof(uint64_t);
+  const size_t xrows = (size_t)(n + 1 + 7) / 8 * 8;
+  return sizeof(double) * (2 * xrows * KC + 2 * (size_t)(tm + tn) * KC) + 2 * sizeof(uint64_t) +
+         1024;  // + alignment slack for the 1024-byte swizzle atoms
 }
 
-int pick_kc(int n) {  // sample-chunk length for the 64x64 tile
-  // keep the double-buffered sample stage <= 96 KB so >= 2 CTAs fit per SM
-  if (2 * 16 * (size_t)n * 8 <= 96 * 1024) return 16;
-  if (2 * 8 * (size_t)n * 8 <= 96 * 1024) return 8;
-  if (2 * 4 * (size_t)n * 8 <= 160 * 1024) return 4;
-  return 0;
+int pick_kc(int n) {  // 16-sample chunks (one 128-byte swizzle span) while they fit
+  return moment_smem_bytes(16, n, 64, 64) <= 227 * 1024 ? 16 : 0;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D map over xt (inner: padded samples, outer: variables), box 16 x min(n, 256),
+// 128-byte swizzle
+static cudaError_t make_xt_map(const MomentArgs &a, CUtensorMap *map) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  cuuint64_t dims[2] = {(cuuint64_t)a.ldx, (cuuint64_t)a.n};
+  cuuint64_t strides[1] = {(cuuint64_t)a.ldx * sizeof(double)};
+  cuuint32_t box[2] = {16, (cuuint32_t)(a.n < 256 ? a.n : 256)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(a.x), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 template <int KC, int M, int TM, int TN>
 static cudaError_t go_v1(const MomentArgs &args, int grid, cudaStream_t stream) {
   const size_t smem = moment_smem_bytes(KC, args.n, TM, TN);
-  auto kern = args.ones ? k_moment_dmma<KC, M, true, TM, TN> : k_moment_dmma<KC, M, false, TM, TN>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = k_moment_dmma<KC, M, TM, TN>;
+  CUtensorMap map;
+  cudaError_t e = make_xt_map(args, &map);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kThreads, smem, stream>>>(args);
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kThreads, smem, stream>>>(map, args);
   return cudaGetLastError();
 }
 
-// v1 tile shapes: 64x64 for every KC / order; the thin / small shapes
+// tile shapes: 64x64 for every KC / order; the thin / small shapes
 // (staircase-friendly, chosen per plan by the tile model) for KC = 16 and
 // orders 2..8.
 bool v1_shape_supported(int KC, int m, int tm, int tn) {
+  if (KC != 16) return false;
   if (tm == 64 && tn == 64) return true;
   if (KC != 16 || m < 2 || m > 8) return false;
   return (tm == 16 && tn == 128) || (tm == 128 && tn == 16) || (tm == 32 && tn == 64) ||
@@ -320,8 +391,8 @@ cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t
   static const bool generic = getenv("BCG_FORCE_GENERIC_M") != nullptr;  // debug knob
   const int m = generic ? 0 : args.h + args.r;
   cudaError_t e = cudaErrorInvalidValue;
+  if (!v1_shape_supported(KC, m < 2 ? 2 : m, tm, tn)) return cudaErrorInvalidValue;
   if (!(tm == 64 && tn == 64)) {
-    if (!v1_shape_supported(KC, m, tm, tn)) return cudaErrorInvalidValue;
 #define GOS(M, TMV, TNV) e = go_v1<16, M, TMV, TNV>(args, grid, stream)
 #define SHAPE(TMV, TNV)                                   \
   if (tm == TMV && tn == TNV) {                           \
@@ -347,17 +418,8 @@ cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t
     return e;
   }
 #define GO16(M, ...) e = go_v1<16, M, 64, 64>(args, grid, stream)
-#define GO8(M, ...) e = go_v1<8, M, 64, 64>(args, grid, stream)
-#define GO4(M, ...) e = go_v1<4, M, 64, 64>(args, grid, stream)
-  switch (KC) {
-    case 16: BCG_DISPATCH_M(m, GO16, 0) break;
-    case 8: BCG_DISPATCH_M(m, GO8, 0) break;
-    case 4: BCG_DISPATCH_M(m, GO4, 0) break;
-    default: break;
-  }
+  BCG_DISPATCH_M(m, GO16, 0)
 #undef GO16
-#undef GO8
-#undef GO4
   return e;
 }
 

@@ -105,7 +105,7 @@ std::vector<std::vector<std::vector<int>>> partitions_min2(int m, int sigma) {
 
 static void build_fact_tables(Plan &p);
 
-int default_variant() {
+int default_variant() {  // only the v1 kernel family (variant 0) remains
   const char *env = std::getenv("BCG_MOMENT_VARIANT");
   if (env && *env) return std::atoi(env);
   return 0;
@@ -185,7 +185,8 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant, bool fused
   if (n < 1 || m < 1 || b < 1) return "n, m and b must all be >= 1";
   p.fused = fused;
   p.variant = variant < 0 ? default_variant() : variant;
-  ws_tile_shape(p.variant, &p.tm, &p.tn);
+  p.tm = kTM;
+  p.tn = kTN;
   if (m > 16) return "kernel supports 2 <= m <= 16";
   p.n = n;
   p.m = m;

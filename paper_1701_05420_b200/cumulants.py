@@ -17,11 +17,13 @@ from . import _native
 from .errors import ValidationError
 from .layout import MAX_M, enumerate_partitions_min2, layout
 from .moments import (
-    _center_device,
+    _center_transposed,
     _colstats,
     _device_matrix,
     _moment_device,
+    _moment_device_t,
     _raise_if_nonfinite,
+    _rowstats,
     as_data_matrix,
     resolve_engine,
 )
@@ -166,28 +168,30 @@ class CumulantSet:
 def cumulants_device(X, m_max: int, b: int, c1_host: bool = True, timer: dict | None = None):
     """Core of cumulants_upto on a device matrix: returns (c1, [C_2..C_m]).
 
-    One colstats pass (means + finite scan), one centering pass, one
-    centering check, then per order one moment GEMM and one in-place
-    recursion -- the reference's sequence (bc/cumulants.py:182-193) without
-    its repeated validation scans.  ``timer`` (bench.py) collects CUDA events
-    around the top-order moment launch.
+    One colstats pass (means + finite scan), one pass that centers and
+    transposes into the moment kernel's layout (the reference's xt,
+    bc/_engines.py:95), one centering check, then per order one moment GEMM
+    and one in-place recursion -- the reference's sequence
+    (bc/cumulants.py:182-193) without its repeated validation scans.
+    ``timer`` (bench.py) collects CUDA events around the top-order moment.
     """
     t, n = X.shape
     st = _colstats(X, mean=True, bad=True)
     _raise_if_nonfinite(X, st["bad"])
     tensors: list[BlockSymTensor] = []
     if m_max >= 2:
-        Xc = _center_device(X, st["mean"])
-        _check_centered(Xc)
+        xt = _center_transposed(X, st["mean"])
+        sums, sq = _rowstats(xt, t)
+        _check_centered_stats(sums, sq, t)
         central: dict = {}  # central moments M_4.. kept for the factored recursion
         for k in range(2, m_max + 1):
             if timer is not None and k == m_max:
                 torch = _native.torch_cuda()
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 timer.setdefault("moment_top", []).append(ev)
-                Mk = _moment_device(Xc, k, b, events=ev)
+                Mk = _moment_device_t(xt, t, k, b, events=ev)
             else:
-                Mk = _moment_device(Xc, k, b)
+                Mk = _moment_device_t(xt, t, k, b)
             if 4 <= k <= m_max - 2:
                 central[k] = Mk.data.clone()
             if k >= 4:

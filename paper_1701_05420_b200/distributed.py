@@ -61,15 +61,22 @@ class CudaOps:
         return st["sums"], st["sumsq"], st["bad"]
 
     def center(self, X, mean):
-        from .moments import _center_device
+        """Centered data in the moment kernel's transposed layout: (xt, t)."""
+        from .moments import _center_transposed
 
-        return _center_device(X, mean)
+        return _center_transposed(X, mean), X.shape[0]
 
-    def moment_raw(self, X, k: int, b: int):
-        from .moments import _moment_raw_into
+    def centered_stats(self, centered):
+        from .moments import _rowstats
 
-        out = torch.zeros(layout(X.shape[1], k, b).size, dtype=torch.float64, device=X.device)
-        _moment_raw_into(X, k, b, out)
+        return _rowstats(*centered)
+
+    def moment_raw(self, centered, k: int, b: int):
+        from .moments import _moment_raw_t_into
+
+        xt, t = centered
+        out = torch.zeros(layout(xt.shape[0], k, b).size, dtype=torch.float64, device=xt.device)
+        _moment_raw_t_into(xt, t, k, b, out)
         return out
 
     def divide(self, buf, t: int):
@@ -127,7 +134,7 @@ def cumulants_upto_sharded(x_local, m_max: int, b: int = 2, group=None, ops=None
     tensors = []
     if m_max >= 2:
         Xc = ops.center(X, mean)
-        csum, csq, _ = ops.colstats(Xc)
+        csum, csq = ops.centered_stats(Xc)
         both = torch.cat([csum, csq])
         dist.all_reduce(both, group=group)
         _check_centered(both[:n], both[n:], t_total)

@@ -124,6 +124,56 @@ def _moment_raw_into(X, m: int, b: int, out, key_range=None) -> None:
     _native.check(rc, "moment")
 
 
+def _center_transposed(X, mean):
+    """Xc^T: centered (mean may be None) and transposed into the moment
+    kernel's padded layout (n x padded_t(t)) in one pass (bcg_transpose_pad)."""
+    torch = _native.torch_cuda()
+    t, n = X.shape
+    lib = _native.lib()
+    ldt = int(lib.bcg_padded_t(t))
+    xt = torch.empty((n, ldt), dtype=torch.float64, device=X.device)
+    _native.check(lib.bcg_transpose_pad(X.data_ptr(), t, n, n, mean.data_ptr() if mean is not None else None,
+                                        xt.data_ptr(), ldt, _native.stream_handle()), "center")
+    return xt
+
+
+def _rowstats(xt, t: int):
+    """Column sums / sums of squares of the data from its transposed layout."""
+    torch = _native.torch_cuda()
+    n, ldt = xt.shape
+    sums = torch.empty(n, dtype=torch.float64, device=xt.device)
+    sq = torch.empty(n, dtype=torch.float64, device=xt.device)
+    _native.check(_native.lib().bcg_rowstats(xt.data_ptr(), n, t, ldt, sums.data_ptr(), sq.data_ptr(),
+                                             _native.stream_handle()), "rowstats")
+    return sums, sq
+
+
+def _moment_raw_t_into(xt, t: int, m: int, b: int, out) -> None:
+    """Accumulate packed RAW order-m sums from the transposed layout."""
+    torch = _native.torch_cuda()
+    n, ldt = xt.shape
+    plan = _native.plan(n, m, b)
+    wsb = plan.ws_bytes(t)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=xt.device) if wsb else None
+    _native.check(_native.lib().bcg_moment_raw_t(plan.handle, xt.data_ptr(), t, ldt, out.data_ptr(),
+                                                 ws.data_ptr() if ws is not None else None, wsb,
+                                                 _native.stream_handle()), "moment")
+
+
+def _moment_device_t(xt, t: int, m: int, b: int, events=None) -> BlockSymTensor:
+    """Order-m moment from the transposed layout (m >= 2)."""
+    torch = _native.torch_cuda()
+    n = xt.shape[0]
+    out = torch.zeros(layout(n, m, b).size, dtype=torch.float64, device=xt.device)
+    if events is not None:
+        events[0].record()
+    _moment_raw_t_into(xt, t, m, b, out)
+    if events is not None:
+        events[1].record()
+    _divide(out, t)
+    return BlockSymTensor(n, m, b, data=out)
+
+
 def _divide(buf, t: int) -> None:
     _native.check(_native.lib().bcg_div(buf.numel(), buf.data_ptr(), float(t), buf.data_ptr(),
                                         _native.stream_handle()), "scale")

@@ -32,6 +32,10 @@ class OracleOps:
     def center(self, X, mean):
         return X - mean
 
+    def centered_stats(self, Xc):
+        s, q, _ = self.colstats(Xc)
+        return s, q
+
     def moment_raw(self, X, k, b):
         return torch.as_tensor(orc.moment_raw_sums(X.numpy(), k, b))
 
