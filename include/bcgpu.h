@@ -84,10 +84,17 @@ int bcg_plan_create_ex(int64_t n, int32_t m, int32_t b, int32_t variant,
  * (bcg_plan_output).  host_only != 0: tables only (layout / selfcheck). */
 int bcg_plan_create_fused(int64_t n, int32_t m, int32_t b, int32_t host_only,
                           bcg_plan **plan);
-/* Moment-kernel choice of the plan: variant (0 = v1), CTA tile tm x tn
- * (picked per plan by the staircase tile model) and the number of tiles. */
+/* Moment-kernel choice of the plan: variant (0 = v1), CTA tile tm x tn of
+ * its first GEMM (picked per GEMM by the staircase tile model) and the number
+ * of tiles over all its GEMMs. */
 int bcg_plan_kernel(const bcg_plan *plan, int32_t *variant, int32_t *tm,
                     int32_t *tn, int64_t *ntiles);
+/* The plan's moment GEMMs: 1, or 2 for a hybrid odd-order plan (keys split
+ * by their middle entry at split_T: key[h] >= T -> an (h | m-h) GEMM, else
+ * (h+1 | m-h-1)).  Gemm i (< *ngemm) is described by info[0..3] = h, r, tm,
+ * tn and *ntiles; pass i < 0 to query only *ngemm and *split_T. */
+int bcg_plan_gemm(const bcg_plan *plan, int32_t i, int32_t *ngemm, int32_t *split_T,
+                  int32_t *info, int64_t *ntiles);
 /* Output size of bcg_moment_raw on this plan (S_m, or S_2 + ... + S_m for a
  * fused plan) and, if order_base != NULL (m + 2 entries), each order's start
  * offset in it (fused plans; zeros otherwise, order_base[m + 1] = S_out). */

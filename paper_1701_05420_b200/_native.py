@@ -39,6 +39,8 @@ SIGNATURES = [
     ("bcg_plan_output", ctypes.c_int, [_vp, ctypes.POINTER(_i64), _vp]),
     ("bcg_plan_kernel", ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                                        ctypes.POINTER(_i64)]),
+    ("bcg_plan_gemm", ctypes.c_int, [_vp, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32), _vp,
+                                     ctypes.POINTER(_i64)]),
     ("bcg_plan_create_host", ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(_vp)]),
     ("bcg_plan_destroy", ctypes.c_int, [_vp]),
     ("bcg_plan_selfcheck", ctypes.c_int, [_vp]),
@@ -172,6 +174,17 @@ class Plan:
         check(self._lib.bcg_plan_kernel(self._h, ctypes.byref(v), ctypes.byref(tm), ctypes.byref(tn),
                                         ctypes.byref(nt)))
         return v.value, tm.value, tn.value, nt.value
+
+    def gemms(self):
+        """(split_T, [(h, r, tm, tn, ntiles), ...]) of the plan's moment GEMMs."""
+        ng, T = _i32(), _i32()
+        check(self._lib.bcg_plan_gemm(self._h, -1, ctypes.byref(ng), ctypes.byref(T), None, None))
+        out = []
+        for i in range(ng.value):
+            info, nt = (_i32 * 4)(), _i64()
+            check(self._lib.bcg_plan_gemm(self._h, i, None, None, info, ctypes.byref(nt)))
+            out.append((*info, nt.value))
+        return T.value, out
 
     def ws_bytes(self, t: int) -> int:
         out = _sz()

@@ -57,14 +57,15 @@ constexpr int64_t kWsCap = (int64_t)2 << 30;  // 2 GiB of split-K partials at mo
 
 Slicing choose_slicing(const bcg::Plan &p, int64_t t) {
   Slicing s{bcg::pick_kc((int)p.n), 1, 1, bcg::kSliceLen};
-  if (s.KC != 0 && !(p.tm == 64 && p.tn == 64)) s.KC = 16;
   if (s.KC == 0 || t <= 0) return s;
   s.nslices = (int)((t + bcg::kSliceLen - 1) / bcg::kSliceLen);
   // slices per launch: as many as the workspace cap allows (fewest launches,
   // no small tail launch), balanced across launches; a plan with enough tiles
   // to fill the GPU by itself (>= 8 waves) runs one slice per launch and
   // accumulates straight into `out` (no workspace, no reduce pass).
-  const int64_t ntiles = std::max<int64_t>(1, (int64_t)p.tiles.size());
+  int64_t ntiles = 0;
+  for (const bcg::Gemm &g : p.gemm) ntiles += (int64_t)g.tiles.size();
+  ntiles = std::max<int64_t>(1, ntiles);
   const int64_t S = p.S_out;
   int64_t cap = kWsCap / std::max<int64_t>(1, S * 8);
   if (ntiles >= 8 * 148 * 4) cap = 1;
@@ -100,24 +101,8 @@ int run_moment(const bcg::Plan &p, const double *xt, int64_t t, int64_t ldt, dou
   a.t = t;
   a.ldx = ldt;
   a.n = (int)p.n;
-  a.h = p.h;
-  a.r = p.r;
-  a.rowcols = p.d_rowcols;
-  a.colcols = p.d_colcols;
-  a.row_keybase = p.d_row_keybase;
-  a.row_olin = p.d_row_olin;
-  a.row_cstart = p.d_row_cstart;
-  a.col_rank = p.d_col_rank;
-  a.col_olin = p.d_col_olin;
-  a.col_size = p.d_col_size;
   a.offs = p.d_koff;
   a.ones = p.fused ? 1 : 0;
-  a.tiles = p.d_tiles;
-  a.tile_kmin = p.d_tile_kmin;
-  a.tile_kmax = p.d_tile_kmax;
-  a.ntiles = (int)p.tiles.size();
-  a.R = p.R;
-  a.C = p.C;
   a.nslices_total = sl.nslices;
   a.slice_len = sl.slice_len;
   a.out = out;
@@ -131,10 +116,31 @@ int run_moment(const bcg::Plan &p, const double *xt, int64_t t, int64_t ldt, dou
   for (int g0 = 0; g0 < sl.nslices; g0 += sl.group) {
     a.slice0 = g0;
     a.nslices = std::min(sl.group, sl.nslices - g0);
-    const int64_t grid = (int64_t)a.ntiles * a.nslices;
-    if (grid > INT32_MAX) return fail(BCG_EINVAL, "moment grid too large");
-    CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream, p.tm, p.tn), "moment kernel");
-    bcg::g_launches++;
+    // every GEMM of the plan writes a disjoint set of keys of the same slice
+    // partials, so one reduce pass follows them all
+    for (const bcg::Gemm &g : p.gemm) {
+      if (g.tiles.empty()) continue;
+      a.h = g.h;
+      a.r = g.r;
+      a.rowcols = g.d_rowcols;
+      a.colcols = g.d_colcols;
+      a.row_keybase = g.d_row_keybase;
+      a.row_olin = g.d_row_olin;
+      a.row_cstart = g.d_row_cstart;
+      a.col_rank = g.d_col_rank;
+      a.col_olin = g.d_col_olin;
+      a.col_size = g.d_col_size;
+      a.tiles = g.d_tiles;
+      a.tile_kmin = g.d_tile_kmin;
+      a.tile_kmax = g.d_tile_kmax;
+      a.ntiles = (int)g.tiles.size();
+      a.R = g.R;
+      a.C = g.C;
+      const int64_t grid = (int64_t)a.ntiles * a.nslices;
+      if (grid > INT32_MAX) return fail(BCG_EINVAL, "moment grid too large");
+      CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream, g.tm, g.tn), "moment kernel");
+      bcg::g_launches++;
+    }
     if (a.nslices > 1) {
       CUDA_TRY(bcg::launch_reduce_slices(a.ws, a.nslices, a.S, lo, hi, out, stream),
                "split-K reduce");
@@ -203,9 +209,33 @@ int bcg_plan_create_fused(int64_t n, int32_t m, int32_t b, int32_t host_only, bc
 int bcg_plan_kernel(const bcg_plan *plan, int32_t *variant, int32_t *tm, int32_t *tn, int64_t *ntiles) {
   if (!plan) return fail(BCG_EINVAL, "plan is NULL");
   if (variant) *variant = plan->p.variant;
-  if (tm) *tm = plan->p.tm;
-  if (tn) *tn = plan->p.tn;
-  if (ntiles) *ntiles = (int64_t)plan->p.tiles.size();
+  // the first (largest) GEMM's tile shape; tiles summed over the GEMMs
+  const bcg::Gemm *g0 = plan->p.gemm.empty() ? nullptr : &plan->p.gemm[0];
+  if (tm) *tm = g0 ? g0->tm : 0;
+  if (tn) *tn = g0 ? g0->tn : 0;
+  if (ntiles) {
+    *ntiles = 0;
+    for (const bcg::Gemm &g : plan->p.gemm) *ntiles += (int64_t)g.tiles.size();
+  }
+  return BCG_OK;
+}
+
+int bcg_plan_gemm(const bcg_plan *plan, int32_t i, int32_t *ngemm, int32_t *split_T, int32_t *info,
+                  int64_t *ntiles) {
+  if (!plan) return fail(BCG_EINVAL, "plan is NULL");
+  const bcg::Plan &p = plan->p;
+  if (ngemm) *ngemm = (int32_t)p.gemm.size();
+  if (split_T) *split_T = p.split_T;
+  if (i < 0) return BCG_OK;
+  if (i >= (int32_t)p.gemm.size()) return fail(BCG_EINVAL, "gemm index out of range");
+  const bcg::Gemm &g = p.gemm[i];
+  if (info) {
+    info[0] = g.h;
+    info[1] = g.r;
+    info[2] = g.tm;
+    info[3] = g.tn;
+  }
+  if (ntiles) *ntiles = (int64_t)g.tiles.size();
   return BCG_OK;
 }
 
@@ -225,14 +255,15 @@ int bcg_plan_selfcheck(const bcg_plan *plan) {
   if (p.m < 2) return BCG_OK;
   const int64_t S = p.S_out;
   std::vector<uint8_t> seen(S, 0);
-  for (const bcg::Tile &tl : p.tiles) {
-    for (int64_t r = tl.row0; r < std::min<int64_t>(tl.row0 + p.tm, p.R); ++r) {
-      for (int64_t c = tl.col0; c < std::min<int64_t>(tl.col0 + p.tn, p.C); ++c) {
-        if (c < p.row_cstart[r]) continue;
-        const int64_t kg = p.row_keybase[r] + p.col_rank[c];
+  for (const bcg::Gemm &g : p.gemm)
+  for (const bcg::Tile &tl : g.tiles) {
+    for (int64_t r = tl.row0; r < std::min<int64_t>(tl.row0 + g.tm, g.R); ++r) {
+      for (int64_t c = tl.col0; c < std::min<int64_t>(tl.col0 + g.tn, g.C); ++c) {
+        if (c < g.row_cstart[r]) continue;
+        const int64_t kg = g.row_keybase[r] + g.col_rank[c];
         if (kg < 0 || kg >= (int64_t)p.koff.size()) return fail(BCG_EINVAL, "selfcheck: key index out of range");
         if (p.koff[kg] < 0) continue;  // fused: order 0 / 1 element
-        const int64_t lin = (int64_t)p.row_olin[r] * p.col_size[c] + p.col_olin[c];
+        const int64_t lin = (int64_t)g.row_olin[r] * g.col_size[c] + g.col_olin[c];
         const int64_t addr = p.koff[kg] + lin;
         // locate (order, block) of addr and check the element's data columns
         int o = p.m;
@@ -254,10 +285,10 @@ int bcg_plan_selfcheck(const bcg_plan *plan) {
         }
         // the GEMM element's columns, ones (-1) removed, must equal (key, offsets)'s
         int64_t got[16], ng = 0;
-        for (int q = 0; q < p.h; ++q)
-          if (p.rowcols[r * p.h + q] >= 0) got[ng++] = p.rowcols[r * p.h + q];
-        for (int q = 0; q < p.r; ++q)
-          if (p.colcols[c * p.r + q] >= 0) got[ng++] = p.colcols[c * p.r + q];
+        for (int q = 0; q < g.h; ++q)
+          if (g.rowcols[r * g.h + q] >= 0) got[ng++] = g.rowcols[r * g.h + q];
+        for (int q = 0; q < g.r; ++q)
+          if (g.colcols[c * g.r + q] >= 0) got[ng++] = g.colcols[c * g.r + q];
         if (ng != o) return fail(BCG_EINVAL, "selfcheck: order mismatch");
         for (int q = 0; q < o; ++q)
           if (got[q] != cols[q]) return fail(BCG_EINVAL, "selfcheck: column mismatch");
@@ -348,7 +379,7 @@ int bcg_moment_raw(const bcg_plan *plan, const double *x, int64_t t, int64_t ldx
   const bcg::Plan &p = plan->p;
   if (p.m < 2 || p.m > 16) return fail(BCG_EINVAL, "kernel supports 2 <= m <= 16");
   if (ldx < p.n) return fail(BCG_EINVAL, "ldx < n");
-  if (!p.d_tiles) return fail(BCG_EINVAL, "host-only plan");
+  if (!p.d_koff) return fail(BCG_EINVAL, "host-only plan");
   return moment_rowmajor(p, x, t, ldx, out, ws, ws_bytes, 0, p.lay[p.m].K, static_cast<cudaStream_t>(stream));
 }
 
@@ -357,7 +388,7 @@ int bcg_moment_raw_t(const bcg_plan *plan, const double *xt, int64_t t, int64_t 
   if (!plan) return fail(BCG_EINVAL, "plan is NULL");
   const bcg::Plan &p = plan->p;
   if (p.m < 2 || p.m > 16) return fail(BCG_EINVAL, "kernel supports 2 <= m <= 16");
-  if (!p.d_tiles) return fail(BCG_EINVAL, "host-only plan");
+  if (!p.d_koff) return fail(BCG_EINVAL, "host-only plan");
   return run_moment(p, xt, t, ldt, out, ws, ws_bytes, 0, p.lay[p.m].K, static_cast<cudaStream_t>(stream));
 }
 
@@ -367,7 +398,7 @@ int bcg_moment_raw_range(const bcg_plan *plan, const double *x, int64_t t, int64
   const bcg::Plan &p = plan->p;
   if (p.m < 2 || p.m > 16) return fail(BCG_EINVAL, "kernel supports 2 <= m <= 16");
   if (ldx < p.n) return fail(BCG_EINVAL, "ldx < n");
-  if (!p.d_tiles) return fail(BCG_EINVAL, "host-only plan");
+  if (!p.d_koff) return fail(BCG_EINVAL, "host-only plan");
   k0 = std::max<int64_t>(k0, 0);
   k1 = std::min<int64_t>(k1, p.lay[p.m].K);
   if (k1 <= k0) return BCG_OK;

@@ -43,6 +43,10 @@
 #include "kr.cuh"
 #include "plan.h"
 
+#ifndef BCG_MOMENT_PART
+#error "moment.cu is compiled once per BCG_MOMENT_PART (0..6), see _build.py"
+#endif
+
 namespace bcg {
 
 constexpr int kThreads = 128;
@@ -135,10 +139,10 @@ __device__ __forceinline__ double2 kr_pair(const double *const (&row)[8], const 
   return p;
 }
 
-template <int KC, int M, int TM, int TN>
+// H, R: compile-time row / column mode counts (0: the runtime a.h / a.r)
+template <int KC, int H, int R, int TM, int TN>
 __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant__ CUtensorMap tmap, MomentArgs a) {
   using SH = V1Shape<KC, TM, TN>;
-  constexpr int H = M / 2, R = M - M / 2;  // compile-time mode counts (0: runtime)
   constexpr int LDX = KC;                  // staged row: 16 doubles = one 128-byte swizzle span
   constexpr int LDK = SH::LDK, MT = SH::MT, NT = SH::NT;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -311,6 +315,8 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
   }
 }
 
+#if BCG_MOMENT_PART == 0
+// ---- part 0: shape-independent host code, the split-K reduce, dispatch ----
 // out[i] = ((out[i] + ws[0][i]) + ws[1][i]) + ...  for i in [lo, hi): the
 // slices of one group added sequentially, so the association of the whole
 // split-K sum is the same for any grouping of the slices.
@@ -334,6 +340,51 @@ int pick_kc(int n) {  // 16-sample chunks (one 128-byte swizzle span) while they
   return moment_smem_bytes(16, n, 64, 64) <= 227 * 1024 ? 16 : 0;
 }
 
+// tile shapes: 64x64 for every KC / order; the thin / small shapes
+// (staircase-friendly, chosen per plan by the tile model) for KC = 16 and
+// orders 2..8.
+bool v1_shape_supported(int KC, int m, int tm, int tn) {
+  if (KC != 16) return false;
+  if (tm == 64 && tn == 64) return true;
+  if (m < 2 || m > 8) return false;
+  return (tm == 16 && tn == 128) || (tm == 128 && tn == 16) || (tm == 32 && tn == 64) ||
+         (tm == 64 && tn == 32) || (tm == 32 && tn == 32);
+}
+
+#define BCG_SHAPE_DECL(TMV, TNV) \
+  cudaError_t launch_moment_##TMV##x##TNV(const MomentArgs &args, int grid, cudaStream_t stream, bool generic);
+BCG_SHAPE_DECL(64, 64)
+BCG_SHAPE_DECL(16, 128)
+BCG_SHAPE_DECL(128, 16)
+BCG_SHAPE_DECL(32, 64)
+BCG_SHAPE_DECL(64, 32)
+BCG_SHAPE_DECL(32, 32)
+#undef BCG_SHAPE_DECL
+
+cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t stream, int tm, int tn) {
+  static const bool generic = getenv("BCG_FORCE_GENERIC_M") != nullptr;  // debug knob
+  const int h = args.h, r = args.r;
+  if (KC != 16 || h < 1 || r < 1 || h > 8 || r > 8) return cudaErrorInvalidValue;
+  if (!v1_shape_supported(KC, h + r, tm, tn)) return cudaErrorInvalidValue;
+#define GO(TMV, TNV) \
+  if (tm == TMV && tn == TNV) return launch_moment_##TMV##x##TNV(args, grid, stream, generic);
+  GO(64, 64) GO(16, 128) GO(128, 16) GO(32, 64) GO(64, 32) GO(32, 32)
+#undef GO
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_reduce_slices(const double *ws, int nslices, int64_t S, int64_t lo, int64_t hi,
+                                 double *out, cudaStream_t stream) {
+  if (hi <= lo) return cudaSuccess;
+  int64_t blocks = (hi - lo + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_reduce_slices<<<(int)blocks, 256, 0, stream>>>(ws, nslices, S, lo, hi, out);
+  return cudaGetLastError();
+}
+
+#else
+// ---- parts 1..6: the kernel instantiations of one CTA tile shape each
+// (separate translation units so nvcc compiles them in parallel) ----
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -363,10 +414,10 @@ static cudaError_t make_xt_map(const MomentArgs &a, CUtensorMap *map) {
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int KC, int M, int TM, int TN>
+template <int KC, int H, int R, int TM, int TN>
 static cudaError_t go_v1(const MomentArgs &args, int grid, cudaStream_t stream) {
   const size_t smem = moment_smem_bytes(KC, args.n, TM, TN);
-  auto kern = k_moment_dmma<KC, M, TM, TN>;
+  auto kern = k_moment_dmma<KC, H, R, TM, TN>;
   CUtensorMap map;
   cudaError_t e = make_xt_map(args, &map);
   if (e != cudaSuccess) return e;
@@ -376,60 +427,45 @@ static cudaError_t go_v1(const MomentArgs &args, int grid, cudaStream_t stream) 
   return cudaGetLastError();
 }
 
-// tile shapes: 64x64 for every KC / order; the thin / small shapes
-// (staircase-friendly, chosen per plan by the tile model) for KC = 16 and
-// orders 2..8.
-bool v1_shape_supported(int KC, int m, int tm, int tn) {
-  if (KC != 16) return false;
-  if (tm == 64 && tn == 64) return true;
-  if (KC != 16 || m < 2 || m > 8) return false;
-  return (tm == 16 && tn == 128) || (tm == 128 && tn == 16) || (tm == 32 && tn == 64) ||
-         (tm == 64 && tn == 32) || (tm == 32 && tn == 32);
-}
-
-cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t stream, int tm, int tn) {
-  static const bool generic = getenv("BCG_FORCE_GENERIC_M") != nullptr;  // debug knob
-  const int m = generic ? 0 : args.h + args.r;
-  cudaError_t e = cudaErrorInvalidValue;
-  if (!v1_shape_supported(KC, m < 2 ? 2 : m, tm, tn)) return cudaErrorInvalidValue;
-  if (!(tm == 64 && tn == 64)) {
-#define GOS(M, TMV, TNV) e = go_v1<16, M, TMV, TNV>(args, grid, stream)
-#define SHAPE(TMV, TNV)                                   \
-  if (tm == TMV && tn == TNV) {                           \
-    switch (m) {                                          \
-      case 2: GOS(2, TMV, TNV); break;                    \
-      case 3: GOS(3, TMV, TNV); break;                    \
-      case 4: GOS(4, TMV, TNV); break;                    \
-      case 5: GOS(5, TMV, TNV); break;                    \
-      case 6: GOS(6, TMV, TNV); break;                    \
-      case 7: GOS(7, TMV, TNV); break;                    \
-      case 8: GOS(8, TMV, TNV); break;                    \
-      default: break;                                     \
-    }                                                     \
-    return e;                                             \
+// (h | r) splits with a compiled specialization: the balanced split of every
+// order 2..8 and, for odd orders, its mirror (the second GEMM of a hybrid plan);
+// other splits (orders 9..16) take the runtime-mode-count kernel (64 x 64)
+#define BCG_SHAPE_DEF(TMV, TNV)                                                                        \
+  cudaError_t launch_moment_##TMV##x##TNV(const MomentArgs &args, int grid, cudaStream_t stream,        \
+                                          bool generic) {                                              \
+    const int h = args.h, r = args.r;                                                                  \
+    if (!generic) {                                                                                    \
+      BCG_SPLIT(1, 1) BCG_SPLIT(1, 2) BCG_SPLIT(2, 1) BCG_SPLIT(2, 2) BCG_SPLIT(2, 3) BCG_SPLIT(3, 2) \
+      BCG_SPLIT(3, 3) BCG_SPLIT(3, 4) BCG_SPLIT(4, 3) BCG_SPLIT(4, 4)                                  \
+    }                                                                                                  \
+    if constexpr (TMV == 64 && TNV == 64) return go_v1<16, 0, 0, TMV, TNV>(args, grid, stream);      \
+    else                                                                                               \
+    return cudaErrorInvalidValue;                                                                      \
   }
-    SHAPE(16, 128)
-    SHAPE(128, 16)
-    SHAPE(32, 64)
-    SHAPE(64, 32)
-    SHAPE(32, 32)
-#undef SHAPE
-#undef GOS
-    return e;
-  }
-#define GO16(M, ...) e = go_v1<16, M, 64, 64>(args, grid, stream)
-  BCG_DISPATCH_M(m, GO16, 0)
-#undef GO16
-  return e;
-}
+#define BCG_SPLIT(HV, RV) \
+  if (h == HV && r == RV) return go_v1<16, HV, RV, TMV_, TNV_>(args, grid, stream);
 
-cudaError_t launch_reduce_slices(const double *ws, int nslices, int64_t S, int64_t lo, int64_t hi,
-                                 double *out, cudaStream_t stream) {
-  if (hi <= lo) return cudaSuccess;
-  int64_t blocks = (hi - lo + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  k_reduce_slices<<<(int)blocks, 256, 0, stream>>>(ws, nslices, S, lo, hi, out);
-  return cudaGetLastError();
-}
+#if BCG_MOMENT_PART == 1
+#define TMV_ 64
+#define TNV_ 64
+#elif BCG_MOMENT_PART == 2
+#define TMV_ 16
+#define TNV_ 128
+#elif BCG_MOMENT_PART == 3
+#define TMV_ 128
+#define TNV_ 16
+#elif BCG_MOMENT_PART == 4
+#define TMV_ 32
+#define TNV_ 64
+#elif BCG_MOMENT_PART == 5
+#define TMV_ 64
+#define TNV_ 32
+#elif BCG_MOMENT_PART == 6
+#define TMV_ 32
+#define TNV_ 32
+#endif
+#define BCG_DEF_EXPAND(A, B) BCG_SHAPE_DEF(A, B)
+BCG_DEF_EXPAND(TMV_, TNV_)
+#endif  // BCG_MOMENT_PART
 
 }  // namespace bcg

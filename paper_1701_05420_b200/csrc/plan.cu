@@ -111,25 +111,25 @@ int default_variant() {  // only the v1 kernel family (variant 0) remains
   return 0;
 }
 
-// Staircase tile list for a tm x tn CTA tile (tiles whose elements all map to
-// orders < 2 are dropped).  Returns the number of useful elements covered.
-static int64_t build_tiles(const Plan &p, int tm, int tn, std::vector<Tile> *tiles, std::vector<int32_t> *kmin_out,
-                           std::vector<int32_t> *kmax_out) {
+// Staircase tile list of GEMM g for a tm x tn CTA tile (tiles whose elements
+// all map to orders < 2 are dropped).  Returns the number of tiles.
+static int64_t build_tiles(const Plan &p, const Gemm &g, int tm, int tn, std::vector<Tile> *tiles,
+                           std::vector<int32_t> *kmin_out, std::vector<int32_t> *kmax_out) {
   if (tiles) tiles->clear();
   if (kmin_out) kmin_out->clear();
   if (kmax_out) kmax_out->clear();
   int64_t ntiles = 0;
-  for (int64_t r0 = 0; r0 < p.R; r0 += tm) {
-    const int64_t r1 = std::min<int64_t>(r0 + tm, p.R);
-    for (int64_t c0 = p.row_cstart[r0]; c0 < p.C; c0 += tn) {
-      const int64_t c1 = std::min<int64_t>(c0 + tn, p.C);
+  for (int64_t r0 = 0; r0 < g.R; r0 += tm) {
+    const int64_t r1 = std::min<int64_t>(r0 + tm, g.R);
+    for (int64_t c0 = g.row_cstart[r0]; c0 < g.C; c0 += tn) {
+      const int64_t c1 = std::min<int64_t>(c0 + tn, g.C);
       int64_t kmin = INT64_MAX, kmax = -1;
       bool live = false;
       for (int64_t rr = r0; rr < r1; ++rr) {
-        int64_t cs = std::max<int64_t>(c0, p.row_cstart[rr]);
+        int64_t cs = std::max<int64_t>(c0, g.row_cstart[rr]);
         if (cs >= c1) continue;
-        const int64_t klo = p.row_keybase[rr] + p.col_rank[cs];
-        const int64_t khi = p.row_keybase[rr] + p.col_rank[c1 - 1];
+        const int64_t klo = g.row_keybase[rr] + g.col_rank[cs];
+        const int64_t khi = g.row_keybase[rr] + g.col_rank[c1 - 1];
         kmin = std::min<int64_t>(kmin, klo);
         kmax = std::max<int64_t>(kmax, khi);
         for (int64_t kk = klo; kk <= khi && !live; ++kk) live = p.koff[kk] >= 0;
@@ -144,49 +144,149 @@ static int64_t build_tiles(const Plan &p, int tm, int tn, std::vector<Tile> *til
   return ntiles;
 }
 
-// Modeled cost per useful FMA of a v1 tile shape: tiled area / useful area
-// (staircase waste) x (1 + 10 * Khatri-Rao products per FMA).  The weight of
-// a KR product (its X loads, DMULs on the shared FP64 pipe, the smem store,
-// ~10 FMA-equivalents) and the negligible effect of fragment-load pressure
-// are fitted to the shape sweep in profiles/r01_tile_shapes.log.
-static double v1_shape_cost(const Plan &p, int tm, int tn, int64_t useful) {
-  const int64_t ntiles = build_tiles(p, tm, tn, nullptr, nullptr, nullptr);
-  const double waste = (double)ntiles * tm * tn / (double)std::max<int64_t>(1, useful);
-  const double kr = 1.0 / tn + 1.0 / tm;
-  return waste * (1.0 + 10.0 * kr);
+static int64_t gemm_useful(const Gemm &g) {
+  int64_t u = 0;
+  for (int64_t r = 0; r < g.R; ++r) u += g.C - g.row_cstart[r];
+  return u;
 }
 
-static void choose_v1_shape(Plan &p) {
-  p.tm = 64;
-  p.tn = 64;
+// Modeled cost (in useful-FMA units) of running GEMM g with a tm x tn tile:
+// tiled area x (1 + 10 * Khatri-Rao products per FMA).  The weight of a KR
+// product (~10 FMA-equivalents: its X loads, DMULs on the shared FP64 pipe,
+// the smem store) and the negligible effect of fragment-load pressure are
+// fitted to the shape sweep in profiles/r01_tile_shapes.log.
+static double gemm_cost(const Plan &p, const Gemm &g, int tm, int tn) {
+  const int64_t ntiles = build_tiles(p, g, tm, tn, nullptr, nullptr, nullptr);
+  return (double)ntiles * tm * tn * (1.0 + 10.0 * (1.0 / tn + 1.0 / tm));
+}
+
+static void choose_shape(const Plan &p, Gemm &g) {
+  g.tm = kTM;
+  g.tn = kTN;
+  const int m = g.h + g.r;
   const char *env = std::getenv("BCG_TILE");
   int etm = 0, etn = 0;
-  if (env && std::sscanf(env, "%dx%d", &etm, &etn) == 2 && v1_shape_supported(pick_kc((int)p.n), p.m, etm, etn)) {
-    p.tm = etm;
-    p.tn = etn;
+  if (env && std::sscanf(env, "%dx%d", &etm, &etn) == 2 && v1_shape_supported(pick_kc((int)p.n), m, etm, etn)) {
+    g.tm = etm;
+    g.tn = etn;
     return;
   }
-  if (pick_kc((int)p.n) != 16 || p.m < 2 || p.m > 8) return;
-  int64_t useful = 0;
-  for (int64_t r = 0; r < p.R; ++r) useful += p.C - p.row_cstart[r];
+  if (pick_kc((int)p.n) != 16 || m < 2 || m > 8) return;
   static const int shapes[][2] = {{64, 64}, {16, 128}, {128, 16}, {32, 64}, {64, 32}, {32, 32}};
-  double best = v1_shape_cost(p, 64, 64, useful);
+  double best = gemm_cost(p, g, 64, 64);
   for (const auto &sh : shapes) {
-    const double c = v1_shape_cost(p, sh[0], sh[1], useful);
+    const double c = gemm_cost(p, g, sh[0], sh[1]);
     if (c < best * 0.97) {  // switch only for a clear modeled gain
       best = c;
-      p.tm = sh[0];
-      p.tn = sh[1];
+      g.tm = sh[0];
+      g.tn = sh[1];
     }
   }
+}
+
+// GEMM tables over the symbol alphabet 1..N (sym_edge / sym_col0, col0 < 0:
+// the ones column): rows = sorted h-tuples grouped by last entry v <= vmax,
+// cols = sorted (m-h)-tuples, row group v valid from the first column whose
+// tuple starts with >= max(v, tcol).
+static std::string build_gemm(Plan &p, Gemm &g, const std::vector<int64_t> &sym_edge,
+                              const std::vector<int64_t> &sym_col0, int64_t N, int h, int64_t vmax,
+                              int64_t tcol) {
+  const int m = p.m;
+  g.h = h;
+  g.r = m - h;
+  const int r = g.r;
+  std::vector<int64_t> lt, rt;
+  enum_sorted(N, h, lt);
+  enum_sorted(N, r, rt);
+  const int64_t NL = (int64_t)lt.size() / h, NR = (int64_t)rt.size() / r;
+  std::vector<int64_t> lorder(NL);
+  std::iota(lorder.begin(), lorder.end(), 0);
+  // (last entry, lexicographic): lex order is already the secondary order
+  std::stable_sort(lorder.begin(), lorder.end(),
+                   [&](int64_t a, int64_t c) { return lt[a * h + h - 1] < lt[c * h + h - 1]; });
+  // right columns, lexicographic
+  std::vector<int64_t> rstart(NR + 1, 0);
+  for (int64_t i = 0; i < NR; ++i) {
+    int64_t sz = 1;
+    for (int q = 0; q < r; ++q) sz *= sym_edge[rt[i * r + q]];
+    rstart[i + 1] = rstart[i] + sz;
+  }
+  g.C = rstart[NR];
+  g.colcols.resize(g.C * r);
+  g.col_rank.resize(g.C);
+  g.col_olin.resize(g.C);
+  g.col_size.resize(g.C);
+  for (int64_t i = 0; i < NR; ++i) {
+    const int64_t *Rt = &rt[i * r];
+    int64_t e[16];
+    for (int q = 0; q < r; ++q) e[q] = sym_edge[Rt[q]];
+    const int64_t sz = rstart[i + 1] - rstart[i];
+    for (int64_t o = 0; o < sz; ++o) {
+      int64_t c = rstart[i] + o, rem = o;
+      for (int q = r - 1; q >= 0; --q) {
+        const int64_t c0 = sym_col0[Rt[q]];
+        g.colcols[c * r + q] = (int16_t)(c0 < 0 ? -1 : c0 + rem % e[q]);
+        rem /= e[q];
+      }
+      g.col_rank[c] = (int32_t)i;
+      g.col_olin[c] = (int32_t)o;
+      g.col_size[c] = (int32_t)sz;
+    }
+  }
+  // first column of the suffix {R : R[0] >= v}; (v, ..., v) is its first tuple
+  std::vector<int64_t> cstart_v(N + 2, g.C), rank_first_v(N + 2, NR);
+  for (int64_t v = 1; v <= N; ++v) {
+    std::vector<int64_t> vv(r, v);
+    const int64_t rk = multiset_rank(vv.data(), r, N);
+    rank_first_v[v] = rk;
+    cstart_v[v] = rstart[rk];
+  }
+  // rows
+  g.R = 0;
+  for (int64_t i = 0; i < NL; ++i) {
+    const int64_t *L = &lt[lorder[i] * h];
+    const int64_t v = L[h - 1];
+    if (v > vmax || cstart_v[std::max(v, tcol)] >= g.C) continue;
+    int64_t sz = 1;
+    for (int q = 0; q < h; ++q) sz *= sym_edge[L[q]];
+    g.R += sz;
+  }
+  g.rowcols.resize(g.R * h);
+  g.row_keybase.resize(g.R);
+  g.row_olin.resize(g.R);
+  g.row_cstart.resize(g.R);
+  int64_t row = 0;
+  for (int64_t i = 0; i < NL; ++i) {
+    const int64_t *L = &lt[lorder[i] * h];
+    const int64_t v = L[h - 1];
+    const int64_t vc = std::max(v, tcol);
+    if (v > vmax || cstart_v[vc] >= g.C) continue;
+    int64_t full[16], e[16];
+    for (int q = 0; q < h; ++q) full[q] = L[q];
+    for (int q = h; q < m; ++q) full[q] = v;
+    const int64_t kbase = multiset_rank(full, m, N) - rank_first_v[v];
+    int64_t sz = 1;
+    for (int q = 0; q < h; ++q) sz *= (e[q] = sym_edge[L[q]]);
+    for (int64_t o = 0; o < sz; ++o, ++row) {
+      int64_t rem = o;
+      for (int q = h - 1; q >= 0; --q) {
+        const int64_t c0 = sym_col0[L[q]];
+        g.rowcols[row * h + q] = (int16_t)(c0 < 0 ? -1 : c0 + rem % e[q]);
+        rem /= e[q];
+      }
+      g.row_keybase[row] = (int32_t)kbase;
+      g.row_olin[row] = (int32_t)o;
+      g.row_cstart[row] = (int32_t)cstart_v[vc];
+    }
+  }
+  if (g.R > INT32_MAX || g.C > INT32_MAX) return "GEMM dimension overflow";
+  return "";
 }
 
 std::string build_plan(int64_t n, int m, int b, Plan &p, int variant, bool fused) {
   if (n < 1 || m < 1 || b < 1) return "n, m and b must all be >= 1";
   p.fused = fused;
   p.variant = variant < 0 ? default_variant() : variant;
-  p.tm = kTM;
-  p.tn = kTN;
   if (m > 16) return "kernel supports 2 <= m <= 16";
   p.n = n;
   p.m = m;
@@ -247,94 +347,43 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant, bool fused
       p.koff[k] = p.order_base[o] + p.lay[o].offs[multiset_rank(sub, o, p.nbar)];
     }
   }
-  p.h = m / 2;
-  p.r = m - p.h;
-  const int h = p.h, r = p.r;
-  std::vector<int64_t> lt, rt;
-  enum_sorted(N, h, lt);
-  enum_sorted(N, r, rt);
-  const int64_t NL = (int64_t)lt.size() / h, NR = (int64_t)rt.size() / r;
-  std::vector<int64_t> lorder(NL);
-  std::iota(lorder.begin(), lorder.end(), 0);
-  // (last entry, lexicographic): lex order is already the secondary order
-  std::stable_sort(lorder.begin(), lorder.end(),
-                   [&](int64_t a, int64_t c) { return lt[a * h + h - 1] < lt[c * h + h - 1]; });
-
-  // right columns, lexicographic
-  std::vector<int64_t> rstart(NR + 1, 0);
-  for (int64_t i = 0; i < NR; ++i) {
-    int64_t sz = 1;
-    for (int q = 0; q < r; ++q) sz *= sym_edge[rt[i * r + q]];
-    rstart[i + 1] = rstart[i] + sz;
+  // ---- the GEMM(s) ----
+  // odd m, unfused: try the hybrid split of the keys by their middle entry
+  // (key[h] < T: (h+1 | r-1) GEMM; else (h | r)), pick the T whose 64 x 64
+  // tiling covers the staircase with the least area (independent of the tile
+  // shapes chosen below, so every shape gives the same factorization)
+  const int h0 = m / 2;
+  p.gemm.assign(1, Gemm());
+  p.split_T = 0;
+  {
+    std::string err = build_gemm(p, p.gemm[0], sym_edge, sym_col0, N, h0, N, 1);
+    if (!err.empty()) return err;
   }
-  p.C = rstart[NR];
-  p.colcols.resize(p.C * r);
-  p.col_rank.resize(p.C);
-  p.col_olin.resize(p.C);
-  p.col_size.resize(p.C);
-  for (int64_t i = 0; i < NR; ++i) {
-    const int64_t *R = &rt[i * r];
-    int64_t e[16];
-    for (int q = 0; q < r; ++q) e[q] = sym_edge[R[q]];
-    int64_t sz = rstart[i + 1] - rstart[i];
-    for (int64_t o = 0; o < sz; ++o) {
-      int64_t c = rstart[i] + o, rem = o;
-      for (int q = r - 1; q >= 0; --q) {
-        const int64_t c0 = sym_col0[R[q]];
-        p.colcols[c * r + q] = (int16_t)(c0 < 0 ? -1 : c0 + rem % e[q]);
-        rem /= e[q];
+  if (!p.fused && (m % 2) == 1 && m >= 3 && !std::getenv("BCG_NO_HYBRID")) {
+    double best = gemm_cost(p, p.gemm[0], 64, 64);
+    for (int64_t T = 2; T <= N; ++T) {
+      Gemm ga, gb;
+      if (!build_gemm(p, ga, sym_edge, sym_col0, N, h0, N, T).empty()) continue;
+      if (!build_gemm(p, gb, sym_edge, sym_col0, N, h0 + 1, T - 1, 1).empty()) continue;
+      const double c = (ga.R ? gemm_cost(p, ga, 64, 64) : 0.0) + (gb.R ? gemm_cost(p, gb, 64, 64) : 0.0);
+      if (c < best * 0.97) {
+        best = c;
+        p.split_T = (int)T;
       }
-      p.col_rank[c] = (int32_t)i;
-      p.col_olin[c] = (int32_t)o;
-      p.col_size[c] = (int32_t)sz;
+    }
+    if (p.split_T) {
+      p.gemm.assign(2, Gemm());
+      build_gemm(p, p.gemm[0], sym_edge, sym_col0, N, h0, N, p.split_T);
+      build_gemm(p, p.gemm[1], sym_edge, sym_col0, N, h0 + 1, p.split_T - 1, 1);
+      if (p.gemm[1].R == 0) p.gemm.pop_back();
+      if (p.gemm[0].R == 0) p.gemm.erase(p.gemm.begin());
     }
   }
-  // first column of the suffix {R : R[0] >= v}; (v, ..., v) is its first tuple
-  std::vector<int64_t> cstart_v(N + 2, p.C), rank_first_v(N + 2, NR);
-  for (int64_t v = 1; v <= N; ++v) {
-    std::vector<int64_t> vv(r, v);
-    int64_t rk = multiset_rank(vv.data(), r, N);
-    rank_first_v[v] = rk;
-    cstart_v[v] = rstart[rk];
+  // per-GEMM CTA tile shape (tile model) and tile lists
+  for (Gemm &g : p.gemm) {
+    choose_shape(p, g);
+    build_tiles(p, g, g.tm, g.tn, &g.tiles, &g.tile_kmin, &g.tile_kmax);
   }
-  // rows
-  p.R = 0;
-  for (int64_t i = 0; i < NL; ++i) {
-    int64_t sz = 1;
-    for (int q = 0; q < h; ++q) sz *= sym_edge[lt[lorder[i] * h + q]];
-    p.R += sz;
-  }
-  p.rowcols.resize(p.R * h);
-  p.row_keybase.resize(p.R);
-  p.row_olin.resize(p.R);
-  p.row_cstart.resize(p.R);
-  int64_t row = 0;
-  for (int64_t i = 0; i < NL; ++i) {
-    const int64_t *L = &lt[lorder[i] * h];
-    const int64_t v = L[h - 1];
-    int64_t full[16], e[16];
-    for (int q = 0; q < h; ++q) full[q] = L[q];
-    for (int q = h; q < m; ++q) full[q] = v;
-    const int64_t kbase = multiset_rank(full, m, N) - rank_first_v[v];
-    int64_t sz = 1;
-    for (int q = 0; q < h; ++q) sz *= (e[q] = sym_edge[L[q]]);
-    for (int64_t o = 0; o < sz; ++o, ++row) {
-      int64_t rem = o;
-      for (int q = h - 1; q >= 0; --q) {
-        const int64_t c0 = sym_col0[L[q]];
-        p.rowcols[row * h + q] = (int16_t)(c0 < 0 ? -1 : c0 + rem % e[q]);
-        rem /= e[q];
-      }
-      p.row_keybase[row] = (int32_t)kbase;
-      p.row_olin[row] = (int32_t)o;
-      p.row_cstart[row] = (int32_t)cstart_v[v];
-    }
-  }
-  if (p.R > INT32_MAX || p.C > INT32_MAX) return "GEMM dimension overflow";
-
-  // staircase tiles; v1 plans pick the CTA tile shape by the tile model
-  if (p.variant == 0) choose_v1_shape(p);
-  build_tiles(p, p.tm, p.tn, &p.tiles, &p.tile_kmin, &p.tile_kmax);
 
   // ---- recursion tables ----
   p.part_mask.clear();
@@ -427,18 +476,22 @@ static cudaError_t up(T **dst, const std::vector<T> &src) {
 
 std::string upload_plan(Plan &p) {
   cudaError_t e = cudaSuccess;
+  for (Gemm &g : p.gemm) {
+#define UPG(d, s) if (e == cudaSuccess) e = up(&g.d, g.s)
+    UPG(d_rowcols, rowcols);
+    UPG(d_colcols, colcols);
+    UPG(d_row_keybase, row_keybase);
+    UPG(d_row_olin, row_olin);
+    UPG(d_row_cstart, row_cstart);
+    UPG(d_col_rank, col_rank);
+    UPG(d_col_olin, col_olin);
+    UPG(d_col_size, col_size);
+    UPG(d_tiles, tiles);
+    UPG(d_tile_kmin, tile_kmin);
+    UPG(d_tile_kmax, tile_kmax);
+#undef UPG
+  }
 #define UP(d, s) if (e == cudaSuccess) e = up(&p.d, p.s)
-  UP(d_rowcols, rowcols);
-  UP(d_colcols, colcols);
-  UP(d_row_keybase, row_keybase);
-  UP(d_row_olin, row_olin);
-  UP(d_row_cstart, row_cstart);
-  UP(d_col_rank, col_rank);
-  UP(d_col_olin, col_olin);
-  UP(d_col_size, col_size);
-  UP(d_tiles, tiles);
-  UP(d_tile_kmin, tile_kmin);
-  UP(d_tile_kmax, tile_kmax);
   UP(d_sub_rank, sub_rank);
   UP(d_part_mask, part_mask);
   UP(d_koff, koff);
@@ -457,9 +510,13 @@ std::string upload_plan(Plan &p) {
 }
 
 void free_plan(Plan &p) {
-  void *ptrs[] = {p.d_rowcols, p.d_colcols, p.d_row_keybase, p.d_row_olin, p.d_row_cstart,
-                  p.d_col_rank, p.d_col_olin, p.d_col_size, p.d_offs, p.d_tiles, p.d_tile_kmin, p.d_tile_kmax,
-                  p.d_keys32, p.d_sub_rank, p.d_part_mask, p.d_koff, p.d_term_off,
+  for (Gemm &g : p.gemm) {
+    void *gp[] = {g.d_rowcols, g.d_colcols, g.d_row_keybase, g.d_row_olin, g.d_row_cstart,
+                  g.d_col_rank, g.d_col_olin, g.d_col_size, g.d_tiles, g.d_tile_kmin, g.d_tile_kmax};
+    for (void *q : gp)
+      if (q) cudaFree(q);
+  }
+  void *ptrs[] = {p.d_offs, p.d_keys32, p.d_sub_rank, p.d_part_mask, p.d_koff, p.d_term_off,
                   p.d_full_keys, p.d_partial_keys};
   for (void *q : ptrs)
     if (q) cudaFree(q);

@@ -24,19 +24,14 @@ struct Tile {
   int32_t row0, col0;
 };
 
-struct Plan {
-  int64_t n = 0;
-  int variant = 0;          // moment kernel: 0 = v1 (64x64), >0 = warp-specialized shape
-  bool fused = false;       // one GEMM for all orders 2..m (ones block), output concatenated
-  int tm = kTM, tn = kTN;   // CTA tile of the staircase GEMM
-  int m = 0, b = 0;
-  int64_t nbar = 0;
-  std::vector<Layout> lay;  // index = order, 0..m (0 unused)
-
-  // --- moment GEMM (order m): left = first h modes, right = last r modes ---
+// One staircase GEMM of the order-m moment: rows = left h-tuples (grouped by
+// their last entry v), cols = right r-tuples (lexicographic); row group v's
+// valid columns are the suffix from cs(max(v, tcol)).
+struct Gemm {
   int h = 0, r = 0;
+  int tm = kTM, tn = kTN;               // CTA tile
   int64_t R = 0, C = 0;                 // left rows, right cols
-  std::vector<int16_t> rowcols;         // R x h X-column per mode
+  std::vector<int16_t> rowcols;         // R x h X-column per mode (-1: ones)
   std::vector<int16_t> colcols;         // C x r
   std::vector<int32_t> row_keybase;     // key index of (L, R) = row_keybase + col_rank
   std::vector<int32_t> row_olin;        // within-block linear offset of L's modes
@@ -44,11 +39,33 @@ struct Plan {
   std::vector<int32_t> col_rank;        // lexicographic rank of R among r-tuples
   std::vector<int32_t> col_olin;        // within-block offset of R's modes
   std::vector<int32_t> col_size;        // |R| = prod edges(R)
-  std::vector<int64_t> koff;           // GEMM key -> output offset of its block (-1: not produced)
-  std::vector<int64_t> order_base;     // fused: order o's packed buffer starts at order_base[o]
-  int64_t S_out = 0;                   // output elements (S_m, or S_2 + ... + S_m fused)
   std::vector<Tile> tiles;
   std::vector<int32_t> tile_kmin, tile_kmax;  // key range a tile touches
+  // device copies
+  int16_t *d_rowcols = nullptr, *d_colcols = nullptr;
+  int32_t *d_row_keybase = nullptr, *d_row_olin = nullptr, *d_row_cstart = nullptr;
+  int32_t *d_col_rank = nullptr, *d_col_olin = nullptr, *d_col_size = nullptr;
+  Tile *d_tiles = nullptr;
+  int32_t *d_tile_kmin = nullptr, *d_tile_kmax = nullptr;
+};
+
+struct Plan {
+  int64_t n = 0;
+  int variant = 0;          // moment kernel variant (0: the DMMA kernel)
+  bool fused = false;       // one GEMM for all orders 2..m (ones block), output concatenated
+  int m = 0, b = 0;
+  int64_t nbar = 0;
+  std::vector<Layout> lay;  // index = order, 0..m (0 unused)
+
+  // --- moment GEMM(s) of order m ---
+  // One GEMM with h = m/2, or for odd m the hybrid split: keys with
+  // key[h] >= split_T in the (h | r) GEMM, keys with key[h] < split_T in the
+  // (h+1 | r-1) GEMM (both staircases nearly rectangular, K2).
+  std::vector<Gemm> gemm;
+  int split_T = 0;                      // 0: single GEMM
+  std::vector<int64_t> koff;           // key -> output offset of its block (-1: not produced)
+  std::vector<int64_t> order_base;     // fused: order o's packed buffer starts at order_base[o]
+  int64_t S_out = 0;                   // output elements (S_m, or S_2 + ... + S_m fused)
 
   // --- recursion (order m) ---
   // partition table: for sigma = 2..m/2, partitions in reference order
@@ -65,12 +82,7 @@ struct Plan {
   std::vector<int32_t> full_keys, partial_keys;  // blocks with all edges == b / the rest
 
   // --- device copies ---
-  int16_t *d_rowcols = nullptr, *d_colcols = nullptr;
-  int32_t *d_row_keybase = nullptr, *d_row_olin = nullptr, *d_row_cstart = nullptr;
-  int32_t *d_col_rank = nullptr, *d_col_olin = nullptr, *d_col_size = nullptr;
   int64_t *d_offs = nullptr;           // offs of order m
-  Tile *d_tiles = nullptr;
-  int32_t *d_tile_kmin = nullptr, *d_tile_kmax = nullptr;
   int32_t *d_keys32 = nullptr;          // K_m x m keys (1-based)
   int32_t *d_sub_rank = nullptr;
   int32_t *d_part_mask = nullptr;

@@ -31,6 +31,10 @@
 
 #include "kernels.h"
 
+#ifndef BCG_RF_PART
+#error "recursion_fact.cu is compiled once per BCG_RF_PART (0..6), see _build.py"
+#endif
+
 namespace bcg {
 
 namespace rf {
@@ -291,29 +295,11 @@ __global__ void __launch_bounds__(Staged<M, B>::NTH) k_recursion_staged(RecFactA
   }
 }
 
+#if BCG_RF_PART == 0
+// ---- part 0: dispatch (the (m, b) instantiations live in parts 1..6,
+// separate translation units so nvcc compiles them in parallel) ----
 template <int M, int B>
-static cudaError_t go_fact(const RecFactArgs &a, cudaStream_t stream) {
-  static const bool no_staged = getenv("BCG_RF_NO_STAGED") != nullptr;  // A/B knob
-  if constexpr (Staged<M, B>::ok) {
-    if (!no_staged) {
-      if (a.nkeys <= 0) return cudaSuccess;
-      k_recursion_staged<M, B><<<(unsigned)a.nkeys, Staged<M, B>::NTH, 0, stream>>>(a);
-      g_launches++;
-      return cudaGetLastError();
-    }
-  }
-  constexpr int CT = ct_for(M, B);
-  constexpr int W = rf::ipow(B, CT);
-  const int64_t items = a.nkeys * W;
-  const int threads = kRfThreads;
-  const int64_t steps = (items + threads - 1) / threads;
-  if (steps <= 0) return cudaSuccess;
-  static const int per_cta = getenv("BCG_RF_STEPS") ? atoi(getenv("BCG_RF_STEPS")) : 1;  // tuning knob
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(steps, (steps + per_cta - 1) / per_cta));
-  k_recursion_fact<M, B, CT><<<(unsigned)blocks, threads, 0, stream>>>(a);
-  g_launches++;
-  return cudaGetLastError();
-}
+cudaError_t go_fact(const RecFactArgs &a, cudaStream_t stream);
 
 int recursion_fact_terms(int m) { return rf::term_count(m); }
 
@@ -340,5 +326,46 @@ cudaError_t launch_recursion_fact(const RecFactArgs &a, int m, int b, cudaStream
   }
 #undef RF_B
 }
+#else
+template <int M, int B>
+cudaError_t go_fact(const RecFactArgs &a, cudaStream_t stream) {
+  static const bool no_staged = getenv("BCG_RF_NO_STAGED") != nullptr;  // A/B knob
+  if constexpr (Staged<M, B>::ok) {
+    if (!no_staged) {
+      if (a.nkeys <= 0) return cudaSuccess;
+      k_recursion_staged<M, B><<<(unsigned)a.nkeys, Staged<M, B>::NTH, 0, stream>>>(a);
+      g_launches++;
+      return cudaGetLastError();
+    }
+  }
+  constexpr int CT = ct_for(M, B);
+  constexpr int W = rf::ipow(B, CT);
+  const int64_t items = a.nkeys * W;
+  const int threads = kRfThreads;
+  const int64_t steps = (items + threads - 1) / threads;
+  if (steps <= 0) return cudaSuccess;
+  static const int per_cta = getenv("BCG_RF_STEPS") ? atoi(getenv("BCG_RF_STEPS")) : 1;  // tuning knob
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(steps, (steps + per_cta - 1) / per_cta));
+  k_recursion_fact<M, B, CT><<<(unsigned)blocks, threads, 0, stream>>>(a);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+#define RF_INST(M, B) template cudaError_t go_fact<M, B>(const RecFactArgs &, cudaStream_t);
+#if BCG_RF_PART == 1
+RF_INST(4, 1) RF_INST(4, 2) RF_INST(4, 3) RF_INST(4, 4) RF_INST(4, 5) RF_INST(4, 6) RF_INST(4, 7) RF_INST(4, 8)
+#elif BCG_RF_PART == 2
+RF_INST(5, 1) RF_INST(5, 2) RF_INST(5, 3) RF_INST(5, 4)
+#elif BCG_RF_PART == 3
+RF_INST(5, 5) RF_INST(5, 6) RF_INST(5, 7) RF_INST(5, 8)
+#elif BCG_RF_PART == 4
+RF_INST(6, 1) RF_INST(6, 2) RF_INST(6, 3)
+#elif BCG_RF_PART == 5
+RF_INST(6, 4) RF_INST(6, 5) RF_INST(6, 6)
+#elif BCG_RF_PART == 6
+RF_INST(6, 7) RF_INST(6, 8)
+#endif
+#undef RF_INST
+#endif  // BCG_RF_PART
 
 }  // namespace bcg

@@ -75,6 +75,20 @@ def test_gemm_mapping_selfcheck(n, m, b):
     _native.check(_native.lib().bcg_plan_selfcheck(plan.handle))
 
 
+def test_hybrid_odd_order_plan():
+    # odd orders split the keys by their middle entry into an (h | h+1) and an
+    # (h+1 | h) GEMM when that tiles the staircase with less area; both parts
+    # together must still produce every element once (selfcheck)
+    plan = _native.Plan(48, 5, 4, host_only=True)
+    T, parts = plan.gemms()
+    assert T >= 2 and [(h, r) for h, r, *_ in parts] == [(2, 3), (3, 2)]
+    assert plan.kernel()[3] == sum(p[4] for p in parts)
+    _native.check(_native.lib().bcg_plan_selfcheck(plan.handle))
+    # even orders keep the single balanced GEMM
+    T, parts = _native.Plan(64, 4, 8, host_only=True).gemms()
+    assert T == 0 and [(h, r) for h, r, *_ in parts] == [(2, 2)]
+
+
 def test_plan_errors():
     from paper_1701_05420_b200 import ValidationError
 

@@ -1,7 +1,8 @@
-"""Time the top-order moment GEMM per kernel variant (and check it against
-variant 0 on the same data).
+"""Time the order-m moment GEMM of the bench configs (plan knobs such as
+BCG_TILE / BCG_NO_HYBRID are read from the environment when the plan is built,
+so compare settings across separate runs).
 
-    python tools/tune_moment.py --variants 0 1 2 3 4 --configs cfg2 cfg3 cfg4 [--t 0]
+    python tools/tune_moment.py --configs cfg2 cfg3 cfg4 [--t 0] [--order 0]
 """
 
 import argparse
@@ -19,7 +20,7 @@ from paper_1701_05420_b200.moments import _moment_device, center  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--variants", type=int, nargs="+", default=[0, 1, 2, 3, 4])
+    ap.add_argument("--variants", type=int, nargs="+", default=[0])
     ap.add_argument("--configs", nargs="+", default=["cfg2", "cfg3", "cfg4"])
     ap.add_argument("--t", type=int, default=0)
     ap.add_argument("--order", type=int, default=0)
