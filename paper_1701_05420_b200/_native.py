@@ -214,7 +214,7 @@ def plan(n: int, m: int, b: int, fused: bool = False) -> Plan:
     """Cached device plan for (n, m, b), the current kernel variant and
     whether it is the fused multi-order plan."""
     key = (int(n), int(m), int(b), -1 if fused else moment_variant(), bool(fused),
-           os.environ.get("BCG_TILE", ""))
+           os.environ.get("BCG_TILE", ""), os.environ.get("BCG_MB", ""), os.environ.get("BCG_NO_HYBRID", ""))
     with _lock:
         p = _plans.get(key)
         if p is None:

@@ -1,8 +1,9 @@
-"""Time the order-m moment GEMM of the bench configs (plan knobs such as
-BCG_TILE / BCG_NO_HYBRID are read from the environment when the plan is built,
-so compare settings across separate runs).
+"""Time the order-m moment GEMM of the bench configs under several plan
+settings (environment knobs read when a plan is built: BCG_TILE=TMxTN,
+BCG_MB=TMxTNxLA, BCG_NO_HYBRID=1), checking every setting bitwise against the
+first on the same data.
 
-    python tools/tune_moment.py --configs cfg2 cfg3 cfg4 [--t 0] [--order 0]
+    python tools/tune_moment.py --configs cfg2 cfg3 --settings "" BCG_MB=64x64x1 [--t 0] [--order 0]
 """
 
 import argparse
@@ -17,10 +18,21 @@ import torch  # noqa: E402
 import workloads  # noqa: E402
 from paper_1701_05420_b200.moments import _moment_device, center  # noqa: E402
 
+KNOBS = ("BCG_TILE", "BCG_MB", "BCG_NO_HYBRID")
+
+
+def apply(setting):
+    for k in KNOBS:
+        os.environ.pop(k, None)
+    for kv in setting.split(","):
+        if kv:
+            k, v = kv.split("=")
+            os.environ[k] = v
+
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--variants", type=int, nargs="+", default=[0])
+    ap.add_argument("--settings", nargs="+", default=[""])
     ap.add_argument("--configs", nargs="+", default=["cfg2", "cfg3", "cfg4"])
     ap.add_argument("--t", type=int, default=0)
     ap.add_argument("--order", type=int, default=0)
@@ -33,11 +45,12 @@ def main():
         xc = center(torch.from_numpy(workloads.generate(name, t)).cuda())
         flops = 2.0 * t * workloads.stored_elements(cfg.n, m, cfg.b)
         ref = None
-        for v in a.variants:
-            os.environ["BCG_MOMENT_VARIANT"] = str(v)
+        for st in a.settings:
+            apply(st)
             out = _moment_device(xc, m, cfg.b).data  # warm-up + plan
             if ref is None:
                 ref = out.clone()
+            diff = int((out != ref).sum())
             err = float(((out - ref).abs() / ref.abs().clamp_min(1e-300)).max())
             ts = []
             for _ in range(a.reps):
@@ -48,9 +61,10 @@ def main():
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1))
             ms = min(ts)
-            print(f"{name} m={m} t={t} variant {v}: {ms:9.2f} ms  {flops / ms / 1e9:6.2f} TFLOP/s "
-                  f"({100 * flops / ms / 1e9 / 37.1:5.1f}% of 37.1)  max rel diff vs v{a.variants[0]} {err:.1e}",
+            print(f"{name} m={m} t={t} [{st or 'default'}]: {ms:9.2f} ms  {flops / ms / 1e9:6.2f} TFLOP/s "
+                  f"({100 * flops / ms / 1e9 / 37.1:5.1f}% of 37.1)  vs first: {diff} differ, max rel {err:.1e}",
                   flush=True)
+        apply("")
 
 
 if __name__ == "__main__":
