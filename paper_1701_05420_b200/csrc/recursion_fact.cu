@@ -76,7 +76,28 @@ __host__ __device__ constexpr int head_offset(int mask, int M, int CT, int B, in
   return off;
 }
 
+// the same, forced to a compile-time constant (keeps the unrolled row loops
+// cheap to compile: the offsets are folded by the front end)
+template <int MASK, int M, int CT, int B, int ROW>
+struct HeadOff {
+  static constexpr int value = head_offset(MASK, M, CT, B, ROW);
+};
+
 }  // namespace rf
+
+// acc[row] -= f1[row offset in S] * f2[row offset in REST] for every register row
+template <int M, int B, int CT, int S, bool LDG, int... Rs>
+__device__ __forceinline__ void rows_fma(double *acc, const double *f1, const double *f2,
+                                         std::integer_sequence<int, Rs...>) {
+  constexpr int REST = ((1 << M) - 1) & ~S;
+  if constexpr (LDG) {
+    ((acc[Rs] = fma(-__ldg(f1 + rf::HeadOff<S, M, CT, B, Rs>::value), __ldg(f2 + rf::HeadOff<REST, M, CT, B, Rs>::value),
+                    acc[Rs])), ...);
+  } else {
+    ((acc[Rs] = fma(-f1[rf::HeadOff<S, M, CT, B, Rs>::value], f2[rf::HeadOff<REST, M, CT, B, Rs>::value], acc[Rs])),
+     ...);
+  }
+}
 
 // Thread <-> (output block, trailing index c): the block is viewed as ROWS x W
 // with the leading M-CT modes as rows and the trailing CT modes as columns.
@@ -101,12 +122,7 @@ __device__ __forceinline__ void apply_term(double (&acc)[rf::ipow(B, M - CT)], c
   }
   const double *f1 = a.cum[s] + toff[2 * T] + o1;
   const double *f2 = (r <= 3 ? a.cum[r] : a.cmom[r]) + toff[2 * T + 1] + o2;
-#pragma unroll
-  for (int row = 0; row < ROWS; ++row) {
-    const double u = __ldg(f1 + rf::head_offset(S, M, CT, B, row));
-    const double v = __ldg(f2 + rf::head_offset(REST, M, CT, B, row));
-    acc[row] = fma(-u, v, acc[row]);
-  }
+  rows_fma<M, B, CT, S, true>(acc, f1, f2, std::make_integer_sequence<int, ROWS>{});
 }
 
 template <int M, int B, int CT, int... Ts>
@@ -119,7 +135,7 @@ __device__ __forceinline__ void apply_terms(double (&acc)[rf::ipow(B, M - CT)], 
 constexpr int kRfThreads = 128;
 
 template <int M, int B, int CT>
-__global__ void __launch_bounds__(kRfThreads, 4) k_recursion_fact(RecFactArgs a) {
+__global__ void __launch_bounds__(kRfThreads, (rf::ipow(B, M - CT) > 32 ? 3 : 4)) k_recursion_fact(RecFactArgs a) {
   constexpr int NT = rf::term_count(M);
   constexpr int ROWS = rf::ipow(B, M - CT);  // elements per thread (registers)
   constexpr int W = rf::ipow(B, CT);         // threads per block
@@ -246,12 +262,7 @@ __device__ __forceinline__ void apply_term_staged(double (&acc)[Staged<M, B>::RO
   }
   const double *f1 = sm + O1 + o1;
   const double *f2 = sm + O2 + o2;
-#pragma unroll
-  for (int row = 0; row < ROWS; ++row) {
-    const double u = f1[rf::head_offset(S, M, CT, B, row)];
-    const double v = f2[rf::head_offset(REST, M, CT, B, row)];
-    acc[row] = fma(-u, v, acc[row]);
-  }
+  rows_fma<M, B, CT, S, false>(acc, f1, f2, std::make_integer_sequence<int, ROWS>{});
 }
 
 template <int M, int B, int... Ts>
@@ -295,6 +306,176 @@ __global__ void __launch_bounds__(Staged<M, B>::NTH) k_recursion_staged(RecFactA
   }
 }
 
+// ---------------------------------------------------------------------------
+// v4: persistent, software-pipelined.  Each CTA walks a contiguous run of
+// output blocks; while it evaluates block i from shared memory, cp.async (8-byte
+// LDGSTS, L1-allocating) is already staging block i+1's M_m block and every
+// factor sub-block it needs, and block i+2's term-offset row.  The HBM stream
+// of M_m and the L2 reads of the factors thus overlap the arithmetic instead of
+// sitting in front of it (v2/v3 are latency-bound: long-scoreboard stalls at
+// 25% occupancy).  The result goes straight from registers to global memory
+// (coalesced).  Register tile: the leading R modes (<= 64 rows), threads over
+// the trailing modes (<= 64 columns).
+namespace rf {
+__host__ __device__ constexpr int r_pipe(int M, int B) {
+  int r = 0;
+  while (r < M && ipow(B, M - r) > 64) ++r;
+  return r;
+}
+}  // namespace rf
+
+#ifndef BCG_RF_STAGES
+#define BCG_RF_STAGES 2
+#endif
+
+template <int M, int B>
+struct Pipe {
+  static constexpr int NT = rf::term_count(M);
+  static constexpr int R = rf::r_pipe(M, B);
+  static constexpr int CT = M - R;
+  static constexpr int W = rf::ipow(B, CT);
+  static constexpr int ROWS = rf::ipow(B, R);
+  static constexpr int NTH = (W + 31) / 32 * 32;
+  static constexpr int SEG = rf::seg_before(M, B, NT);
+  static constexpr int BLK = rf::ipow(B, M);
+  static constexpr int STAGE = (SEG + BLK + 1) / 2 * 2;  // doubles per stage
+  static constexpr int STAGES = BCG_RF_STAGES;
+  static constexpr int TSLOTS = 2 * STAGES - 1;         // term-offset rows in flight
+  static constexpr int TROW = 2 * NT + 2;               // int32 per row: term offsets, offs[key] (int64)
+  static constexpr int TROW_P = (TROW + 3) / 4 * 4;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE * 8 + (size_t)TSLOTS * TROW_P * 4;
+  static constexpr bool ok = ROWS <= 64 && SMEM <= 160 * 1024;
+};
+
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int M, int B, int T>
+__device__ __forceinline__ void pipe_stage_term(double *st, const RecFactArgs &a, const int32_t *trow, int tid) {
+  constexpr int S = rf::term_mask(M, T);
+  constexpr int s = rf::popc(S), r = M - s;
+  constexpr int L1 = rf::ipow(B, s), L2 = rf::ipow(B, r);
+  constexpr int O1 = rf::seg_before(M, B, T), O2 = O1 + L1;
+  constexpr int NTH = Pipe<M, B>::NTH;
+  const double *src1 = a.cum[s] + trow[2 * T];
+  const double *src2 = (r <= 3 ? a.cum[r] : a.cmom[r]) + trow[2 * T + 1];
+#pragma unroll
+  for (int i = tid; i < L1; i += NTH) cp_async8(st + O1 + i, src1 + i);
+#pragma unroll
+  for (int i = tid; i < L2; i += NTH) cp_async8(st + O2 + i, src2 + i);
+}
+
+template <int M, int B, int... Ts>
+__device__ __forceinline__ void pipe_stage(double *st, const RecFactArgs &a, const int32_t *trow, int tid,
+                                           std::integer_sequence<int, Ts...>) {
+  using P = Pipe<M, B>;
+  (pipe_stage_term<M, B, Ts>(st, a, trow, tid), ...);
+  const double *src = a.mk + *reinterpret_cast<const int64_t *>(trow + 2 * P::NT);
+  double *dst = st + P::SEG;
+#pragma unroll 4
+  for (int i = tid; i < P::BLK; i += P::NTH) cp_async8(dst + i, src + i);
+}
+
+template <int M, int B, int T>
+__device__ __forceinline__ void pipe_apply_term(double (&acc)[Pipe<M, B>::ROWS], const int (&dig)[M],
+                                                const double *st) {
+  constexpr int CT = Pipe<M, B>::CT, ROWS = Pipe<M, B>::ROWS;
+  constexpr int S = rf::term_mask(M, T);
+  constexpr int REST = ((1 << M) - 1) & ~S;
+  constexpr int s = rf::popc(S);
+  constexpr int O1 = rf::seg_before(M, B, T), O2 = O1 + rf::ipow(B, s);
+  int o1 = 0, o2 = 0;
+#pragma unroll
+  for (int q = M - CT; q < M; ++q) {
+    if (S & (1 << q)) o1 += dig[q] * rf::stride_in(S, q, B);
+    if (REST & (1 << q)) o2 += dig[q] * rf::stride_in(REST, q, B);
+  }
+  const double *f1 = st + O1 + o1;
+  const double *f2 = st + O2 + o2;
+  rows_fma<M, B, CT, S, false>(acc, f1, f2, std::make_integer_sequence<int, ROWS>{});
+}
+
+template <int M, int B, int... Ts>
+__device__ __forceinline__ void pipe_apply(double (&acc)[Pipe<M, B>::ROWS], const int (&dig)[M], const double *st,
+                                           std::integer_sequence<int, Ts...>) {
+  (pipe_apply_term<M, B, Ts>(acc, dig, st), ...);
+}
+
+template <int M, int B>
+__global__ void __launch_bounds__(Pipe<M, B>::NTH) k_recursion_pipe(RecFactArgs a) {
+  using P = Pipe<M, B>;
+  constexpr int D = P::STAGES - 1;  // blocks staged ahead of the one being evaluated
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *stages = reinterpret_cast<double *>(smem_raw);
+  int32_t *trows = reinterpret_cast<int32_t *>(smem_raw + (size_t)P::STAGES * P::STAGE * 8);
+  const int tid = threadIdx.x;
+  const int64_t k_begin = a.nkeys * blockIdx.x / gridDim.x;
+  const int64_t k_end = a.nkeys * (blockIdx.x + 1) / gridDim.x;
+  if (k_begin >= k_end) return;
+  auto stage_trow = [&](int64_t i) {  // term-offset row + block offset of key i
+    const int32_t key = a.keys[i];
+    int32_t *row = trows + (i % P::TSLOTS) * P::TROW_P;
+    for (int j = tid; j < 2 * P::NT; j += P::NTH) cp_async4(row + j, a.term_off + (int64_t)key * 2 * P::NT + j);
+    if (tid == 0) cp_async8(row + 2 * P::NT, a.offs + key);
+  };
+  // prologue: offsets of keys k_begin .. k_begin+2D-1, then the data of the first D keys
+  for (int64_t i = k_begin; i < k_begin + 2 * D && i < k_end; ++i) stage_trow(i);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int64_t i = k_begin; i < k_begin + D; ++i) {
+    if (i < k_end) pipe_stage<M, B>(stages + (i % P::STAGES) * P::STAGE, a, trows + (i % P::TSLOTS) * P::TROW_P,
+                                    tid, std::make_integer_sequence<int, P::NT>{});
+    cp_async_commit();
+  }
+  const bool active = tid < P::W;
+  const int c = active ? tid : 0;
+  int dig[M];
+#pragma unroll
+  for (int q = 0; q < M; ++q) dig[q] = 0;
+  {
+    int rem = c;
+#pragma unroll
+    for (int q = M - 1; q >= M - P::CT; --q) {
+      dig[q] = rem % B;
+      rem /= B;
+    }
+  }
+  for (int64_t i = k_begin; i < k_end; ++i) {
+    // block i's group is complete once at most D-1 newer groups are pending
+    cp_async_wait<D - 1>();
+    __syncthreads();
+    // stage block i+D (its offsets came with the group of iteration i-D, now
+    // complete) and the offsets of block i+2D
+    const int64_t j = i + D;
+    if (j < k_end) pipe_stage<M, B>(stages + (j % P::STAGES) * P::STAGE, a, trows + (j % P::TSLOTS) * P::TROW_P,
+                                    tid, std::make_integer_sequence<int, P::NT>{});
+    if (i + 2 * D < k_end) stage_trow(i + 2 * D);
+    cp_async_commit();
+    const double *st = stages + (i % P::STAGES) * P::STAGE;
+    const int64_t off = *reinterpret_cast<const int64_t *>(trows + (i % P::TSLOTS) * P::TROW_P + 2 * P::NT);
+    if (active) {
+      double acc[P::ROWS];
+#pragma unroll
+      for (int row = 0; row < P::ROWS; ++row) acc[row] = st[P::SEG + row * P::W + c];
+      pipe_apply<M, B>(acc, dig, st, std::make_integer_sequence<int, P::NT>{});
+      double *blk = a.mk + off + c;
+#pragma unroll
+      for (int row = 0; row < P::ROWS; ++row) blk[(int64_t)row * P::W] = acc[row];
+    }
+    __syncthreads();  // stage i % STAGES and its offset row are reused below
+  }
+}
+
 #if BCG_RF_PART == 0
 // ---- part 0: dispatch (the (m, b) instantiations live in parts 1..6,
 // separate translation units so nvcc compiles them in parallel) ----
@@ -327,18 +508,8 @@ cudaError_t launch_recursion_fact(const RecFactArgs &a, int m, int b, cudaStream
 #undef RF_B
 }
 #else
-template <int M, int B>
-cudaError_t go_fact(const RecFactArgs &a, cudaStream_t stream) {
-  static const bool no_staged = getenv("BCG_RF_NO_STAGED") != nullptr;  // A/B knob
-  if constexpr (Staged<M, B>::ok) {
-    if (!no_staged) {
-      if (a.nkeys <= 0) return cudaSuccess;
-      k_recursion_staged<M, B><<<(unsigned)a.nkeys, Staged<M, B>::NTH, 0, stream>>>(a);
-      g_launches++;
-      return cudaGetLastError();
-    }
-  }
-  constexpr int CT = ct_for(M, B);
+template <int M, int B, int CT>
+static cudaError_t go_fact_v2(const RecFactArgs &a, cudaStream_t stream) {
   constexpr int W = rf::ipow(B, CT);
   const int64_t items = a.nkeys * W;
   const int threads = kRfThreads;
@@ -349,6 +520,54 @@ cudaError_t go_fact(const RecFactArgs &a, cudaStream_t stream) {
   k_recursion_fact<M, B, CT><<<(unsigned)blocks, threads, 0, stream>>>(a);
   g_launches++;
   return cudaGetLastError();
+}
+
+template <int M, int B>
+cudaError_t go_fact(const RecFactArgs &a, cudaStream_t stream) {
+  // A/B knob: BCG_RF_VARIANT=2 (v2), 3 (v3 staged), 4 (v4 pipelined)
+  static const int variant = getenv("BCG_RF_VARIANT") ? atoi(getenv("BCG_RF_VARIANT")) : 0;
+  static const bool no_staged = getenv("BCG_RF_NO_STAGED") != nullptr || variant == 2 || variant == 4;
+  if constexpr (Pipe<M, B>::ok) {
+    if (variant == 4) {  // measured slower than v2/v3 everywhere (profiles/r01_recursion_v4_sweep.log)
+      if (a.nkeys <= 0) return cudaSuccess;
+      using P = Pipe<M, B>;
+      static int grid_cap = 0;
+      if (!grid_cap) {
+        cudaError_t e = cudaFuncSetAttribute(k_recursion_pipe<M, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)P::SMEM);
+        if (e != cudaSuccess) return e;
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_recursion_pipe<M, B>, P::NTH, P::SMEM);
+        if (e != cudaSuccess) return e;
+        grid_cap = std::max(1, per_sm) * sms;
+      }
+      const int64_t grid = std::min<int64_t>(a.nkeys, grid_cap);
+      k_recursion_pipe<M, B><<<(unsigned)grid, P::NTH, P::SMEM, stream>>>(a);
+      g_launches++;
+      return cudaGetLastError();
+    }
+  }
+  if constexpr (Staged<M, B>::ok) {
+    if (!no_staged) {
+      if (a.nkeys <= 0) return cudaSuccess;
+      k_recursion_staged<M, B><<<(unsigned)a.nkeys, Staged<M, B>::NTH, 0, stream>>>(a);
+      g_launches++;
+      return cudaGetLastError();
+    }
+  }
+  constexpr int CT = ct_for(M, B);
+  // A/B knob BCG_RF_TILE=+1: one more leading mode in registers (where it stays
+  // <= 64 rows), -1: one fewer
+  constexpr int CTW = (CT > 1 && rf::ipow(B, M - CT + 1) <= 64) ? CT - 1 : CT;
+  constexpr int CTN = CT < M - 1 ? CT + 1 : CT;
+  // default: the wider tile when the narrow one keeps fewer than 16 rows
+  // (b = 6, m = 6: 6 -> 36 rows, 1.9x faster at the cfg5 layout)
+  static const int tile = getenv("BCG_RF_TILE") ? atoi(getenv("BCG_RF_TILE")) : (rf::ipow(B, M - CT) < 16 ? 1 : 0);
+  if (tile > 0 && CTW != CT) return go_fact_v2<M, B, CTW>(a, stream);
+  if (tile < 0 && CTN != CT) return go_fact_v2<M, B, CTN>(a, stream);
+  return go_fact_v2<M, B, CT>(a, stream);
 }
 
 #define RF_INST(M, B) template cudaError_t go_fact<M, B>(const RecFactArgs &, cudaStream_t);

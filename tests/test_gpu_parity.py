@@ -433,3 +433,38 @@ def test_sharded_path_over_nccl_single_rank(tmp_path, rng):
     np.testing.assert_allclose(got["mean"], c1, rtol=1e-13)
     for k in range(2, 7):
         np.testing.assert_allclose(got[f"c{k}"], want[k], rtol=1e-9, atol=1e-12)
+
+
+_VARIANT_SHAPES = [(16, 4, 8, 300), (12, 5, 4, 400), (9, 6, 3, 300), (12, 6, 6, 200), (12, 5, 6, 300), (7, 6, 3, 250)]
+
+
+@pytest.mark.parametrize("env", [{"BCG_RF_VARIANT": "2", "BCG_RF_TILE": "-1"}, {"BCG_RF_VARIANT": "2", "BCG_RF_TILE": "0"},
+                                 {"BCG_RF_VARIANT": "2", "BCG_RF_TILE": "1"}, {"BCG_RF_VARIANT": "3"},
+                                 {"BCG_RF_VARIANT": "4"}, {}])
+def test_recursion_variants_match_oracle(env, tmp_path):
+    """Every factored-recursion kernel variant (the knobs are read once per
+    process, so each runs in a subprocess) gives the oracle's cumulants,
+    incl. b = 6 (wide register tile), b = 8, partial-edge blocks."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "c.npz"
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_1701_05420_b200 as bcg\n"
+        "res = {}\n"
+        "for i, (n, m, b, t) in enumerate(%r):\n"
+        "    x = np.random.default_rng(i).exponential(1.0, (t, n)) + np.random.default_rng(100 + i).standard_normal((t, n))\n"
+        "    cs = bcg.cumulants_upto(x, m, b=b)\n"
+        "    for k in range(2, m + 1):\n"
+        "        res[f'{i}_{k}'] = cs[k].packed_host()\n"
+        "np.savez(%r, **res)\n" % (root, _VARIANT_SHAPES, str(out)))
+    subprocess.run([sys.executable, "-c", code], check=True, env={**os.environ, **env}, timeout=600)
+    got = np.load(out)
+    for i, (n, m, b, t) in enumerate(_VARIANT_SHAPES):
+        x = np.random.default_rng(i).exponential(1.0, (t, n)) + np.random.default_rng(100 + i).standard_normal((t, n))
+        _, want = orc.cumulants_upto(x, m, b)
+        for k in range(2, m + 1):
+            np.testing.assert_allclose(got[f"{i}_{k}"], want[k], rtol=1e-9, atol=1e-12, err_msg=f"{env} shape {i} k={k}")
