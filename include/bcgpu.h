@@ -169,6 +169,12 @@ int bcg_rowstats(const double *xt, int64_t n, int64_t t, int64_t ldt,
 int bcg_moment_raw_range(const bcg_plan *plan, const double *x, int64_t t,
                          int64_t ldx, double *out, void *ws, size_t ws_bytes,
                          int64_t k0, int64_t k1, void *stream);
+/* bcg_moment_raw_t restricted to blocks [k0, k1): the per-rank moment of the
+ * block-split multi-GPU mode (distributed.cumulants_upto_block_split), every
+ * rank reading all of xt; bitwise identical to the full call on its blocks. */
+int bcg_moment_raw_t_range(const bcg_plan *plan, const double *xt, int64_t t,
+                           int64_t ldt, double *out, void *ws, size_t ws_bytes,
+                           int64_t k0, int64_t k1, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Cumulant recursion, in place: on entry mk holds the order-m central moment

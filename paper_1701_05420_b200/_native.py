@@ -56,6 +56,7 @@ SIGNATURES = [
     ("bcg_transpose_pad", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp]),
     ("bcg_rowstats", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     ("bcg_moment_raw_range", ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _sz, _i64, _i64, _vp]),
+    ("bcg_moment_raw_t_range", ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _sz, _i64, _i64, _vp]),
     ("bcg_cumulant_recursion", ctypes.c_int, [_vp, _vp, _vp, _vp]),
     ("bcg_cumulant_recursion_range", ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
     ("bcg_cumulant_recursion_ex", ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _vp]),

@@ -405,6 +405,18 @@ int bcg_moment_raw_range(const bcg_plan *plan, const double *x, int64_t t, int64
   return moment_rowmajor(p, x, t, ldx, out, ws, ws_bytes, k0, k1, static_cast<cudaStream_t>(stream));
 }
 
+int bcg_moment_raw_t_range(const bcg_plan *plan, const double *xt, int64_t t, int64_t ldt, double *out, void *ws,
+                           size_t ws_bytes, int64_t k0, int64_t k1, void *stream) {
+  if (!plan) return fail(BCG_EINVAL, "plan is NULL");
+  const bcg::Plan &p = plan->p;
+  if (p.m < 2 || p.m > 16) return fail(BCG_EINVAL, "kernel supports 2 <= m <= 16");
+  if (!p.d_koff) return fail(BCG_EINVAL, "host-only plan");
+  k0 = std::max<int64_t>(k0, 0);
+  k1 = std::min<int64_t>(k1, p.lay[p.m].K);
+  if (k1 <= k0) return BCG_OK;
+  return run_moment(p, xt, t, ldt, out, ws, ws_bytes, k0, k1, static_cast<cudaStream_t>(stream));
+}
+
 int bcg_transpose_pad(const double *x, int64_t t, int64_t n, int64_t ldx, const double *mean, double *xt, int64_t ldt,
                       void *stream) {
   if (t < 1 || n < 1 || ldx < n || ldt < t) return fail(BCG_EINVAL, "bad transpose shape");
@@ -547,16 +559,17 @@ static int recursion_dispatch(const bcg_plan *plan, double *mk, const double *co
   for (int k = 2; k <= m - 2; ++k)
     if (!lower[k - 2]) return fail(BCG_EINVAL, "missing lower cumulant of order " + std::to_string(k));
   bcg::RecFactArgs a{};
-  a.offs = p.d_offs;
   a.term_off = p.d_term_off;
   for (int k = 2; k <= m - 2; ++k) {
     a.cum[k] = lower[k - 2];
+    a.cum_len[k] = p.lay[k].offs.back();
     if (k >= 4) a.cmom[k] = cmom[k - 2];
   }
   a.mk = mk;
   auto lo_f = std::lower_bound(p.full_keys.begin(), p.full_keys.end(), (int32_t)k0) - p.full_keys.begin();
   auto hi_f = std::lower_bound(p.full_keys.begin(), p.full_keys.end(), (int32_t)k1) - p.full_keys.begin();
-  a.keys = p.d_full_keys + lo_f;
+  a.blk_off = p.d_full_offs + lo_f;
+  a.term_off = p.d_term_off + lo_f * 2 * p.fact_terms;
   a.nkeys = hi_f - lo_f;
   if (a.nkeys > 0) CUDA_TRY(bcg::launch_recursion_fact(a, m, p.b, s), "factored recursion kernel");
   auto lo_p = std::lower_bound(p.partial_keys.begin(), p.partial_keys.end(), (int32_t)k0) - p.partial_keys.begin();

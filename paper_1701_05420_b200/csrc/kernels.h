@@ -83,12 +83,12 @@ struct RecursionArgs {
 cudaError_t launch_recursion(const RecursionArgs &args, cudaStream_t stream);
 
 struct RecFactArgs {
-  const int32_t *keys;      // full output blocks to process (indices into the order-m layout)
-  int64_t nkeys;
-  const int64_t *offs;      // order-m block offsets
-  const int32_t *term_off;  // [K][nterms][2] element offsets of each term's factor blocks
+  int64_t nkeys;            // full output blocks to process (work items 0 .. nkeys-1)
+  const int64_t *blk_off;   // [nkeys] M_m element offset of each block
+  const int32_t *term_off;  // [nkeys][nterms][2] element offsets of each term's factor blocks
   const double *cum[16];    // packed C_k, k = 2 .. m-2
   const double *cmom[16];   // packed central moments M_k, k = 4 .. m-2
+  int64_t cum_len[16];      // stored elements of C_k (shared-memory residency of C_2, C_3)
   double *mk;               // in: M_m, out: C_m
 };
 int recursion_fact_terms(int m);

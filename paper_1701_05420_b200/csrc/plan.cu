@@ -433,6 +433,7 @@ static void build_fact_tables(Plan &p) {
   const int m = p.m;
   p.fact_terms = 0;
   p.term_off.clear();
+  p.full_offs.clear();
   p.full_keys.clear();
   p.partial_keys.clear();
   const Layout &LM = p.lay[m];
@@ -450,9 +451,14 @@ static void build_fact_tables(Plan &p) {
     if (c >= 2 && c <= m - 2) masks.push_back(s);
   }
   p.fact_terms = (int)masks.size();
-  p.term_off.resize((size_t)LM.K * masks.size() * 2);
-  for (int64_t k = 0; k < LM.K; ++k) {
+  // indexed by position in full_keys (the kernels' work list), so a kernel
+  // reads one contiguous row per output block, no key -> table indirection
+  p.term_off.resize(p.full_keys.size() * masks.size() * 2);
+  p.full_offs.resize(p.full_keys.size());
+  for (size_t i = 0; i < p.full_keys.size(); ++i) {
+    const int64_t k = p.full_keys[i];
     const int64_t *key = &LM.keys[k * m];
+    p.full_offs[i] = LM.offs[k];
     for (size_t t = 0; t < masks.size(); ++t) {
       int64_t a[16], c[16];
       int na = 0, nc = 0;
@@ -460,8 +466,8 @@ static void build_fact_tables(Plan &p) {
         if (masks[t] & (1 << q)) a[na++] = key[q];
         else c[nc++] = key[q];
       }
-      p.term_off[(k * masks.size() + t) * 2] = (int32_t)p.lay[na].offs[multiset_rank(a, na, p.nbar)];
-      p.term_off[(k * masks.size() + t) * 2 + 1] = (int32_t)p.lay[nc].offs[multiset_rank(c, nc, p.nbar)];
+      p.term_off[(i * masks.size() + t) * 2] = (int32_t)p.lay[na].offs[multiset_rank(a, na, p.nbar)];
+      p.term_off[(i * masks.size() + t) * 2 + 1] = (int32_t)p.lay[nc].offs[multiset_rank(c, nc, p.nbar)];
     }
   }
 }
@@ -496,6 +502,7 @@ std::string upload_plan(Plan &p) {
   UP(d_part_mask, part_mask);
   UP(d_koff, koff);
   UP(d_term_off, term_off);
+  UP(d_full_offs, full_offs);
   UP(d_full_keys, full_keys);
   UP(d_partial_keys, partial_keys);
 #undef UP
@@ -517,7 +524,7 @@ void free_plan(Plan &p) {
       if (q) cudaFree(q);
   }
   void *ptrs[] = {p.d_offs, p.d_keys32, p.d_sub_rank, p.d_part_mask, p.d_koff, p.d_term_off,
-                  p.d_full_keys, p.d_partial_keys};
+                  p.d_full_offs, p.d_full_keys, p.d_partial_keys};
   for (void *q : ptrs)
     if (q) cudaFree(q);
   for (auto &q : p.d_lower_offs)

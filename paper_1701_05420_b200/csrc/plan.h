@@ -78,7 +78,8 @@ struct Plan {
   std::vector<int32_t> sub_rank;        // K_m x nslots lower-block index per slot
   // factored recursion (recursion_fact.cu): terms S containing mode 0
   int fact_terms = 0;                   // 0: not supported for (m, b)
-  std::vector<int32_t> term_off;        // K_m x terms x 2 factor-block element offsets
+  std::vector<int32_t> term_off;        // full blocks x terms x 2 factor-block element offsets
+  std::vector<int64_t> full_offs;       // M_m element offset of each full block
   std::vector<int32_t> full_keys, partial_keys;  // blocks with all edges == b / the rest
 
   // --- device copies ---
@@ -88,6 +89,7 @@ struct Plan {
   int32_t *d_part_mask = nullptr;
   int64_t *d_koff = nullptr;
   int32_t *d_term_off = nullptr;
+  int64_t *d_full_offs = nullptr;
   int32_t *d_full_keys = nullptr, *d_partial_keys = nullptr;
   int64_t *d_lower_offs[16] = {nullptr};  // offs of orders 2..m-2
 };

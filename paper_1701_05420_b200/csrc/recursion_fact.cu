@@ -86,17 +86,23 @@ struct HeadOff {
 }  // namespace rf
 
 // acc[row] -= f1[row offset in S] * f2[row offset in REST] for every register row
-template <int M, int B, int CT, int S, bool LDG, int... Rs>
+template <bool LDG>
+__device__ __forceinline__ double ld_factor(const double *p) {
+  if constexpr (LDG) {
+    return __ldg(p);
+  } else {
+    return *p;
+  }
+}
+// LDG1 / LDG2: factor read through the read-only global path (else: a plain
+// load, shared memory where the factor tensor is resident there)
+template <int M, int B, int CT, int S, bool LDG1, bool LDG2, int... Rs>
 __device__ __forceinline__ void rows_fma(double *acc, const double *f1, const double *f2,
                                          std::integer_sequence<int, Rs...>) {
   constexpr int REST = ((1 << M) - 1) & ~S;
-  if constexpr (LDG) {
-    ((acc[Rs] = fma(-__ldg(f1 + rf::HeadOff<S, M, CT, B, Rs>::value), __ldg(f2 + rf::HeadOff<REST, M, CT, B, Rs>::value),
-                    acc[Rs])), ...);
-  } else {
-    ((acc[Rs] = fma(-f1[rf::HeadOff<S, M, CT, B, Rs>::value], f2[rf::HeadOff<REST, M, CT, B, Rs>::value], acc[Rs])),
-     ...);
-  }
+  ((acc[Rs] = fma(-ld_factor<LDG1>(f1 + rf::HeadOff<S, M, CT, B, Rs>::value),
+                  ld_factor<LDG2>(f2 + rf::HeadOff<REST, M, CT, B, Rs>::value), acc[Rs])),
+   ...);
 }
 
 // Thread <-> (output block, trailing index c): the block is viewed as ROWS x W
@@ -105,9 +111,9 @@ __device__ __forceinline__ void rows_fma(double *acc, const double *f1, const do
 // broadcast or contiguous across the warp), each thread keeps its ROWS
 // elements in registers, and the row offsets into every factor are
 // compile-time immediates.
-template <int M, int B, int CT, int T>
+template <int M, int B, int CT, int RES, int T>
 __device__ __forceinline__ void apply_term(double (&acc)[rf::ipow(B, M - CT)], const int (&dig)[M],
-                                           const RecFactArgs &a, const int32_t *toff) {
+                                           const RecFactArgs &a, const int32_t *toff, const double *const *res) {
   constexpr int S = rf::term_mask(M, T);
   constexpr int FULL = (1 << M) - 1;
   constexpr int REST = FULL & ~S;
@@ -120,50 +126,103 @@ __device__ __forceinline__ void apply_term(double (&acc)[rf::ipow(B, M - CT)], c
     if (S & (1 << q)) o1 += dig[q] * rf::stride_in(S, q, B);
     if (REST & (1 << q)) o2 += dig[q] * rf::stride_in(REST, q, B);
   }
-  const double *f1 = a.cum[s] + toff[2 * T] + o1;
-  const double *f2 = (r <= 3 ? a.cum[r] : a.cmom[r]) + toff[2 * T + 1] + o2;
-  rows_fma<M, B, CT, S, true>(acc, f1, f2, std::make_integer_sequence<int, ROWS>{});
+  // RES bit (k - 2): C_k resident in shared memory (k = 2, 3)
+  constexpr bool R1 = s <= 3 && ((RES >> (s - 2)) & 1);
+  constexpr bool R2 = r <= 3 && ((RES >> (r - 2)) & 1);
+  const double *f1 = (R1 ? res[s - 2] : a.cum[s]) + toff[2 * T] + o1;
+  const double *f2 = (R2 ? res[r - 2] : (r <= 3 ? a.cum[r] : a.cmom[r])) + toff[2 * T + 1] + o2;
+  rows_fma<M, B, CT, S, !R1, !R2>(acc, f1, f2, std::make_integer_sequence<int, ROWS>{});
 }
 
-template <int M, int B, int CT, int... Ts>
+template <int M, int B, int CT, int RES, int... Ts>
 __device__ __forceinline__ void apply_terms(double (&acc)[rf::ipow(B, M - CT)], const int (&dig)[M],
-                                            const RecFactArgs &a, const int32_t *toff,
+                                            const RecFactArgs &a, const int32_t *toff, const double *const *res,
                                             std::integer_sequence<int, Ts...>) {
-  (apply_term<M, B, CT, Ts>(acc, dig, a, toff), ...);
+  (apply_term<M, B, CT, RES, Ts>(acc, dig, a, toff, res), ...);
 }
 
 constexpr int kRfThreads = 128;
+constexpr int kRfThreadsRes = 512;  // one CTA per SM when C_2 (and C_3) are resident
 
-template <int M, int B, int CT>
-__global__ void __launch_bounds__(kRfThreads, (rf::ipow(B, M - CT) > 32 ? 3 : 4)) k_recursion_fact(RecFactArgs a) {
+template <int M, int B, int CT, int RES>
+struct FactCfg {
+  static constexpr int NTHR = RES ? kRfThreadsRes : kRfThreads;
+  static constexpr int MINB = RES ? 1 : (rf::ipow(B, M - CT) > 32 ? 3 : 4);
+  static constexpr int NT = rf::term_count(M);
+  static constexpr int W = rf::ipow(B, CT);
+  static constexpr int NGRP = NTHR / kRfThreads;  // independent 128-thread groups per CTA
+  static constexpr int KPC = (kRfThreads + W - 1) / W + 1;  // max output blocks per group step
+  static constexpr int TOFF_GRP = (KPC * 2 * NT + 3) / 4 * 4;  // int32 per group
+  static constexpr int TOFF_BYTES = NGRP * TOFF_GRP * 4;
+};
+
+// barrier over the 128 threads of group g only (named barrier 1 + g)
+__device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(1 + g), "r"(kRfThreads) : "memory");
+}
+
+// RES = 0: v2 as measured in round 1 (128 threads, factors through L1).
+// RES = 1 / 3: the same evaluation with C_2 / C_2 and C_3 copied whole into
+// shared memory first (persistent CTAs, 512 threads = 4 independent
+// 128-thread groups synchronised by named barriers, so their M_m loads stay
+// out of phase): those factor reads become LDS (short latency, ~1 wavefront
+// per warp access instead of ~3 for the scattered 8-byte global reads), only
+// C_4 / M_4 factors still go through L1.
+template <int M, int B, int CT, int RES>
+__global__ void __launch_bounds__(FactCfg<M, B, CT, RES>::NTHR, FactCfg<M, B, CT, RES>::MINB)
+    k_recursion_fact(RecFactArgs a) {
+  using FC = FactCfg<M, B, CT, RES>;
+  constexpr int kThr = FC::NTHR;
   constexpr int NT = rf::term_count(M);
   constexpr int ROWS = rf::ipow(B, M - CT);  // elements per thread (registers)
   constexpr int W = rf::ipow(B, CT);         // threads per block
-  constexpr int KPC = (kRfThreads + W - 1) / W + 1;  // max output blocks per step
-  __shared__ int32_t s_toff[KPC * 2 * NT];
-  // each CTA walks a contiguous run of steps (128 items each): consecutive
+  constexpr int KPC = FC::KPC;
+  extern __shared__ __align__(16) unsigned char rf_smem[];
+  const int grp = threadIdx.x / kRfThreads, gtid = threadIdx.x % kRfThreads;
+  int32_t *s_toff = reinterpret_cast<int32_t *>(rf_smem) + grp * FC::TOFF_GRP;
+  const double *res[2] = {nullptr, nullptr};
+  if constexpr (RES != 0) {
+    double *dst = reinterpret_cast<double *>(rf_smem + FC::TOFF_BYTES);
+#pragma unroll
+    for (int k = 2; k <= 3; ++k) {
+      if ((RES >> (k - 2)) & 1) {
+        const double *src = a.cum[k];
+        for (int64_t i = threadIdx.x; i < a.cum_len[k]; i += kThr) dst[i] = __ldg(src + i);
+        res[k - 2] = dst;
+        dst += a.cum_len[k];
+      }
+    }
+  }
+  if constexpr (RES != 0) __syncthreads();  // resident tensors staged
+  // each group walks a contiguous run of steps (128 items each): consecutive
   // output blocks share most factor blocks, which then stay in this SM's L1
-  const int64_t nsteps = (a.nkeys * W + kRfThreads - 1) / kRfThreads;
-  const int64_t per = (nsteps + gridDim.x - 1) / gridDim.x;
-  const int64_t s_begin = (int64_t)blockIdx.x * per;
-  const int64_t s_end = min(nsteps, s_begin + per);
-  for (int64_t step = s_begin; step < s_end; ++step) {
-    const int64_t item0 = step * kRfThreads;
-    const int64_t kb0 = item0 / W;
-    __syncthreads();  // previous step done with s_toff
+  // 32-bit item space: the host launches at most 2^31 items at a time
+  const uint32_t nsteps = (uint32_t)((a.nkeys * W + kRfThreads - 1) / kRfThreads);
+  const uint32_t ngroups = gridDim.x * FC::NGRP;
+  const uint32_t gg = blockIdx.x * FC::NGRP + grp;
+  const uint32_t s_begin = (uint32_t)((uint64_t)nsteps * gg / ngroups);
+  const uint32_t s_end = (uint32_t)((uint64_t)nsteps * (gg + 1) / ngroups);
+  for (uint32_t step = s_begin; step < s_end; ++step) {
+    const uint32_t item0 = step * kRfThreads;
+    const uint32_t kb0 = item0 / W;
+    group_sync(grp);  // previous step done with s_toff
     // stage the term-offset tables of this step's output blocks (coalesced),
     // so every factor address below is a shared-memory read away
-    for (int i = threadIdx.x; i < KPC * 2 * NT; i += kRfThreads) {
-      const int64_t kb = kb0 + i / (2 * NT);
-      if (kb < a.nkeys) s_toff[i] = a.term_off[(int64_t)a.keys[kb] * 2 * NT + i % (2 * NT)];
+    // (one contiguous run of the block-ordered table: coalesced, no indirection)
+    {
+      const int32_t *src = a.term_off + (int64_t)kb0 * 2 * NT;
+      const int64_t left = (a.nkeys - (int64_t)kb0) * 2 * NT;
+      const int lim = left < KPC * 2 * NT ? (int)left : KPC * 2 * NT;
+      for (int i = gtid; i < lim; i += kRfThreads) s_toff[i] = __ldg(src + i);
     }
-    __syncthreads();
-    const int64_t item = item0 + threadIdx.x;
-    const int64_t kb = item / W;
+    group_sync(grp);
+    // 32-bit item arithmetic within the step (the host keeps nkeys * W < 2^31)
+    const int rel = (int)(item0 - kb0 * W) + gtid;  // item offset from block kb0's first item
+    const int kbr = rel / W;                           // W is a compile-time constant
+    const int64_t kb = (int64_t)kb0 + kbr;
     if (kb >= a.nkeys) continue;
-    const int c = (int)(item - kb * W);
-    const int32_t key = a.keys[kb];
-    const int32_t *toff = s_toff + (kb - kb0) * 2 * NT;
+    const int c = rel - kbr * W;
+    const int32_t *toff = s_toff + kbr * 2 * NT;
     int dig[M];
 #pragma unroll
     for (int q = 0; q < M; ++q) dig[q] = 0;
@@ -175,11 +234,11 @@ __global__ void __launch_bounds__(kRfThreads, (rf::ipow(B, M - CT) > 32 ? 3 : 4)
         rem /= B;
       }
     }
-    double *blk = a.mk + a.offs[key] + c;
+    double *blk = a.mk + __ldg(a.blk_off + kb) + c;
     double acc[ROWS];
 #pragma unroll
     for (int row = 0; row < ROWS; ++row) acc[row] = blk[(int64_t)row * W];
-    apply_terms<M, B, CT>(acc, dig, a, toff, std::make_integer_sequence<int, NT>{});
+    apply_terms<M, B, CT, RES>(acc, dig, a, toff, res, std::make_integer_sequence<int, NT>{});
 #pragma unroll
     for (int row = 0; row < ROWS; ++row) blk[(int64_t)row * W] = acc[row];
   }
@@ -230,7 +289,8 @@ struct Staged {
   static constexpr int SEG = rf::seg_before(M, B, NT);
   // staging pays off when the factor sub-blocks are no larger than the
   // output block itself (cfg2, cfg3; cfg4's 25 terms stage 2.6x the block)
-  static constexpr bool ok = SEG * 8 <= 48 * 1024 && NTH <= 1024 && ROWS <= 32 && SEG <= rf::ipow(B, M);
+  static constexpr bool fits = SEG * 8 <= 48 * 1024 && NTH <= 1024 && ROWS <= 32;
+  static constexpr bool ok = fits && SEG <= rf::ipow(B, M);
 };
 
 template <int M, int B, int T>
@@ -262,7 +322,7 @@ __device__ __forceinline__ void apply_term_staged(double (&acc)[Staged<M, B>::RO
   }
   const double *f1 = sm + O1 + o1;
   const double *f2 = sm + O2 + o2;
-  rows_fma<M, B, CT, S, false>(acc, f1, f2, std::make_integer_sequence<int, ROWS>{});
+  rows_fma<M, B, CT, S, false, false>(acc, f1, f2, std::make_integer_sequence<int, ROWS>{});
 }
 
 template <int M, int B, int... Ts>
@@ -279,8 +339,7 @@ __global__ void __launch_bounds__(Staged<M, B>::NTH) k_recursion_staged(RecFactA
   using ST = Staged<M, B>;
   __shared__ double sm[ST::SEG];
   const int tid = threadIdx.x;
-  const int32_t key = a.keys[blockIdx.x];
-  const int32_t *toff = a.term_off + (int64_t)key * 2 * ST::NT;
+  const int32_t *toff = a.term_off + (int64_t)blockIdx.x * 2 * ST::NT;
   const bool active = tid < ST::W;
   const int c = active ? tid : 0;
   int dig[M];
@@ -294,7 +353,7 @@ __global__ void __launch_bounds__(Staged<M, B>::NTH) k_recursion_staged(RecFactA
       rem /= B;
     }
   }
-  double *blk = a.mk + a.offs[key] + c;
+  double *blk = a.mk + a.blk_off[blockIdx.x] + c;
   double acc[ST::ROWS];
   // M_m first: its HBM latency overlaps the factor staging
 #pragma unroll
@@ -401,7 +460,7 @@ __device__ __forceinline__ void pipe_apply_term(double (&acc)[Pipe<M, B>::ROWS],
   }
   const double *f1 = st + O1 + o1;
   const double *f2 = st + O2 + o2;
-  rows_fma<M, B, CT, S, false>(acc, f1, f2, std::make_integer_sequence<int, ROWS>{});
+  rows_fma<M, B, CT, S, false, false>(acc, f1, f2, std::make_integer_sequence<int, ROWS>{});
 }
 
 template <int M, int B, int... Ts>
@@ -422,10 +481,9 @@ __global__ void __launch_bounds__(Pipe<M, B>::NTH) k_recursion_pipe(RecFactArgs 
   const int64_t k_end = a.nkeys * (blockIdx.x + 1) / gridDim.x;
   if (k_begin >= k_end) return;
   auto stage_trow = [&](int64_t i) {  // term-offset row + block offset of key i
-    const int32_t key = a.keys[i];
     int32_t *row = trows + (i % P::TSLOTS) * P::TROW_P;
-    for (int j = tid; j < 2 * P::NT; j += P::NTH) cp_async4(row + j, a.term_off + (int64_t)key * 2 * P::NT + j);
-    if (tid == 0) cp_async8(row + 2 * P::NT, a.offs + key);
+    for (int j = tid; j < 2 * P::NT; j += P::NTH) cp_async4(row + j, a.term_off + i * 2 * P::NT + j);
+    if (tid == 0) cp_async8(row + 2 * P::NT, a.blk_off + i);
   };
   // prologue: offsets of keys k_begin .. k_begin+2D-1, then the data of the first D keys
   for (int64_t i = k_begin; i < k_begin + 2 * D && i < k_end; ++i) stage_trow(i);
@@ -508,18 +566,63 @@ cudaError_t launch_recursion_fact(const RecFactArgs &a, int m, int b, cudaStream
 #undef RF_B
 }
 #else
-template <int M, int B, int CT>
-static cudaError_t go_fact_v2(const RecFactArgs &a, cudaStream_t stream) {
+template <int M, int B, int CT, int RES>
+static cudaError_t launch_v2(const RecFactArgs &a_in, cudaStream_t stream) {
+  using FC = FactCfg<M, B, CT, RES>;
   constexpr int W = rf::ipow(B, CT);
+  // the kernel's item arithmetic is 32-bit: launch key chunks of < 2^31 items
+  constexpr int64_t kMaxKeys = ((int64_t)1 << 31) / W - 1;
+  RecFactArgs a = a_in;
+  while (a.nkeys > kMaxKeys) {
+    RecFactArgs part = a;
+    part.nkeys = kMaxKeys;
+    cudaError_t e = launch_v2<M, B, CT, RES>(part, stream);
+    if (e != cudaSuccess) return e;
+    a.blk_off += kMaxKeys;
+    a.term_off += kMaxKeys * 2 * FC::NT;
+    a.nkeys -= kMaxKeys;
+  }
   const int64_t items = a.nkeys * W;
-  const int threads = kRfThreads;
-  const int64_t steps = (items + threads - 1) / threads;
+  const int threads = FC::NTHR;
+  const int64_t steps = (items + kRfThreads - 1) / kRfThreads;  // 128-item group steps
   if (steps <= 0) return cudaSuccess;
-  static const int per_cta = getenv("BCG_RF_STEPS") ? atoi(getenv("BCG_RF_STEPS")) : 1;  // tuning knob
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(steps, (steps + per_cta - 1) / per_cta));
-  k_recursion_fact<M, B, CT><<<(unsigned)blocks, threads, 0, stream>>>(a);
+  size_t smem = FC::TOFF_BYTES;
+  for (int k = 2; k <= 3; ++k)
+    if ((RES >> (k - 2)) & 1) smem += (size_t)a.cum_len[k] * 8;
+  int64_t blocks;
+  if (RES == 0) {
+    static const int per_cta = getenv("BCG_RF_STEPS") ? atoi(getenv("BCG_RF_STEPS")) : 1;  // tuning knob
+    blocks = std::max<int64_t>(1, std::min<int64_t>(steps, (steps + per_cta - 1) / per_cta));
+  } else {  // persistent: one CTA per SM (the resident copy is paid once per CTA)
+    cudaError_t e = cudaFuncSetAttribute(k_recursion_fact<M, B, CT, RES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_recursion_fact<M, B, CT, RES>, threads, smem);
+    if (e != cudaSuccess) return e;
+    blocks = std::max<int64_t>(1, std::min<int64_t>((steps + FC::NGRP - 1) / FC::NGRP,
+                                                    (int64_t)std::max(1, per_sm) * sms));
+  }
+  k_recursion_fact<M, B, CT, RES><<<(unsigned)blocks, threads, smem, stream>>>(a);
   g_launches++;
   return cudaGetLastError();
+}
+
+// BCG_RF_RES=1/3 (A/B knob): C_2 / C_2 and C_3 resident in shared memory
+// where they fit.  Measured slower than RES=0 on every config (the smaller
+// L1 hurts the C_4 / M_4 factor reads more than LDS helps;
+// profiles/r01_recursion_res.log), so the default is 0.
+template <int M, int B, int CT>
+static cudaError_t go_fact_v2(const RecFactArgs &a, cudaStream_t stream) {
+  static const int forced = getenv("BCG_RF_RES") ? atoi(getenv("BCG_RF_RES")) : 0;
+  const size_t budget = 200 * 1024 - FactCfg<M, B, CT, 1>::TOFF_BYTES;
+  const size_t c2 = (size_t)a.cum_len[2] * 8, c3 = M >= 5 ? (size_t)a.cum_len[3] * 8 : 0;
+  const int res = forced;
+  if (res == 3 && M >= 5 && c2 + c3 <= budget) return launch_v2<M, B, CT, 3>(a, stream);
+  if (res >= 1 && c2 <= budget) return launch_v2<M, B, CT, 1>(a, stream);
+  return launch_v2<M, B, CT, 0>(a, stream);
 }
 
 template <int M, int B>
@@ -549,8 +652,8 @@ cudaError_t go_fact(const RecFactArgs &a, cudaStream_t stream) {
       return cudaGetLastError();
     }
   }
-  if constexpr (Staged<M, B>::ok) {
-    if (!no_staged) {
+  if constexpr (Staged<M, B>::fits) {
+    if (Staged<M, B>::ok ? !no_staged : variant == 3) {
       if (a.nkeys <= 0) return cudaSuccess;
       k_recursion_staged<M, B><<<(unsigned)a.nkeys, Staged<M, B>::NTH, 0, stream>>>(a);
       g_launches++;

@@ -1,18 +1,31 @@
-"""Multi-GPU cumulants: the sample axis t sharded across ranks (one process per
-GPU, torch.distributed over NCCL).
+"""Multi-GPU cumulants: one process per GPU, torch.distributed over NCCL.
 
-This is the paper's Alg. 3 and the reference's
-sample-split ``moment_parallel`` (bc/moments.py:66-96) with the threads
-replaced by GPUs and the Python reduction loop by collectives:
+Two ways to split the work (SURVEY §8 e and §8 f row 3):
+
+**Sample split** (``cumulants_upto_sharded``; the default, BASELINE cfg5).
+The paper's Alg. 3 and the reference's ``moment_parallel``
+(bc/moments.py:66-96) with the threads replaced by GPUs:
 
 1. every rank holds a contiguous row shard (bounds t*s//p, bc/moments.py:66-68);
 2. column sums are all-reduced (n doubles) -> the single global mean the
    reference's ``center`` uses (bc/cumulants.py:190); each rank centers its shard;
-3. per order k: local packed RAW sums (the DMMA GEMM) -> NCCL all-reduce(SUM)
-   -> / t_total, i.e. the global central moment M_k on every rank;
-4. the recursion is split by block list (bc/moments.py:114-131): rank r
-   corrects blocks [K r/W, K (r+1)/W) in place and an all-gather rebuilds C_k
-   everywhere (the next order's recursion reads every block of it).
+3. per order k: local packed RAW sums (the DMMA GEMM), then
+   * orders the later recursions read (k <= m-2): NCCL all-reduce(SUM) ->
+     / t_total -> every rank runs the (microsecond-scale) recursion on all
+     blocks, so C_k (and the central moment M_k the factored recursion needs)
+     is replicated without a second collective;
+   * the two top orders (k >= m-1, k >= 4): reduce-scatter by block range
+     (bc/moments.py:114-131 split) -> / t_total -> recursion on the rank's
+     own blocks -> all-gather: 2x the packed size on the wire instead of the
+     3x of all-reduce + all-gather (cfg5: C6 is 20 GB).
+
+**Block split** (``cumulants_upto_block_split``; ``moment_parallel_blocks``,
+bc/moments.py:99-131, across GPUs).  Every rank holds ALL of X; rank r
+computes blocks [K r/W, K (r+1)/W) of every order (moment + recursion) and an
+all-gather per order rebuilds C_k.  No moment collective, no partial M_k per
+GPU (cfg5: 20 GB less per GPU), X read W times in total; results bitwise equal
+to the single-GPU path (every key range of the moment kernel sums in the same
+order).
 
 The per-rank compute goes through an ``ops`` object; the default is the
 sm_100a library.  (The CPU multi-process tests substitute the oracle for it to
@@ -60,6 +73,13 @@ class CudaOps:
         st = _colstats(X, sums=True, sumsq=True, bad=True)
         return st["sums"], st["sumsq"], st["bad"]
 
+    def colmean(self, X):
+        """(mean, first_bad) of the whole matrix, as cumulants_upto computes them."""
+        from .moments import _colstats
+
+        st = _colstats(X, mean=True, bad=True)
+        return st["mean"], st["bad"]
+
     def center(self, X, mean):
         """Centered data in the moment kernel's transposed layout: (xt, t)."""
         from .moments import _center_transposed
@@ -71,12 +91,26 @@ class CudaOps:
 
         return _rowstats(*centered)
 
-    def moment_raw(self, centered, k: int, b: int):
-        from .moments import _moment_raw_t_into
+    def moment_raw(self, centered, k: int, b: int, key_range=None):
+        """Packed RAW order-k sums (all blocks, or blocks [k0, k1) only; the
+        rest of the buffer stays zero)."""
+        from . import _native
 
         xt, t = centered
-        out = torch.zeros(layout(xt.shape[0], k, b).size, dtype=torch.float64, device=xt.device)
-        _moment_raw_t_into(xt, t, k, b, out)
+        n, ldt = xt.shape
+        out = torch.zeros(layout(n, k, b).size, dtype=torch.float64, device=xt.device)
+        plan = _native.plan(n, k, b)
+        wsb = plan.ws_bytes(t)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=xt.device) if wsb else None
+        wsp = ws.data_ptr() if ws is not None else None
+        lib = _native.lib()
+        if key_range is None:
+            rc = lib.bcg_moment_raw_t(plan.handle, xt.data_ptr(), t, ldt, out.data_ptr(), wsp, wsb,
+                                      _native.stream_handle())
+        else:
+            rc = lib.bcg_moment_raw_t_range(plan.handle, xt.data_ptr(), t, ldt, out.data_ptr(), wsp, wsb,
+                                            int(key_range[0]), int(key_range[1]), _native.stream_handle())
+        _native.check(rc, "moment")
         return out
 
     def divide(self, buf, t: int):
@@ -84,7 +118,10 @@ class CudaOps:
 
         _divide(buf, t)
 
-    def recursion_range(self, mk, n: int, k: int, b: int, lower: dict, k0: int, k1: int):
+    def recursion_range(self, mk, n: int, k: int, b: int, lower: dict, k0: int, k1: int, central=None):
+        """C_k in place on blocks [k0, k1) of the packed M_k.  ``central``
+        (order -> packed central moment, orders 4..k-2) selects the factored
+        kernel at k >= 6 (bcg_cumulant_recursion_ex)."""
         import ctypes
 
         from . import _native
@@ -93,8 +130,12 @@ class CudaOps:
         arr = (ctypes.c_void_p * 15)()
         for j, t in lower.items():
             arr[j - 2] = t.data_ptr()
-        _native.check(_native.lib().bcg_cumulant_recursion_range(
-            plan.handle, mk.data_ptr(), arr, int(k0), int(k1), _native.stream_handle()), "recursion")
+        cm = (ctypes.c_void_p * 15)()
+        for j, t in (central or {}).items():
+            if 4 <= j <= k - 2:
+                cm[j - 2] = t.data_ptr()
+        _native.check(_native.lib().bcg_cumulant_recursion_ex(
+            plan.handle, mk.data_ptr(), arr, cm, int(k0), int(k1), _native.stream_handle()), "recursion")
 
 
 def _check_centered(sums, sumsq, t: int):
@@ -139,6 +180,7 @@ def cumulants_upto_sharded(x_local, m_max: int, b: int = 2, group=None, ops=None
         dist.all_reduce(both, group=group)
         _check_centered(both[:n], both[n:], t_total)
         lower: dict = {}
+        central: dict = {}  # central moments M_4..M_{m-2} (factored recursion)
         for k in range(2, m_max + 1):
             top = k == m_max and timer is not None
             if top:
@@ -149,17 +191,79 @@ def cumulants_upto_sharded(x_local, m_max: int, b: int = 2, group=None, ops=None
             if top:
                 ev1.record()
                 timer.setdefault("moment_top", []).append((ev0, ev1))
-            if world > 1:
-                dist.all_reduce(mk, group=group)
-            ops.divide(mk, t_total)
-            if k >= 4:
-                lay = layout(n, k, b)
-                if world == 1:
-                    ops.recursion_range(mk, n, k, b, lower, 0, lay.K)
-                else:
-                    k0, k1 = block_bounds(lay.K, world, rank)
-                    ops.recursion_range(mk, n, k, b, lower, k0, k1)
+            lay = layout(n, k, b)
+            if world > 1 and k >= 4 and k >= m_max - 1:
+                # top orders: reduce-scatter -> own blocks -> all-gather
+                k0, k1 = block_bounds(lay.K, world, rank)
+                _reduce_scatter_blocks(mk, lay, world, group)
+                lo, hi = int(lay.offs[k0]), int(lay.offs[k1])
+                ops.divide(mk[lo:hi], t_total)
+                ops.recursion_range(mk, n, k, b, lower, k0, k1, central)
+                _allgather_blocks(mk, lay, world, group)
+            else:
+                if world > 1:
+                    dist.all_reduce(mk, group=group)
+                ops.divide(mk, t_total)
+                if 4 <= k <= m_max - 2:
+                    central[k] = mk.clone()
+                if k >= 4:
+                    ops.recursion_range(mk, n, k, b, lower, 0, lay.K, central)
+            lower[k] = mk
+            tensors.append(mk)
+    return mean, tensors
+
+
+def cumulants_upto_block_split(x_full, m_max: int, b: int = 2, group=None, ops=None,
+                               timer: Optional[dict] = None):
+    """Cumulants C_1..C_m of ``x_full`` (the SAME full matrix on every rank),
+    split by block list across ranks: rank r computes the moments and the
+    recursion of blocks [K r/W, K (r+1)/W) of every order; an all-gather per
+    order rebuilds C_k on every rank.  Collective; returns (c1, [C_2..C_m]),
+    bitwise identical to the single-GPU ``cumulants_upto``."""
+    if not 1 <= m_max <= MAX_M:
+        raise ValidationError(f"m_max must be in 1..{MAX_M}, got {m_max}")
+    ops = ops or CudaOps()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    X = ops.matrix(x_full)
+    t, n = X.shape
+    mean, bad = ops.colmean(X)
+    if int(bad.item()) >= 0:
+        i = int(bad.item())
+        raise ValidationError(f"non-finite value at row {i // n + 1}, column {i % n + 1}")
+    if m_max >= 2 and t < 2:
+        raise ValidationError("at least two samples are required for order >= 2")
+    tensors = []
+    if m_max >= 2:
+        Xc = ops.center(X, mean)
+        csum, csq = ops.centered_stats(Xc)
+        _check_centered(csum, csq, t)
+        lower: dict = {}
+        central: dict = {}
+        for k in range(2, m_max + 1):
+            lay = layout(n, k, b)
+            k0, k1 = block_bounds(lay.K, world, rank)
+            top = k == m_max and timer is not None
+            if top:
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev0.record()
+            mk = ops.moment_raw(Xc, k, b, key_range=(k0, k1))
+            if top:
+                ev1.record()
+                timer.setdefault("moment_top", []).append((ev0, ev1))
+            lo, hi = int(lay.offs[k0]), int(lay.offs[k1])
+            ops.divide(mk[lo:hi], t)
+            if 4 <= k <= m_max - 2:
+                # the factored recursion of higher orders reads the central
+                # moment of every block: gather it before correcting in place
+                if world > 1:
                     _allgather_blocks(mk, lay, world, group)
+                central[k] = mk.clone()
+            if k >= 4:
+                ops.recursion_range(mk, n, k, b, lower, k0, k1, central)
+            if world > 1:
+                _allgather_blocks(mk, lay, world, group)
             lower[k] = mk
             tensors.append(mk)
     return mean, tensors
@@ -170,12 +274,32 @@ def _device_div(v, t, ops):
     return v
 
 
-def _allgather_blocks(mk, lay, world: int, group) -> None:
-    """Rebuild the full packed tensor from each rank's block range."""
+def _block_spans(lay, world: int):
     spans = []
     for r in range(world):
         k0, k1 = block_bounds(lay.K, world, r)
         spans.append((int(lay.offs[k0]), int(lay.offs[k1])))
+    return spans
+
+
+def _reduce_scatter_blocks(mk, lay, world: int, group) -> None:
+    """Sum ``mk`` over ranks into this rank's block range only (the other
+    ranges are left stale; _allgather_blocks overwrites them)."""
+    spans = _block_spans(lay, world)
+    width = max(hi - lo for lo, hi in spans)
+    rank = dist.get_rank(group)
+    send = torch.zeros(width * world, dtype=mk.dtype, device=mk.device)
+    for r, (a, z) in enumerate(spans):
+        send[r * width: r * width + (z - a)] = mk[a:z]
+    recv = torch.empty(width, dtype=mk.dtype, device=mk.device)
+    dist.reduce_scatter_tensor(recv, send, group=group)
+    lo, hi = spans[rank]
+    mk[lo:hi] = recv[: hi - lo]
+
+
+def _allgather_blocks(mk, lay, world: int, group) -> None:
+    """Rebuild the full packed tensor from each rank's block range."""
+    spans = _block_spans(lay, world)
     width = max(hi - lo for lo, hi in spans)
     rank = dist.get_rank(group)
     lo, hi = spans[rank]

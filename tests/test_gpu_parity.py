@@ -399,18 +399,21 @@ def test_v1_tile_shapes_match_oracle_and_each_other(tile, monkeypatch, rng):
         np.testing.assert_allclose(packed(bcg.moment(x2, m, b)), orc.moment(x2, m, b), rtol=1e-12, atol=1e-14)
 
 
-def _nccl_worker(rank, world, port, x, m, b, out):
+def _nccl_worker(rank, world, port, x, m, b, out, mode="samples"):
     import os
 
     import torch.distributed as dist
 
-    from paper_1701_05420_b200.distributed import cumulants_upto_sharded, shard_bounds
+    from paper_1701_05420_b200.distributed import cumulants_upto_block_split, cumulants_upto_sharded, shard_bounds
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world)
-    lo, hi = shard_bounds(x.shape[0], world, rank)
-    mean, ts = cumulants_upto_sharded(torch.from_numpy(x[lo:hi]).cuda(), m, b)
+    if mode == "samples":
+        lo, hi = shard_bounds(x.shape[0], world, rank)
+        mean, ts = cumulants_upto_sharded(torch.from_numpy(x[lo:hi]).cuda(), m, b)
+    else:
+        mean, ts = cumulants_upto_block_split(torch.from_numpy(x).cuda(), m, b)
     np.savez(out, mean=mean.cpu().numpy(), **{f"c{k}": t.cpu().numpy() for k, t in enumerate(ts, 2)})
     dist.destroy_process_group()
 
@@ -435,10 +438,33 @@ def test_sharded_path_over_nccl_single_rank(tmp_path, rng):
         np.testing.assert_allclose(got[f"c{k}"], want[k], rtol=1e-9, atol=1e-12)
 
 
+def test_block_split_path_over_nccl_single_rank_bitwise(tmp_path, rng):
+    """The block-split multi-GPU mode on the real CUDA ops + NCCL (world size
+    1 here) is bitwise identical to cumulants_upto (every key range of the
+    moment kernel sums in the same order)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    x = rng.exponential(1.0, size=(3001, 9)) + rng.standard_normal((3001, 9))
+    out = str(tmp_path / "r0.npz")
+    mp.spawn(_nccl_worker, args=(1, port, x, 6, 3, out, "blocks"), nprocs=1, join=True)
+    got = np.load(out)
+    cs = bcg.cumulants_upto(x, 6, b=3)
+    np.testing.assert_array_equal(got["mean"], cs[1])
+    for k in range(2, 7):
+        np.testing.assert_array_equal(got[f"c{k}"], cs[k].packed_host())
+
+
 _VARIANT_SHAPES = [(16, 4, 8, 300), (12, 5, 4, 400), (9, 6, 3, 300), (12, 6, 6, 200), (12, 5, 6, 300), (7, 6, 3, 250)]
 
 
 @pytest.mark.parametrize("env", [{"BCG_RF_VARIANT": "2", "BCG_RF_TILE": "-1"}, {"BCG_RF_VARIANT": "2", "BCG_RF_TILE": "0"},
+                                 {"BCG_RF_VARIANT": "2", "BCG_RF_RES": "0"}, {"BCG_RF_VARIANT": "2", "BCG_RF_RES": "1"},
+                                 {"BCG_RF_VARIANT": "2", "BCG_RF_RES": "3"},
                                  {"BCG_RF_VARIANT": "2", "BCG_RF_TILE": "1"}, {"BCG_RF_VARIANT": "3"},
                                  {"BCG_RF_VARIANT": "4"}, {}])
 def test_recursion_variants_match_oracle(env, tmp_path):
