@@ -85,6 +85,19 @@ struct HeadOff {
 
 }  // namespace rf
 
+// cp.async (LDGSTS) helpers
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 // acc[row] -= f1[row offset in S] * f2[row offset in REST] for every register row
 template <bool LDG>
 __device__ __forceinline__ double ld_factor(const double *p) {
@@ -241,6 +254,121 @@ __global__ void __launch_bounds__(FactCfg<M, B, CT, RES>::NTHR, FactCfg<M, B, CT
     apply_terms<M, B, CT, RES>(acc, dig, a, toff, res, std::make_integer_sequence<int, NT>{});
 #pragma unroll
     for (int row = 0; row < ROWS; ++row) blk[(int64_t)row * W] = acc[row];
+  }
+}
+
+// v5: v2's evaluation in persistent CTAs whose 128-thread groups walk a
+// contiguous run of steps with a one-step software pipeline: while step s is
+// evaluated, cp.async (LDGSTS) is already streaming step s+1's M_m rows into
+// a thread-private shared-memory column and step s+1's term-offset rows into
+// the other half of a double buffer, so the HBM latency of M_m no longer sits
+// in front of every step (v2 is long-scoreboard bound at ~25% occupancy).
+template <int M, int B, int CT, int... Ts>
+__device__ __forceinline__ void apply_terms_from1(double (&acc)[rf::ipow(B, M - CT)], const int (&dig)[M],
+                                                  const RecFactArgs &a, const int32_t *toff,
+                                                  std::integer_sequence<int, Ts...>) {
+  (apply_term<M, B, CT, 0, Ts + 1>(acc, dig, a, toff, nullptr), ...);
+}
+
+template <int M, int B, int CT>
+struct PipeCfg {
+  static constexpr int NT = rf::term_count(M);
+  static constexpr int ROWS = rf::ipow(B, M - CT);
+  static constexpr int W = rf::ipow(B, CT);
+  static constexpr int KPC = (kRfThreads + W - 1) / W + 1;
+  static constexpr int TOFF = (KPC * 2 * NT + 3) / 4 * 4;  // int32 per buffer
+  static constexpr size_t SMEM = (size_t)2 * TOFF * 4 + (size_t)ROWS * kRfThreads * 8;
+};
+
+template <int M, int B, int CT>
+__global__ void __launch_bounds__(kRfThreads, (rf::ipow(B, M - CT) > 32 ? 2 : 3)) k_recursion_fact_pipe(RecFactArgs a) {
+  using PC = PipeCfg<M, B, CT>;
+  constexpr int NT = PC::NT, ROWS = PC::ROWS, W = PC::W, KPC = PC::KPC;
+  extern __shared__ __align__(16) unsigned char rf_smem[];
+  int32_t *s_toff = reinterpret_cast<int32_t *>(rf_smem);                 // [2][TOFF]
+  double *s_m = reinterpret_cast<double *>(rf_smem + 2 * PC::TOFF * 4);   // [ROWS][128]
+  const int tid = threadIdx.x;
+  const uint32_t nsteps = (uint32_t)((a.nkeys * W + kRfThreads - 1) / kRfThreads);
+  const uint32_t s_begin = (uint32_t)((uint64_t)nsteps * blockIdx.x / gridDim.x);
+  const uint32_t s_end = (uint32_t)((uint64_t)nsteps * (blockIdx.x + 1) / gridDim.x);
+  if (s_begin >= s_end) return;
+  auto stage_toff = [&](uint32_t step, int buf) {
+    const uint32_t kb0 = step * kRfThreads / W;
+    const int32_t *src = a.term_off + (int64_t)kb0 * 2 * NT;
+    const int64_t left = (a.nkeys - (int64_t)kb0) * 2 * NT;
+    const int lim = left < KPC * 2 * NT ? (int)left : KPC * 2 * NT;
+    for (int i = tid; i < lim; i += kRfThreads) cp_async4(s_toff + buf * PC::TOFF + i, src + i);
+  };
+  // item of this thread in step s: (block kb, column c); kb >= nkeys: idle
+  auto item_of = [&](uint32_t step, int64_t &kb, int &c) {
+    const uint32_t item = step * kRfThreads + tid;
+    const uint32_t k = item / W;
+    kb = k;
+    c = (int)(item - k * W);
+  };
+  auto stage_m = [&](int64_t kb, int c) {
+    if (kb < a.nkeys) {
+      const double *src = a.mk + __ldg(a.blk_off + kb) + c;
+#pragma unroll
+      for (int row = 0; row < ROWS; ++row) cp_async8(s_m + row * kRfThreads + tid, src + (int64_t)row * W);
+    }
+  };
+  // prologue: offsets of the first step, then its M_m rows
+  stage_toff(s_begin, 0);
+  cp_async_commit();
+  {
+    int64_t kb;
+    int c;
+    item_of(s_begin, kb, c);
+    stage_m(kb, c);
+  }
+  cp_async_commit();
+  cp_async_wait<1>();  // offsets of the first step
+  __syncthreads();
+  for (uint32_t step = s_begin; step < s_end; ++step) {
+    const int buf = (step - s_begin) & 1;
+    const bool more = step + 1 < s_end;
+    if (more) stage_toff(step + 1, buf ^ 1);
+    cp_async_commit();
+    int64_t kb;
+    int c;
+    item_of(step, kb, c);
+    int64_t kb_n = a.nkeys;
+    int c_n = 0;
+    if (more) item_of(step + 1, kb_n, c_n);
+    const bool active = kb < a.nkeys;
+    int64_t boff = 0;
+    if (active) boff = __ldg(a.blk_off + kb);
+    cp_async_wait<1>();  // this step's M_m rows (the group before the offsets just issued)
+    double acc[ROWS];
+    int dig[M];
+    const int32_t *toff = s_toff + buf * PC::TOFF + (int)(kb - (int64_t)(step * kRfThreads / W)) * 2 * NT;
+    if (active) {
+#pragma unroll
+      for (int q = 0; q < M; ++q) dig[q] = 0;
+      {
+        int rem = c;
+#pragma unroll
+        for (int q = M - 1; q >= M - CT; --q) {
+          dig[q] = rem % B;
+          rem /= B;
+        }
+      }
+#pragma unroll
+      for (int row = 0; row < ROWS; ++row) acc[row] = s_m[row * kRfThreads + tid];
+      apply_term<M, B, CT, 0, 0>(acc, dig, a, toff, nullptr);  // consumes every acc: the LDS are done
+    }
+    // the column is free again: stream the next step's rows into it
+    if (more) stage_m(kb_n, c_n);
+    cp_async_commit();
+    if (active) {
+      apply_terms_from1<M, B, CT>(acc, dig, a, toff, std::make_integer_sequence<int, NT - 1>{});
+      double *blk = a.mk + boff + c;
+#pragma unroll
+      for (int row = 0; row < ROWS; ++row) blk[(int64_t)row * W] = acc[row];
+    }
+    cp_async_wait<1>();  // next step's offsets (older than its M_m rows)
+    __syncthreads();     // ... visible to all; everyone done with this step's offsets
   }
 }
 
@@ -406,17 +534,6 @@ struct Pipe {
   static constexpr bool ok = ROWS <= 64 && SMEM <= 160 * 1024;
 };
 
-__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 template <int M, int B, int T>
 __device__ __forceinline__ void pipe_stage_term(double *st, const RecFactArgs &a, const int32_t *trow, int tid) {
@@ -615,7 +732,44 @@ static cudaError_t launch_v2(const RecFactArgs &a_in, cudaStream_t stream) {
 // L1 hurts the C_4 / M_4 factor reads more than LDS helps;
 // profiles/r01_recursion_res.log), so the default is 0.
 template <int M, int B, int CT>
+static cudaError_t launch_v5(const RecFactArgs &a_in, cudaStream_t stream) {
+  using PC = PipeCfg<M, B, CT>;
+  constexpr int64_t kMaxKeys = ((int64_t)1 << 31) / PC::W - 1;
+  RecFactArgs a = a_in;
+  while (a.nkeys > kMaxKeys) {
+    RecFactArgs part = a;
+    part.nkeys = kMaxKeys;
+    cudaError_t e = launch_v5<M, B, CT>(part, stream);
+    if (e != cudaSuccess) return e;
+    a.blk_off += kMaxKeys;
+    a.term_off += kMaxKeys * 2 * PC::NT;
+    a.nkeys -= kMaxKeys;
+  }
+  const int64_t steps = (a.nkeys * PC::W + kRfThreads - 1) / kRfThreads;
+  if (steps <= 0) return cudaSuccess;
+  static int cap = 0;
+  if (!cap) {
+    cudaError_t e = cudaFuncSetAttribute(k_recursion_fact_pipe<M, B, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)PC::SMEM);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_recursion_fact_pipe<M, B, CT>, kRfThreads, PC::SMEM);
+    if (e != cudaSuccess) return e;
+    static const int ctas = getenv("BCG_RF_PIPE_CTAS") ? atoi(getenv("BCG_RF_PIPE_CTAS")) : 0;  // tuning knob
+    cap = std::max(1, ctas > 0 ? std::min(ctas, per_sm) : per_sm) * sms;
+  }
+  const int64_t grid = std::min<int64_t>(steps, cap);
+  k_recursion_fact_pipe<M, B, CT><<<(unsigned)grid, kRfThreads, PC::SMEM, stream>>>(a);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+template <int M, int B, int CT>
 static cudaError_t go_fact_v2(const RecFactArgs &a, cudaStream_t stream) {
+  static const bool pipe = getenv("BCG_RF_PIPE") && atoi(getenv("BCG_RF_PIPE")) > 0;  // A/B knob
+  if (pipe) return launch_v5<M, B, CT>(a, stream);
   static const int forced = getenv("BCG_RF_RES") ? atoi(getenv("BCG_RF_RES")) : 0;
   const size_t budget = 200 * 1024 - FactCfg<M, B, CT, 1>::TOFF_BYTES;
   const size_t c2 = (size_t)a.cum_len[2] * 8, c3 = M >= 5 ? (size_t)a.cum_len[3] * 8 : 0;
