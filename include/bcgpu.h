@@ -163,6 +163,13 @@ int bcg_transpose_pad(const double *x, int64_t t, int64_t n, int64_t ldx,
  * bc/cumulants.py:31-39).  Deterministic. */
 int bcg_rowstats(const double *xt, int64_t n, int64_t t, int64_t ldt,
                  double *sums, double *sumsq, void *stream);
+/* Same, split into row segments so small n still fills the GPU; `ws` must
+ * hold bcg_rowstats_ws_bytes(n, t) bytes (segment partials, added in segment
+ * order: deterministic). */
+size_t bcg_rowstats_ws_bytes(int64_t n, int64_t t);
+int bcg_rowstats_ws(const double *xt, int64_t n, int64_t t, int64_t ldt,
+                    double *sums, double *sumsq, void *ws, size_t ws_bytes,
+                    void *stream);
 /* Same, restricted to blocks [k0, k1) (only out[offs[k0]:offs[k1]] is
  * touched; bitwise identical to the full call on those blocks) -- the
  * block-split path of moment_parallel_blocks (bc/moments.py:99-131). */

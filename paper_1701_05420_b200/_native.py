@@ -55,6 +55,8 @@ SIGNATURES = [
     ("bcg_padded_t", _i64, [_i64]),
     ("bcg_transpose_pad", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp]),
     ("bcg_rowstats", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    ("bcg_rowstats_ws_bytes", _sz, [_i64, _i64]),
+    ("bcg_rowstats_ws", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
     ("bcg_moment_raw_range", ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _sz, _i64, _i64, _vp]),
     ("bcg_moment_raw_t_range", ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _sz, _i64, _i64, _vp]),
     ("bcg_cumulant_recursion", ctypes.c_int, [_vp, _vp, _vp, _vp]),

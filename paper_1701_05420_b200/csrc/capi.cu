@@ -428,7 +428,24 @@ int64_t bcg_padded_t(int64_t t) { return bcg::padded_t(t); }
 
 int bcg_rowstats(const double *xt, int64_t n, int64_t t, int64_t ldt, double *sums, double *sumsq, void *stream) {
   if (t < 1 || n < 1 || ldt < t) return fail(BCG_EINVAL, "bad shape");
-  CUDA_TRY(bcg::launch_rowstats(xt, n, t, ldt, sums, sumsq, static_cast<cudaStream_t>(stream)), "rowstats");
+  CUDA_TRY(bcg::launch_rowstats(xt, n, t, ldt, sums, sumsq, nullptr, 1, static_cast<cudaStream_t>(stream)),
+           "rowstats");
+  return BCG_OK;
+}
+
+size_t bcg_rowstats_ws_bytes(int64_t n, int64_t t) {
+  if (n < 1 || t < 1) return 0;
+  return (size_t)n * bcg::rowstats_parts(n, t) * 2 * sizeof(double);
+}
+
+int bcg_rowstats_ws(const double *xt, int64_t n, int64_t t, int64_t ldt, double *sums, double *sumsq, void *ws,
+                    size_t ws_bytes, void *stream) {
+  if (t < 1 || n < 1 || ldt < t) return fail(BCG_EINVAL, "bad shape");
+  const int P = bcg::rowstats_parts(n, t);
+  if (ws_bytes < (size_t)n * P * 2 * sizeof(double)) return fail(BCG_EINVAL, "rowstats workspace too small");
+  CUDA_TRY(bcg::launch_rowstats(xt, n, t, ldt, sums, sumsq, static_cast<double *>(ws), P,
+                                static_cast<cudaStream_t>(stream)),
+           "rowstats");
   return BCG_OK;
 }
 

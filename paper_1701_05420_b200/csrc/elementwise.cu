@@ -30,12 +30,15 @@ __global__ void __launch_bounds__(kCsThreads)
     const int64_t c = cbase + c0;
     double s = 0.0, q = 0.0;
     if (active && c < n) {
+      unsigned long long bad = ~0ULL;  // first non-finite position seen (one atomic per thread, after the loop)
+#pragma unroll 4
       for (int64_t r = r0 + rph; r < r1; r += rpi) {
         const double v = x[r * ldx + c];
-        if (!isfinite(v)) atomicMin(first_bad, (unsigned long long)(r * n + c));
+        if (!isfinite(v)) bad = min(bad, (unsigned long long)(r * n + c));
         s += v;
         q += v * v;
       }
+      if (bad != ~0ULL) atomicMin(first_bad, bad);
     }
     red_s[tid] = s;
     red_q[tid] = q;
@@ -222,14 +225,22 @@ cudaError_t launch_pad_rows(const double *src, int64_t n, int64_t t, int64_t lds
   return cudaGetLastError();
 }
 
-// per row c of xt (n x ldt): sums[c] = sum_{l<t} xt[c, l], sumsq[c] = sum xt^2
-// (one CTA per row, fixed-order tree: deterministic)
-__global__ void k_rowstats(const double *__restrict__ xt, int64_t t, int64_t ldt, double *sums, double *sumsq) {
+// per row c of xt (n x ldt): sums[c] = sum_{l<t} xt[c, l], sumsq[c] = sum xt^2.
+// Segment p of P of each row per CTA (grid n x P, so even n = 36 fills the
+// GPU), 4 loads in flight per thread, fixed-order tree; with P > 1 the
+// partials go to `part` and k_rowstats_final adds them in segment order
+// (deterministic).
+__global__ void k_rowstats(const double *__restrict__ xt, int64_t t, int64_t ldt, int P, double *sums,
+                           double *sumsq, double *__restrict__ part) {
   __shared__ double rs[256], rq[256];
-  const int64_t c = blockIdx.x;
+  const int64_t c = blockIdx.x / P;
+  const int p = blockIdx.x % P;
+  const int64_t l0 = t * p / P, l1 = t * (p + 1) / P;
   double s = 0.0, q = 0.0;
-  for (int64_t l = threadIdx.x; l < t; l += 256) {
-    const double v = xt[c * ldt + l];
+  const double *row = xt + c * ldt;
+#pragma unroll 4
+  for (int64_t l = l0 + threadIdx.x; l < l1; l += 256) {
+    const double v = row[l];
     s += v;
     q += v * v;
   }
@@ -244,15 +255,44 @@ __global__ void k_rowstats(const double *__restrict__ xt, int64_t t, int64_t ldt
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    if (sums) sums[c] = rs[0];
-    if (sumsq) sumsq[c] = rq[0];
+    if (part) {
+      part[2 * blockIdx.x] = rs[0];
+      part[2 * blockIdx.x + 1] = rq[0];
+    } else {
+      if (sums) sums[c] = rs[0];
+      if (sumsq) sumsq[c] = rq[0];
+    }
   }
 }
 
+__global__ void k_rowstats_final(const double *__restrict__ part, int64_t n, int P, double *sums, double *sumsq) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0, q = 0.0;
+    for (int p = 0; p < P; ++p) {
+      s += part[2 * (c * P + p)];
+      q += part[2 * (c * P + p) + 1];
+    }
+    if (sums) sums[c] = s;
+    if (sumsq) sumsq[c] = q;
+  }
+}
+
+int rowstats_parts(int64_t n, int64_t t) {
+  int64_t P = (4 * 148 + n - 1) / n;
+  const int64_t by_len = (t + 4095) / 4096;  // >= 4096 samples per segment
+  if (P > by_len) P = by_len;
+  return P < 1 ? 1 : (int)P;
+}
+
 cudaError_t launch_rowstats(const double *xt, int64_t n, int64_t t, int64_t ldt, double *sums, double *sumsq,
-                            cudaStream_t stream) {
-  k_rowstats<<<(unsigned)n, 256, 0, stream>>>(xt, t, ldt, sums, sumsq);
+                            double *ws, int P, cudaStream_t stream) {
+  if (!ws) P = 1;
+  k_rowstats<<<(unsigned)(n * P), 256, 0, stream>>>(xt, t, ldt, P, sums, sumsq, P > 1 ? ws : nullptr);
   g_launches++;
+  if (P > 1) {
+    k_rowstats_final<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(ws, n, P, sums, sumsq);
+    g_launches++;
+  }
   return cudaGetLastError();
 }
 

@@ -54,7 +54,8 @@ cudaError_t launch_transpose_pad(const double *x, int64_t t, int64_t n, int64_t 
 cudaError_t launch_pad_rows(const double *src, int64_t n, int64_t t, int64_t lds, double *dst, int64_t ldt,
                             cudaStream_t stream);
 cudaError_t launch_rowstats(const double *xt, int64_t n, int64_t t, int64_t ldt, double *sums, double *sumsq,
-                            cudaStream_t stream);
+                            double *ws, int P, cudaStream_t stream);
+int rowstats_parts(int64_t n, int64_t t);
 // padded sample count of the transposed layout the moment kernel reads
 inline int64_t padded_t(int64_t t) { return (t + 15) / 16 * 16; }
 cudaError_t launch_div(int64_t len, const double *x, double d, double *out, cudaStream_t stream);

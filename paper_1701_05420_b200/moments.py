@@ -141,10 +141,12 @@ def _rowstats(xt, t: int):
     """Column sums / sums of squares of the data from its transposed layout."""
     torch = _native.torch_cuda()
     n, ldt = xt.shape
-    sums = torch.empty(n, dtype=torch.float64, device=xt.device)
-    sq = torch.empty(n, dtype=torch.float64, device=xt.device)
-    _native.check(_native.lib().bcg_rowstats(xt.data_ptr(), n, t, ldt, sums.data_ptr(), sq.data_ptr(),
-                                             _native.stream_handle()), "rowstats")
+    lib = _native.lib()
+    wsb = int(lib.bcg_rowstats_ws_bytes(n, t))
+    buf = torch.empty(2 * n + wsb // 8, dtype=torch.float64, device=xt.device)
+    sums, sq, ws = buf[:n], buf[n:2 * n], buf[2 * n:]
+    _native.check(lib.bcg_rowstats_ws(xt.data_ptr(), n, t, ldt, sums.data_ptr(), sq.data_ptr(), ws.data_ptr(), wsb,
+                                      _native.stream_handle()), "rowstats")
     return sums, sq
 
 
