@@ -33,6 +33,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", nargs="+", default=["cfg2", "cfg3", "cfg4"])
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--copy-ref", action="store_true", help="also time a same-size device copy (the HBM ceiling at this size)")
     a = ap.parse_args()
     peak, src = hbm_peak()
     for name in a.configs:
@@ -80,8 +81,28 @@ def main():
             torch.cuda.synchronize()
             ms = sorted(x.elapsed_time(y) for x, y in ts)[len(ts) // 2]
             gbs = alg / (ms / 1e3) / 1e9
+            # copy ceiling: a device copy of the same S_m doubles (16 S_m bytes),
+            # timed the same way (L2 flushed, one launch between two events)
+            if a.copy_ref:
+                src_buf = base
+                dst_buf = torch.empty_like(base)
+                cts = []
+                for _ in range(a.reps):
+                    flush.fill_(1.0)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    dst_buf.copy_(src_buf)
+                    e1.record()
+                    cts.append((e0, e1))
+                torch.cuda.synchronize()
+                cms = sorted(x.elapsed_time(y) for x, y in cts)[len(cts) // 2]
+                copy_note = (f"; same-size copy {cms * 1e3:.1f} us = {100 * 16 * S / (cms / 1e3) / 1e9 / peak:.1f}%"
+                             f" -> recursion at {100 * cms / ms:.0f}% of copy speed")
+                del dst_buf
+            else:
+                copy_note = ""
             print(f"{name} m={m} S_m={S} recursion[{label}] {ms * 1e3:9.1f} us  {gbs:8.1f} GB/s "
-                  f"= {100 * gbs / peak:5.1f}% of {peak:.0f} GB/s ({src})", flush=True)
+                  f"= {100 * gbs / peak:5.1f}% of {peak:.0f} GB/s ({src}){copy_note}", flush=True)
         os.environ.pop("BCG_RECURSION_PARTITION", None)
 
 
