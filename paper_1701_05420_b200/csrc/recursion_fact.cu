@@ -372,6 +372,149 @@ __global__ void __launch_bounds__(kRfThreads, (rf::ipow(B, M - CT) > 32 ? 2 : 3)
   }
 }
 
+// v6 (m = 6, 3 <= b <= 7): one CTA per output block, walked in B slabs of
+// fixed mode-1 index i0.  Every term's second factor (the modes NOT holding
+// mode 1: central moment / cumulant of the complement) is the same for all
+// slabs, so it is staged in shared memory ONCE per block; the first factor's
+// slice at i0 (a contiguous run: mode 1 is its leading mode) is staged per
+// slab, double-buffered by cp.async while the previous slab is evaluated.  All
+// factor reads are then LDS (v2 reads them through L1 at ~3 wavefronts per
+// request and re-fetches them from L2: 50 GB of L2->L1 traffic per 20 GB of
+// M_6 at cfg5).  Within a slab (modes 2..6): modes 2, 3 in registers (B^2
+// rows), modes 4..6 across threads (B^3, coalesced M_m / C_m rows).
+template <int B>
+struct Slab6 {
+  static constexpr int M = 6;
+  static constexpr int NT = rf::term_count(M);
+  static constexpr int CT = 3;                    // thread modes of the 5-mode slab
+  static constexpr int ROWS = B * B;
+  static constexpr int W = B * B * B;
+  static constexpr int NTH = (W + 31) / 32 * 32;
+  static constexpr int SLAB = B * B * B * B * B;  // elements per slab
+  // second factors (no mode 1), all terms: offset of term T
+  __host__ __device__ static constexpr int ov(int T) {
+    int o = 0;
+    for (int t = 0; t < T; ++t) o += rf::ipow(B, M - rf::popc(rf::term_mask(M, t)));
+    return o;
+  }
+  // first-factor slices (mode 1 fixed): offset of term T
+  __host__ __device__ static constexpr int ou(int T) {
+    int o = 0;
+    for (int t = 0; t < T; ++t) o += rf::ipow(B, rf::popc(rf::term_mask(M, t)) - 1);
+    return o;
+  }
+  static constexpr int SEGV = ov(NT), SEGU = (ou(NT) + 1) / 2 * 2;
+  // slabs evaluated concurrently (thread groups): two where the CTA stays <= 1024
+  // threads and the stages fit
+  static constexpr int G = (2 * NTH <= 1024 && (SEGV + 4 * SEGU) * 8 <= 200 * 1024) ? 2 : 1;
+  static constexpr size_t SMEM = (size_t)(SEGV + 2 * G * SEGU) * 8;
+  static constexpr bool ok = B >= 3 && B <= 7 && SMEM <= 200 * 1024;
+};
+
+template <int B, int T>
+__device__ __forceinline__ void slab6_stage_v(double *sv, const RecFactArgs &a, const int32_t *toff, int tid) {
+  using SL = Slab6<B>;
+  constexpr int S = rf::term_mask(6, T);
+  constexpr int r = 6 - rf::popc(S);
+  constexpr int L = rf::ipow(B, r);
+  const double *src = (r <= 3 ? a.cum[r] : a.cmom[r]) + __ldg(toff + 2 * T + 1);
+  for (int i = tid; i < L; i += SL::NTH) cp_async8(sv + std::integral_constant<int, SL::ov(T)>::value + i, src + i);
+}
+template <int B, int T>
+__device__ __forceinline__ void slab6_stage_u(double *su, const RecFactArgs &a, const int32_t *toff, int i0, int tid) {
+  using SL = Slab6<B>;
+  constexpr int S = rf::term_mask(6, T);
+  constexpr int s = rf::popc(S);
+  constexpr int L = rf::ipow(B, s - 1);  // the slice of the C_s block at mode-1 index i0
+  const double *src = a.cum[s] + __ldg(toff + 2 * T) + i0 * L;
+  for (int i = tid; i < L; i += SL::NTH) cp_async8(su + std::integral_constant<int, SL::ou(T)>::value + i, src + i);
+}
+template <int B, int... Ts>
+__device__ __forceinline__ void slab6_stage_v_all(double *sv, const RecFactArgs &a, const int32_t *toff, int tid,
+                                                  std::integer_sequence<int, Ts...>) {
+  (slab6_stage_v<B, Ts>(sv, a, toff, tid), ...);
+}
+template <int B, int... Ts>
+__device__ __forceinline__ void slab6_stage_u_all(double *su, const RecFactArgs &a, const int32_t *toff, int i0,
+                                                  int tid, std::integer_sequence<int, Ts...>) {
+  (slab6_stage_u<B, Ts>(su, a, toff, i0, tid), ...);
+}
+
+// term T on a slab: the 5-mode problem over original modes 1..5 (bit q of a
+// slab mask = original mode q+1), u over A = S \ {0}, v over the rest
+template <int B, int T>
+__device__ __forceinline__ void slab6_term(double (&acc)[Slab6<B>::ROWS], const int (&dig)[5], const double *su,
+                                           const double *sv) {
+  using SL = Slab6<B>;
+  constexpr int S = rf::term_mask(6, T);
+  constexpr int A = S >> 1;                   // slab modes of the first factor
+  constexpr int R = (((1 << 6) - 1) & ~S) >> 1;  // slab modes of the second factor
+  int o1 = 0, o2 = 0;
+#pragma unroll
+  for (int q = 5 - SL::CT; q < 5; ++q) {
+    if (A & (1 << q)) o1 += dig[q] * rf::stride_in(A, q, B);
+    if (R & (1 << q)) o2 += dig[q] * rf::stride_in(R, q, B);
+  }
+  rows_fma<5, B, SL::CT, A, false, false>(acc, su + std::integral_constant<int, SL::ou(T)>::value + o1,
+                                          sv + std::integral_constant<int, SL::ov(T)>::value + o2,
+                                          std::make_integer_sequence<int, SL::ROWS>{});
+}
+template <int B, int... Ts>
+__device__ __forceinline__ void slab6_terms(double (&acc)[Slab6<B>::ROWS], const int (&dig)[5], const double *su,
+                                            const double *sv, std::integer_sequence<int, Ts...>) {
+  (slab6_term<B, Ts>(acc, dig, su, sv), ...);
+}
+
+// G slabs are evaluated at once by G thread groups sharing the staged second
+// factors (1 CTA/SM: 14 warps at b = 6 instead of 7).
+template <int B>
+__global__ void __launch_bounds__(Slab6<B>::NTH * Slab6<B>::G) k_recursion_slab6(RecFactArgs a) {
+  using SL = Slab6<B>;
+  constexpr int G = SL::G;
+  extern __shared__ __align__(16) unsigned char rf_smem[];
+  double *sv = reinterpret_cast<double *>(rf_smem);
+  double *su = sv + SL::SEGV;  // [2 stages][G groups][SEGU]
+  const int tid = threadIdx.x % SL::NTH, grp = threadIdx.x / SL::NTH;
+  const int64_t kb = blockIdx.x;
+  const int32_t *toff = a.term_off + kb * 2 * SL::NT;
+  slab6_stage_v_all<B>(sv, a, toff, tid + grp * SL::NTH, std::make_integer_sequence<int, SL::NT>{});
+  if (grp < B) slab6_stage_u_all<B>(su + grp * SL::SEGU, a, toff, grp, tid, std::make_integer_sequence<int, SL::NT>{});
+  cp_async_commit();
+  const bool active = tid < SL::W;
+  const int c = active ? tid : 0;
+  int dig[5];
+  dig[0] = dig[1] = 0;
+  dig[2] = c / (B * B);
+  dig[3] = (c / B) % B;
+  dig[4] = c % B;
+  double *blk = a.mk + __ldg(a.blk_off + kb) + c;
+  constexpr int ROUNDS = (B + G - 1) / G;
+#pragma unroll 1
+  for (int rd = 0; rd < ROUNDS; ++rd) {
+    const int i0 = rd * G + grp;
+    const int nx = i0 + G;  // this group's slab of the next round
+    if (nx < B)
+      slab6_stage_u_all<B>(su + (((rd + 1) & 1) * G + grp) * SL::SEGU, a, toff, nx, tid,
+                           std::make_integer_sequence<int, SL::NT>{});
+    cp_async_commit();
+    const bool live = active && i0 < B;
+    double acc[SL::ROWS];
+    double *row = blk + (int64_t)i0 * SL::SLAB;
+    if (live) {
+#pragma unroll
+      for (int r = 0; r < SL::ROWS; ++r) acc[r] = row[r * SL::W];
+    }
+    cp_async_wait<1>();  // V and this round's U slices have landed (this thread's copies)
+    __syncthreads();     // ... everyone's
+    if (live) {
+      slab6_terms<B>(acc, dig, su + ((rd & 1) * G + grp) * SL::SEGU, sv, std::make_integer_sequence<int, SL::NT>{});
+#pragma unroll
+      for (int r = 0; r < SL::ROWS; ++r) row[r * SL::W] = acc[r];
+    }
+    __syncthreads();  // this round's U buffers are restaged two rounds on
+  }
+}
+
 // trailing (thread) modes: the fewest that leave <= kRfRows register rows
 #ifndef BCG_RF_ROWS
 #define BCG_RF_ROWS 32
@@ -802,6 +945,23 @@ cudaError_t go_fact(const RecFactArgs &a, cudaStream_t stream) {
       }
       const int64_t grid = std::min<int64_t>(a.nkeys, grid_cap);
       k_recursion_pipe<M, B><<<(unsigned)grid, P::NTH, P::SMEM, stream>>>(a);
+      g_launches++;
+      return cudaGetLastError();
+    }
+  }
+  if constexpr (M == 6 && Slab6<B>::ok) {
+    static const bool slab = getenv("BCG_RF_SLAB") ? atoi(getenv("BCG_RF_SLAB")) > 0 : false;  // A/B knob
+    if ((slab && variant == 0) || variant == 6) {
+      if (a.nkeys <= 0) return cudaSuccess;
+      using SL = Slab6<B>;
+      static bool attr = false;
+      if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_recursion_slab6<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)SL::SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+      }
+      k_recursion_slab6<B><<<(unsigned)a.nkeys, SL::NTH * SL::G, SL::SMEM, stream>>>(a);
       g_launches++;
       return cudaGetLastError();
     }

@@ -459,14 +459,15 @@ def test_block_split_path_over_nccl_single_rank_bitwise(tmp_path, rng):
         np.testing.assert_array_equal(got[f"c{k}"], cs[k].packed_host())
 
 
-_VARIANT_SHAPES = [(16, 4, 8, 300), (12, 5, 4, 400), (9, 6, 3, 300), (12, 6, 6, 200), (12, 5, 6, 300), (7, 6, 3, 250)]
+_VARIANT_SHAPES = [(16, 4, 8, 300), (12, 5, 4, 400), (9, 6, 3, 300), (12, 6, 6, 200), (12, 5, 6, 300), (7, 6, 3, 250),
+                   (10, 6, 5, 150), (8, 6, 4, 200)]
 
 
 @pytest.mark.parametrize("env", [{"BCG_RF_VARIANT": "2", "BCG_RF_TILE": "-1"}, {"BCG_RF_VARIANT": "2", "BCG_RF_TILE": "0"},
                                  {"BCG_RF_VARIANT": "2", "BCG_RF_RES": "0"}, {"BCG_RF_VARIANT": "2", "BCG_RF_RES": "1"},
                                  {"BCG_RF_VARIANT": "2", "BCG_RF_RES": "3"},
                                  {"BCG_RF_VARIANT": "2", "BCG_RF_TILE": "1"}, {"BCG_RF_VARIANT": "3"},
-                                 {"BCG_RF_VARIANT": "4"}, {"BCG_RF_VARIANT": "2", "BCG_RF_PIPE": "1"},
+                                 {"BCG_RF_VARIANT": "4"}, {"BCG_RF_VARIANT": "6"}, {"BCG_RF_VARIANT": "2", "BCG_RF_PIPE": "1"},
                                  {"BCG_RF_VARIANT": "2", "BCG_RF_PIPE": "1", "BCG_RF_TILE": "-1"}, {}])
 def test_recursion_variants_match_oracle(env, tmp_path):
     """Every factored-recursion kernel variant (the knobs are read once per
