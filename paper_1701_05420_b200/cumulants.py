@@ -8,6 +8,8 @@ packed M_m buffer; nothing leaves HBM until the caller asks for blocks.
 
 from __future__ import annotations
 
+import os
+
 import ctypes
 from typing import Sequence
 
@@ -183,6 +185,8 @@ def cumulants_device(X, m_max: int, b: int, c1_host: bool = True, timer: dict | 
         xt = _center_transposed(X, st["mean"])
         sums, sq = _rowstats(xt, t)
         _check_centered_stats(sums, sq, t)
+        if timer is None and m_max >= 3 and not _SERIAL_ORDERS:
+            return (st["mean"].cpu().numpy() if c1_host else st["mean"]), _orders_concurrent(xt, t, m_max, b)
         central: dict = {}  # central moments M_4.. kept for the factored recursion
         for k in range(2, m_max + 1):
             if timer is not None and k == m_max:
@@ -199,6 +203,52 @@ def cumulants_device(X, m_max: int, b: int, c1_host: bool = True, timer: dict | 
             tensors.append(Mk)
     c1 = st["mean"].cpu().numpy() if c1_host else st["mean"]
     return c1, tensors
+
+
+# BCG_SERIAL_ORDERS=1: one order after the other on the current stream (A/B knob)
+_SERIAL_ORDERS = os.environ.get("BCG_SERIAL_ORDERS", "0") not in ("", "0")
+_side_streams: dict = {}
+
+
+def _orders_concurrent(xt, t: int, m_max: int, b: int) -> list:
+    """The per-order moment GEMMs only read xt, so orders 2..m-1 are issued
+    on side streams and the top order on the current one: the GPU overlaps
+    the small GEMMs with the big one (no per-GEMM wave tails, no idle SMs
+    while a thin staircase drains).  The recursions then run in order on the
+    current stream.  Every kernel is deterministic, so the results are
+    bitwise those of the serial schedule."""
+    torch = _native.torch_cuda()
+    main = torch.cuda.current_stream()
+    dev = xt.device.index if xt.device.index is not None else torch.cuda.current_device()
+    ready = torch.cuda.Event()
+    ready.record(main)
+    moments: dict = {}
+    done: dict = {}
+    for k in range(2, m_max):
+        key = (dev, k)
+        if key not in _side_streams:
+            _side_streams[key] = torch.cuda.Stream(device=dev)
+        side = _side_streams[key]
+        side.wait_event(ready)
+        with torch.cuda.stream(side):
+            moments[k] = _moment_device_t(xt, t, k, b)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        moments[k].data.record_stream(main)
+        done[k] = ev
+    moments[m_max] = _moment_device_t(xt, t, m_max, b)
+    tensors: list[BlockSymTensor] = []
+    central: dict = {}
+    for k in range(2, m_max + 1):
+        if k in done:
+            main.wait_event(done[k])
+        Mk = moments[k]
+        if 4 <= k <= m_max - 2:
+            central[k] = Mk.data.clone()
+        if k >= 4:
+            _recursion_inplace(Mk, tensors, central)
+        tensors.append(Mk)
+    return tensors
 
 
 def cumulants_upto(x, m_max: int, b: int = 2, engine: str = "auto") -> CumulantSet:

@@ -181,13 +181,22 @@ def cumulants_upto_sharded(x_local, m_max: int, b: int = 2, group=None, ops=None
         _check_centered(both[:n], both[n:], t_total)
         lower: dict = {}
         central: dict = {}  # central moments M_4..M_{m-2} (factored recursion)
+        # all moment GEMMs only read Xc: issue them up front (lower orders on
+        # side streams), so each order's collective overlaps the GEMMs still
+        # running -- the top order's in particular
+        early = _issue_moments(ops, Xc, m_max, b) if timer is None else {}
         for k in range(2, m_max + 1):
             top = k == m_max and timer is not None
             if top:
                 ev0 = torch.cuda.Event(enable_timing=True)
                 ev1 = torch.cuda.Event(enable_timing=True)
                 ev0.record()
-            mk = ops.moment_raw(Xc, k, b)
+            if k in early:
+                mk, ev = early[k]
+                if ev is not None:
+                    torch.cuda.current_stream().wait_event(ev)
+            else:
+                mk = ops.moment_raw(Xc, k, b)
             if top:
                 ev1.record()
                 timer.setdefault("moment_top", []).append((ev0, ev1))
@@ -267,6 +276,35 @@ def cumulants_upto_block_split(x_full, m_max: int, b: int = 2, group=None, ops=N
             lower[k] = mk
             tensors.append(mk)
     return mean, tensors
+
+
+def _issue_moments(ops, centered, m_max: int, b: int) -> dict:
+    """Orders 2..m-1 on per-order side streams, the top order on the current
+    stream; returns {k: (raw sums, event or None)}.  CUDA ops only (the CPU
+    test ops run serially); BCG_SERIAL_ORDERS=1 disables it."""
+    from .cumulants import _SERIAL_ORDERS, _side_streams
+
+    if not isinstance(ops, CudaOps) or m_max < 3 or _SERIAL_ORDERS:
+        return {}
+    main = torch.cuda.current_stream()
+    dev = centered[0].device.index if centered[0].device.index is not None else torch.cuda.current_device()
+    ready = torch.cuda.Event()
+    ready.record(main)
+    out: dict = {}
+    for k in range(2, m_max):
+        key = (dev, k)
+        if key not in _side_streams:
+            _side_streams[key] = torch.cuda.Stream(device=dev)
+        side = _side_streams[key]
+        side.wait_event(ready)
+        with torch.cuda.stream(side):
+            mk = ops.moment_raw(centered, k, b)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        mk.record_stream(main)
+        out[k] = (mk, ev)
+    out[m_max] = (ops.moment_raw(centered, m_max, b), None)
+    return out
 
 
 def _device_div(v, t, ops):

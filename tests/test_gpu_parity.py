@@ -496,3 +496,26 @@ def test_recursion_variants_match_oracle(env, tmp_path):
         _, want = orc.cumulants_upto(x, m, b)
         for k in range(2, m + 1):
             np.testing.assert_allclose(got[f"{i}_{k}"], want[k], rtol=1e-9, atol=1e-12, err_msg=f"{env} shape {i} k={k}")
+
+
+def test_concurrent_order_schedule_is_bitwise_serial(tmp_path):
+    """cumulants_upto issues the per-order GEMMs on side streams; the result is
+    bitwise that of the serial schedule (BCG_SERIAL_ORDERS=1, own process)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    x = np.random.default_rng(3).exponential(1.0, (50_000, 11))
+    np.save(tmp_path / "x.npy", x)
+    code = ("import sys, numpy as np; sys.path.insert(0, %r)\n"
+            "import paper_1701_05420_b200 as bcg\n"
+            "cs = bcg.cumulants_upto(np.load(%r), 6, b=3)\n"
+            "np.savez(%r, **{f'c{k}': cs[k].packed_host() for k in range(2, 7)})\n"
+            % (root, str(tmp_path / "x.npy"), str(tmp_path / "serial.npz")))
+    subprocess.run([sys.executable, "-c", code], check=True, env={**os.environ, "BCG_SERIAL_ORDERS": "1"},
+                   timeout=600)
+    serial = np.load(tmp_path / "serial.npz")
+    cs = bcg.cumulants_upto(x, 6, b=3)
+    for k in range(2, 7):
+        np.testing.assert_array_equal(cs[k].packed_host(), serial[f"c{k}"])
