@@ -579,7 +579,6 @@ static int recursion_dispatch(const bcg_plan *plan, double *mk, const double *co
   a.term_off = p.d_term_off;
   for (int k = 2; k <= m - 2; ++k) {
     a.cum[k] = lower[k - 2];
-    a.cum_len[k] = p.lay[k].offs.back();
     if (k >= 4) a.cmom[k] = cmom[k - 2];
   }
   a.mk = mk;

@@ -89,7 +89,6 @@ struct RecFactArgs {
   const int32_t *term_off;  // [nkeys][nterms][2] element offsets of each term's factor blocks
   const double *cum[16];    // packed C_k, k = 2 .. m-2
   const double *cmom[16];   // packed central moments M_k, k = 4 .. m-2
-  int64_t cum_len[16];      // stored elements of C_k (shared-memory residency of C_2, C_3)
   double *mk;               // in: M_m, out: C_m
 };
 int recursion_fact_terms(int m);

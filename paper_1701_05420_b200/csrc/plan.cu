@@ -144,12 +144,6 @@ static int64_t build_tiles(const Plan &p, const Gemm &g, int tm, int tn, std::ve
   return ntiles;
 }
 
-static int64_t gemm_useful(const Gemm &g) {
-  int64_t u = 0;
-  for (int64_t r = 0; r < g.R; ++r) u += g.C - g.row_cstart[r];
-  return u;
-}
-
 // Modeled cost (in useful-FMA units) of running GEMM g with a tm x tn tile:
 // tiled area x (1 + 10 * Khatri-Rao products per FMA).  The weight of a KR
 // product (~10 FMA-equivalents: its X loads, DMULs on the shared FP64 pipe,

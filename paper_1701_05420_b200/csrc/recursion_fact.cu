@@ -124,9 +124,9 @@ __device__ __forceinline__ void rows_fma(double *acc, const double *f1, const do
 // broadcast or contiguous across the warp), each thread keeps its ROWS
 // elements in registers, and the row offsets into every factor are
 // compile-time immediates.
-template <int M, int B, int CT, int RES, int T>
+template <int M, int B, int CT, int T>
 __device__ __forceinline__ void apply_term(double (&acc)[rf::ipow(B, M - CT)], const int (&dig)[M],
-                                           const RecFactArgs &a, const int32_t *toff, const double *const *res) {
+                                           const RecFactArgs &a, const int32_t *toff) {
   constexpr int S = rf::term_mask(M, T);
   constexpr int FULL = (1 << M) - 1;
   constexpr int REST = FULL & ~S;
@@ -139,99 +139,49 @@ __device__ __forceinline__ void apply_term(double (&acc)[rf::ipow(B, M - CT)], c
     if (S & (1 << q)) o1 += dig[q] * rf::stride_in(S, q, B);
     if (REST & (1 << q)) o2 += dig[q] * rf::stride_in(REST, q, B);
   }
-  // RES bit (k - 2): C_k resident in shared memory (k = 2, 3)
-  constexpr bool R1 = s <= 3 && ((RES >> (s - 2)) & 1);
-  constexpr bool R2 = r <= 3 && ((RES >> (r - 2)) & 1);
-  const double *f1 = (R1 ? res[s - 2] : a.cum[s]) + toff[2 * T] + o1;
-  const double *f2 = (R2 ? res[r - 2] : (r <= 3 ? a.cum[r] : a.cmom[r])) + toff[2 * T + 1] + o2;
-  rows_fma<M, B, CT, S, !R1, !R2>(acc, f1, f2, std::make_integer_sequence<int, ROWS>{});
+  const double *f1 = a.cum[s] + toff[2 * T] + o1;
+  const double *f2 = (r <= 3 ? a.cum[r] : a.cmom[r]) + toff[2 * T + 1] + o2;
+  rows_fma<M, B, CT, S, true, true>(acc, f1, f2, std::make_integer_sequence<int, ROWS>{});
 }
 
-template <int M, int B, int CT, int RES, int... Ts>
+template <int M, int B, int CT, int... Ts>
 __device__ __forceinline__ void apply_terms(double (&acc)[rf::ipow(B, M - CT)], const int (&dig)[M],
-                                            const RecFactArgs &a, const int32_t *toff, const double *const *res,
+                                            const RecFactArgs &a, const int32_t *toff,
                                             std::integer_sequence<int, Ts...>) {
-  (apply_term<M, B, CT, RES, Ts>(acc, dig, a, toff, res), ...);
+  (apply_term<M, B, CT, Ts>(acc, dig, a, toff), ...);
 }
 
 constexpr int kRfThreads = 128;
-constexpr int kRfThreadsRes = 512;  // one CTA per SM when C_2 (and C_3) are resident
 
-template <int M, int B, int CT, int RES>
-struct FactCfg {
-  static constexpr int NTHR = RES ? kRfThreadsRes : kRfThreads;
-  static constexpr int MINB = RES ? 1 : (rf::ipow(B, M - CT) > 32 ? 3 : 4);
-  static constexpr int NT = rf::term_count(M);
-  static constexpr int W = rf::ipow(B, CT);
-  static constexpr int NGRP = NTHR / kRfThreads;  // independent 128-thread groups per CTA
-  static constexpr int KPC = (kRfThreads + W - 1) / W + 1;  // max output blocks per group step
-  static constexpr int TOFF_GRP = (KPC * 2 * NT + 3) / 4 * 4;  // int32 per group
-  static constexpr int TOFF_BYTES = NGRP * TOFF_GRP * 4;
-};
-
-// barrier over the 128 threads of group g only (named barrier 1 + g)
-__device__ __forceinline__ void group_sync(int g) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(1 + g), "r"(kRfThreads) : "memory");
-}
-
-// RES = 0: v2 as measured in round 1 (128 threads, factors through L1).
-// RES = 1 / 3: the same evaluation with C_2 / C_2 and C_3 copied whole into
-// shared memory first (persistent CTAs, 512 threads = 4 independent
-// 128-thread groups synchronised by named barriers, so their M_m loads stay
-// out of phase): those factor reads become LDS (short latency, ~1 wavefront
-// per warp access instead of ~3 for the scattered 8-byte global reads), only
-// C_4 / M_4 factors still go through L1.
-template <int M, int B, int CT, int RES>
-__global__ void __launch_bounds__(FactCfg<M, B, CT, RES>::NTHR, FactCfg<M, B, CT, RES>::MINB)
-    k_recursion_fact(RecFactArgs a) {
-  using FC = FactCfg<M, B, CT, RES>;
-  constexpr int kThr = FC::NTHR;
+template <int M, int B, int CT>
+__global__ void __launch_bounds__(kRfThreads, (rf::ipow(B, M - CT) > 32 ? 3 : 4)) k_recursion_fact(RecFactArgs a) {
   constexpr int NT = rf::term_count(M);
   constexpr int ROWS = rf::ipow(B, M - CT);  // elements per thread (registers)
   constexpr int W = rf::ipow(B, CT);         // threads per block
-  constexpr int KPC = FC::KPC;
-  extern __shared__ __align__(16) unsigned char rf_smem[];
-  const int grp = threadIdx.x / kRfThreads, gtid = threadIdx.x % kRfThreads;
-  int32_t *s_toff = reinterpret_cast<int32_t *>(rf_smem) + grp * FC::TOFF_GRP;
-  const double *res[2] = {nullptr, nullptr};
-  if constexpr (RES != 0) {
-    double *dst = reinterpret_cast<double *>(rf_smem + FC::TOFF_BYTES);
-#pragma unroll
-    for (int k = 2; k <= 3; ++k) {
-      if ((RES >> (k - 2)) & 1) {
-        const double *src = a.cum[k];
-        for (int64_t i = threadIdx.x; i < a.cum_len[k]; i += kThr) dst[i] = __ldg(src + i);
-        res[k - 2] = dst;
-        dst += a.cum_len[k];
-      }
-    }
-  }
-  if constexpr (RES != 0) __syncthreads();  // resident tensors staged
-  // each group walks a contiguous run of steps (128 items each): consecutive
-  // output blocks share most factor blocks, which then stay in this SM's L1
-  // 32-bit item space: the host launches at most 2^31 items at a time
+  constexpr int KPC = (kRfThreads + W - 1) / W + 1;  // max output blocks per step
+  __shared__ int32_t s_toff[KPC * 2 * NT];
+  // each CTA walks a contiguous run of steps (128 items each): consecutive
+  // output blocks share most factor blocks, which then stay in this SM's L1.
+  // 32-bit item space: the host launches at most 2^31 items at a time.
   const uint32_t nsteps = (uint32_t)((a.nkeys * W + kRfThreads - 1) / kRfThreads);
-  const uint32_t ngroups = gridDim.x * FC::NGRP;
-  const uint32_t gg = blockIdx.x * FC::NGRP + grp;
-  const uint32_t s_begin = (uint32_t)((uint64_t)nsteps * gg / ngroups);
-  const uint32_t s_end = (uint32_t)((uint64_t)nsteps * (gg + 1) / ngroups);
+  const uint32_t s_begin = (uint32_t)((uint64_t)nsteps * blockIdx.x / gridDim.x);
+  const uint32_t s_end = (uint32_t)((uint64_t)nsteps * (blockIdx.x + 1) / gridDim.x);
   for (uint32_t step = s_begin; step < s_end; ++step) {
     const uint32_t item0 = step * kRfThreads;
     const uint32_t kb0 = item0 / W;
-    group_sync(grp);  // previous step done with s_toff
-    // stage the term-offset tables of this step's output blocks (coalesced),
-    // so every factor address below is a shared-memory read away
-    // (one contiguous run of the block-ordered table: coalesced, no indirection)
+    __syncthreads();  // previous step done with s_toff
+    // stage the term-offset rows of this step's output blocks: one contiguous
+    // run of the work-list-ordered table (coalesced, no key indirection), so
+    // every factor address below is a shared-memory read away
     {
       const int32_t *src = a.term_off + (int64_t)kb0 * 2 * NT;
       const int64_t left = (a.nkeys - (int64_t)kb0) * 2 * NT;
       const int lim = left < KPC * 2 * NT ? (int)left : KPC * 2 * NT;
-      for (int i = gtid; i < lim; i += kRfThreads) s_toff[i] = __ldg(src + i);
+      for (int i = threadIdx.x; i < lim; i += kRfThreads) s_toff[i] = __ldg(src + i);
     }
-    group_sync(grp);
-    // 32-bit item arithmetic within the step (the host keeps nkeys * W < 2^31)
-    const int rel = (int)(item0 - kb0 * W) + gtid;  // item offset from block kb0's first item
-    const int kbr = rel / W;                           // W is a compile-time constant
+    __syncthreads();
+    const int rel = (int)(item0 - kb0 * W) + threadIdx.x;  // item offset from block kb0's first item
+    const int kbr = rel / W;                                  // W is a compile-time constant
     const int64_t kb = (int64_t)kb0 + kbr;
     if (kb >= a.nkeys) continue;
     const int c = rel - kbr * W;
@@ -251,124 +201,9 @@ __global__ void __launch_bounds__(FactCfg<M, B, CT, RES>::NTHR, FactCfg<M, B, CT
     double acc[ROWS];
 #pragma unroll
     for (int row = 0; row < ROWS; ++row) acc[row] = blk[(int64_t)row * W];
-    apply_terms<M, B, CT, RES>(acc, dig, a, toff, res, std::make_integer_sequence<int, NT>{});
+    apply_terms<M, B, CT>(acc, dig, a, toff, std::make_integer_sequence<int, NT>{});
 #pragma unroll
     for (int row = 0; row < ROWS; ++row) blk[(int64_t)row * W] = acc[row];
-  }
-}
-
-// v5: v2's evaluation in persistent CTAs whose 128-thread groups walk a
-// contiguous run of steps with a one-step software pipeline: while step s is
-// evaluated, cp.async (LDGSTS) is already streaming step s+1's M_m rows into
-// a thread-private shared-memory column and step s+1's term-offset rows into
-// the other half of a double buffer, so the HBM latency of M_m no longer sits
-// in front of every step (v2 is long-scoreboard bound at ~25% occupancy).
-template <int M, int B, int CT, int... Ts>
-__device__ __forceinline__ void apply_terms_from1(double (&acc)[rf::ipow(B, M - CT)], const int (&dig)[M],
-                                                  const RecFactArgs &a, const int32_t *toff,
-                                                  std::integer_sequence<int, Ts...>) {
-  (apply_term<M, B, CT, 0, Ts + 1>(acc, dig, a, toff, nullptr), ...);
-}
-
-template <int M, int B, int CT>
-struct PipeCfg {
-  static constexpr int NT = rf::term_count(M);
-  static constexpr int ROWS = rf::ipow(B, M - CT);
-  static constexpr int W = rf::ipow(B, CT);
-  static constexpr int KPC = (kRfThreads + W - 1) / W + 1;
-  static constexpr int TOFF = (KPC * 2 * NT + 3) / 4 * 4;  // int32 per buffer
-  static constexpr size_t SMEM = (size_t)2 * TOFF * 4 + (size_t)ROWS * kRfThreads * 8;
-};
-
-template <int M, int B, int CT>
-__global__ void __launch_bounds__(kRfThreads, (rf::ipow(B, M - CT) > 32 ? 2 : 3)) k_recursion_fact_pipe(RecFactArgs a) {
-  using PC = PipeCfg<M, B, CT>;
-  constexpr int NT = PC::NT, ROWS = PC::ROWS, W = PC::W, KPC = PC::KPC;
-  extern __shared__ __align__(16) unsigned char rf_smem[];
-  int32_t *s_toff = reinterpret_cast<int32_t *>(rf_smem);                 // [2][TOFF]
-  double *s_m = reinterpret_cast<double *>(rf_smem + 2 * PC::TOFF * 4);   // [ROWS][128]
-  const int tid = threadIdx.x;
-  const uint32_t nsteps = (uint32_t)((a.nkeys * W + kRfThreads - 1) / kRfThreads);
-  const uint32_t s_begin = (uint32_t)((uint64_t)nsteps * blockIdx.x / gridDim.x);
-  const uint32_t s_end = (uint32_t)((uint64_t)nsteps * (blockIdx.x + 1) / gridDim.x);
-  if (s_begin >= s_end) return;
-  auto stage_toff = [&](uint32_t step, int buf) {
-    const uint32_t kb0 = step * kRfThreads / W;
-    const int32_t *src = a.term_off + (int64_t)kb0 * 2 * NT;
-    const int64_t left = (a.nkeys - (int64_t)kb0) * 2 * NT;
-    const int lim = left < KPC * 2 * NT ? (int)left : KPC * 2 * NT;
-    for (int i = tid; i < lim; i += kRfThreads) cp_async4(s_toff + buf * PC::TOFF + i, src + i);
-  };
-  // item of this thread in step s: (block kb, column c); kb >= nkeys: idle
-  auto item_of = [&](uint32_t step, int64_t &kb, int &c) {
-    const uint32_t item = step * kRfThreads + tid;
-    const uint32_t k = item / W;
-    kb = k;
-    c = (int)(item - k * W);
-  };
-  auto stage_m = [&](int64_t kb, int c) {
-    if (kb < a.nkeys) {
-      const double *src = a.mk + __ldg(a.blk_off + kb) + c;
-#pragma unroll
-      for (int row = 0; row < ROWS; ++row) cp_async8(s_m + row * kRfThreads + tid, src + (int64_t)row * W);
-    }
-  };
-  // prologue: offsets of the first step, then its M_m rows
-  stage_toff(s_begin, 0);
-  cp_async_commit();
-  {
-    int64_t kb;
-    int c;
-    item_of(s_begin, kb, c);
-    stage_m(kb, c);
-  }
-  cp_async_commit();
-  cp_async_wait<1>();  // offsets of the first step
-  __syncthreads();
-  for (uint32_t step = s_begin; step < s_end; ++step) {
-    const int buf = (step - s_begin) & 1;
-    const bool more = step + 1 < s_end;
-    if (more) stage_toff(step + 1, buf ^ 1);
-    cp_async_commit();
-    int64_t kb;
-    int c;
-    item_of(step, kb, c);
-    int64_t kb_n = a.nkeys;
-    int c_n = 0;
-    if (more) item_of(step + 1, kb_n, c_n);
-    const bool active = kb < a.nkeys;
-    int64_t boff = 0;
-    if (active) boff = __ldg(a.blk_off + kb);
-    cp_async_wait<1>();  // this step's M_m rows (the group before the offsets just issued)
-    double acc[ROWS];
-    int dig[M];
-    const int32_t *toff = s_toff + buf * PC::TOFF + (int)(kb - (int64_t)(step * kRfThreads / W)) * 2 * NT;
-    if (active) {
-#pragma unroll
-      for (int q = 0; q < M; ++q) dig[q] = 0;
-      {
-        int rem = c;
-#pragma unroll
-        for (int q = M - 1; q >= M - CT; --q) {
-          dig[q] = rem % B;
-          rem /= B;
-        }
-      }
-#pragma unroll
-      for (int row = 0; row < ROWS; ++row) acc[row] = s_m[row * kRfThreads + tid];
-      apply_term<M, B, CT, 0, 0>(acc, dig, a, toff, nullptr);  // consumes every acc: the LDS are done
-    }
-    // the column is free again: stream the next step's rows into it
-    if (more) stage_m(kb_n, c_n);
-    cp_async_commit();
-    if (active) {
-      apply_terms_from1<M, B, CT>(acc, dig, a, toff, std::make_integer_sequence<int, NT - 1>{});
-      double *blk = a.mk + boff + c;
-#pragma unroll
-      for (int row = 0; row < ROWS; ++row) blk[(int64_t)row * W] = acc[row];
-    }
-    cp_async_wait<1>();  // next step's offsets (older than its M_m rows)
-    __syncthreads();     // ... visible to all; everyone done with this step's offsets
   }
 }
 
@@ -636,164 +471,6 @@ __global__ void __launch_bounds__(Staged<M, B>::NTH) k_recursion_staged(RecFactA
   }
 }
 
-// ---------------------------------------------------------------------------
-// v4: persistent, software-pipelined.  Each CTA walks a contiguous run of
-// output blocks; while it evaluates block i from shared memory, cp.async (8-byte
-// LDGSTS, L1-allocating) is already staging block i+1's M_m block and every
-// factor sub-block it needs, and block i+2's term-offset row.  The HBM stream
-// of M_m and the L2 reads of the factors thus overlap the arithmetic instead of
-// sitting in front of it (v2/v3 are latency-bound: long-scoreboard stalls at
-// 25% occupancy).  The result goes straight from registers to global memory
-// (coalesced).  Register tile: the leading R modes (<= 64 rows), threads over
-// the trailing modes (<= 64 columns).
-namespace rf {
-__host__ __device__ constexpr int r_pipe(int M, int B) {
-  int r = 0;
-  while (r < M && ipow(B, M - r) > 64) ++r;
-  return r;
-}
-}  // namespace rf
-
-#ifndef BCG_RF_STAGES
-#define BCG_RF_STAGES 2
-#endif
-
-template <int M, int B>
-struct Pipe {
-  static constexpr int NT = rf::term_count(M);
-  static constexpr int R = rf::r_pipe(M, B);
-  static constexpr int CT = M - R;
-  static constexpr int W = rf::ipow(B, CT);
-  static constexpr int ROWS = rf::ipow(B, R);
-  static constexpr int NTH = (W + 31) / 32 * 32;
-  static constexpr int SEG = rf::seg_before(M, B, NT);
-  static constexpr int BLK = rf::ipow(B, M);
-  static constexpr int STAGE = (SEG + BLK + 1) / 2 * 2;  // doubles per stage
-  static constexpr int STAGES = BCG_RF_STAGES;
-  static constexpr int TSLOTS = 2 * STAGES - 1;         // term-offset rows in flight
-  static constexpr int TROW = 2 * NT + 2;               // int32 per row: term offsets, offs[key] (int64)
-  static constexpr int TROW_P = (TROW + 3) / 4 * 4;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE * 8 + (size_t)TSLOTS * TROW_P * 4;
-  static constexpr bool ok = ROWS <= 64 && SMEM <= 160 * 1024;
-};
-
-
-template <int M, int B, int T>
-__device__ __forceinline__ void pipe_stage_term(double *st, const RecFactArgs &a, const int32_t *trow, int tid) {
-  constexpr int S = rf::term_mask(M, T);
-  constexpr int s = rf::popc(S), r = M - s;
-  constexpr int L1 = rf::ipow(B, s), L2 = rf::ipow(B, r);
-  constexpr int O1 = rf::seg_before(M, B, T), O2 = O1 + L1;
-  constexpr int NTH = Pipe<M, B>::NTH;
-  const double *src1 = a.cum[s] + trow[2 * T];
-  const double *src2 = (r <= 3 ? a.cum[r] : a.cmom[r]) + trow[2 * T + 1];
-#pragma unroll
-  for (int i = tid; i < L1; i += NTH) cp_async8(st + O1 + i, src1 + i);
-#pragma unroll
-  for (int i = tid; i < L2; i += NTH) cp_async8(st + O2 + i, src2 + i);
-}
-
-template <int M, int B, int... Ts>
-__device__ __forceinline__ void pipe_stage(double *st, const RecFactArgs &a, const int32_t *trow, int tid,
-                                           std::integer_sequence<int, Ts...>) {
-  using P = Pipe<M, B>;
-  (pipe_stage_term<M, B, Ts>(st, a, trow, tid), ...);
-  const double *src = a.mk + *reinterpret_cast<const int64_t *>(trow + 2 * P::NT);
-  double *dst = st + P::SEG;
-#pragma unroll 4
-  for (int i = tid; i < P::BLK; i += P::NTH) cp_async8(dst + i, src + i);
-}
-
-template <int M, int B, int T>
-__device__ __forceinline__ void pipe_apply_term(double (&acc)[Pipe<M, B>::ROWS], const int (&dig)[M],
-                                                const double *st) {
-  constexpr int CT = Pipe<M, B>::CT, ROWS = Pipe<M, B>::ROWS;
-  constexpr int S = rf::term_mask(M, T);
-  constexpr int REST = ((1 << M) - 1) & ~S;
-  constexpr int s = rf::popc(S);
-  constexpr int O1 = rf::seg_before(M, B, T), O2 = O1 + rf::ipow(B, s);
-  int o1 = 0, o2 = 0;
-#pragma unroll
-  for (int q = M - CT; q < M; ++q) {
-    if (S & (1 << q)) o1 += dig[q] * rf::stride_in(S, q, B);
-    if (REST & (1 << q)) o2 += dig[q] * rf::stride_in(REST, q, B);
-  }
-  const double *f1 = st + O1 + o1;
-  const double *f2 = st + O2 + o2;
-  rows_fma<M, B, CT, S, false, false>(acc, f1, f2, std::make_integer_sequence<int, ROWS>{});
-}
-
-template <int M, int B, int... Ts>
-__device__ __forceinline__ void pipe_apply(double (&acc)[Pipe<M, B>::ROWS], const int (&dig)[M], const double *st,
-                                           std::integer_sequence<int, Ts...>) {
-  (pipe_apply_term<M, B, Ts>(acc, dig, st), ...);
-}
-
-template <int M, int B>
-__global__ void __launch_bounds__(Pipe<M, B>::NTH) k_recursion_pipe(RecFactArgs a) {
-  using P = Pipe<M, B>;
-  constexpr int D = P::STAGES - 1;  // blocks staged ahead of the one being evaluated
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double *stages = reinterpret_cast<double *>(smem_raw);
-  int32_t *trows = reinterpret_cast<int32_t *>(smem_raw + (size_t)P::STAGES * P::STAGE * 8);
-  const int tid = threadIdx.x;
-  const int64_t k_begin = a.nkeys * blockIdx.x / gridDim.x;
-  const int64_t k_end = a.nkeys * (blockIdx.x + 1) / gridDim.x;
-  if (k_begin >= k_end) return;
-  auto stage_trow = [&](int64_t i) {  // term-offset row + block offset of key i
-    int32_t *row = trows + (i % P::TSLOTS) * P::TROW_P;
-    for (int j = tid; j < 2 * P::NT; j += P::NTH) cp_async4(row + j, a.term_off + i * 2 * P::NT + j);
-    if (tid == 0) cp_async8(row + 2 * P::NT, a.blk_off + i);
-  };
-  // prologue: offsets of keys k_begin .. k_begin+2D-1, then the data of the first D keys
-  for (int64_t i = k_begin; i < k_begin + 2 * D && i < k_end; ++i) stage_trow(i);
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  for (int64_t i = k_begin; i < k_begin + D; ++i) {
-    if (i < k_end) pipe_stage<M, B>(stages + (i % P::STAGES) * P::STAGE, a, trows + (i % P::TSLOTS) * P::TROW_P,
-                                    tid, std::make_integer_sequence<int, P::NT>{});
-    cp_async_commit();
-  }
-  const bool active = tid < P::W;
-  const int c = active ? tid : 0;
-  int dig[M];
-#pragma unroll
-  for (int q = 0; q < M; ++q) dig[q] = 0;
-  {
-    int rem = c;
-#pragma unroll
-    for (int q = M - 1; q >= M - P::CT; --q) {
-      dig[q] = rem % B;
-      rem /= B;
-    }
-  }
-  for (int64_t i = k_begin; i < k_end; ++i) {
-    // block i's group is complete once at most D-1 newer groups are pending
-    cp_async_wait<D - 1>();
-    __syncthreads();
-    // stage block i+D (its offsets came with the group of iteration i-D, now
-    // complete) and the offsets of block i+2D
-    const int64_t j = i + D;
-    if (j < k_end) pipe_stage<M, B>(stages + (j % P::STAGES) * P::STAGE, a, trows + (j % P::TSLOTS) * P::TROW_P,
-                                    tid, std::make_integer_sequence<int, P::NT>{});
-    if (i + 2 * D < k_end) stage_trow(i + 2 * D);
-    cp_async_commit();
-    const double *st = stages + (i % P::STAGES) * P::STAGE;
-    const int64_t off = *reinterpret_cast<const int64_t *>(trows + (i % P::TSLOTS) * P::TROW_P + 2 * P::NT);
-    if (active) {
-      double acc[P::ROWS];
-#pragma unroll
-      for (int row = 0; row < P::ROWS; ++row) acc[row] = st[P::SEG + row * P::W + c];
-      pipe_apply<M, B>(acc, dig, st, std::make_integer_sequence<int, P::NT>{});
-      double *blk = a.mk + off + c;
-#pragma unroll
-      for (int row = 0; row < P::ROWS; ++row) blk[(int64_t)row * P::W] = acc[row];
-    }
-    __syncthreads();  // stage i % STAGES and its offset row are reused below
-  }
-}
-
 #if BCG_RF_PART == 0
 // ---- part 0: dispatch (the (m, b) instantiations live in parts 1..6,
 // separate translation units so nvcc compiles them in parallel) ----
@@ -826,9 +503,8 @@ cudaError_t launch_recursion_fact(const RecFactArgs &a, int m, int b, cudaStream
 #undef RF_B
 }
 #else
-template <int M, int B, int CT, int RES>
-static cudaError_t launch_v2(const RecFactArgs &a_in, cudaStream_t stream) {
-  using FC = FactCfg<M, B, CT, RES>;
+template <int M, int B, int CT>
+static cudaError_t go_fact_v2(const RecFactArgs &a_in, cudaStream_t stream) {
   constexpr int W = rf::ipow(B, CT);
   // the kernel's item arithmetic is 32-bit: launch key chunks of < 2^31 items
   constexpr int64_t kMaxKeys = ((int64_t)1 << 31) / W - 1;
@@ -836,122 +512,28 @@ static cudaError_t launch_v2(const RecFactArgs &a_in, cudaStream_t stream) {
   while (a.nkeys > kMaxKeys) {
     RecFactArgs part = a;
     part.nkeys = kMaxKeys;
-    cudaError_t e = launch_v2<M, B, CT, RES>(part, stream);
+    cudaError_t e = go_fact_v2<M, B, CT>(part, stream);
     if (e != cudaSuccess) return e;
     a.blk_off += kMaxKeys;
-    a.term_off += kMaxKeys * 2 * FC::NT;
+    a.term_off += kMaxKeys * 2 * rf::term_count(M);
     a.nkeys -= kMaxKeys;
   }
-  const int64_t items = a.nkeys * W;
-  const int threads = FC::NTHR;
-  const int64_t steps = (items + kRfThreads - 1) / kRfThreads;  // 128-item group steps
+  const int64_t steps = (a.nkeys * W + kRfThreads - 1) / kRfThreads;
   if (steps <= 0) return cudaSuccess;
-  size_t smem = FC::TOFF_BYTES;
-  for (int k = 2; k <= 3; ++k)
-    if ((RES >> (k - 2)) & 1) smem += (size_t)a.cum_len[k] * 8;
-  int64_t blocks;
-  if (RES == 0) {
-    static const int per_cta = getenv("BCG_RF_STEPS") ? atoi(getenv("BCG_RF_STEPS")) : 1;  // tuning knob
-    blocks = std::max<int64_t>(1, std::min<int64_t>(steps, (steps + per_cta - 1) / per_cta));
-  } else {  // persistent: one CTA per SM (the resident copy is paid once per CTA)
-    cudaError_t e = cudaFuncSetAttribute(k_recursion_fact<M, B, CT, RES>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_recursion_fact<M, B, CT, RES>, threads, smem);
-    if (e != cudaSuccess) return e;
-    blocks = std::max<int64_t>(1, std::min<int64_t>((steps + FC::NGRP - 1) / FC::NGRP,
-                                                    (int64_t)std::max(1, per_sm) * sms));
-  }
-  k_recursion_fact<M, B, CT, RES><<<(unsigned)blocks, threads, smem, stream>>>(a);
+  static const int per_cta = getenv("BCG_RF_STEPS") ? atoi(getenv("BCG_RF_STEPS")) : 1;  // tuning knob
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(steps, (steps + per_cta - 1) / per_cta));
+  k_recursion_fact<M, B, CT><<<(unsigned)blocks, kRfThreads, 0, stream>>>(a);
   g_launches++;
   return cudaGetLastError();
-}
-
-// BCG_RF_RES=1/3 (A/B knob): C_2 / C_2 and C_3 resident in shared memory
-// where they fit.  Measured slower than RES=0 on every config (the smaller
-// L1 hurts the C_4 / M_4 factor reads more than LDS helps;
-// profiles/r01_recursion_res.log), so the default is 0.
-template <int M, int B, int CT>
-static cudaError_t launch_v5(const RecFactArgs &a_in, cudaStream_t stream) {
-  using PC = PipeCfg<M, B, CT>;
-  constexpr int64_t kMaxKeys = ((int64_t)1 << 31) / PC::W - 1;
-  RecFactArgs a = a_in;
-  while (a.nkeys > kMaxKeys) {
-    RecFactArgs part = a;
-    part.nkeys = kMaxKeys;
-    cudaError_t e = launch_v5<M, B, CT>(part, stream);
-    if (e != cudaSuccess) return e;
-    a.blk_off += kMaxKeys;
-    a.term_off += kMaxKeys * 2 * PC::NT;
-    a.nkeys -= kMaxKeys;
-  }
-  const int64_t steps = (a.nkeys * PC::W + kRfThreads - 1) / kRfThreads;
-  if (steps <= 0) return cudaSuccess;
-  static int cap = 0;
-  if (!cap) {
-    cudaError_t e = cudaFuncSetAttribute(k_recursion_fact_pipe<M, B, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)PC::SMEM);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_recursion_fact_pipe<M, B, CT>, kRfThreads, PC::SMEM);
-    if (e != cudaSuccess) return e;
-    static const int ctas = getenv("BCG_RF_PIPE_CTAS") ? atoi(getenv("BCG_RF_PIPE_CTAS")) : 0;  // tuning knob
-    cap = std::max(1, ctas > 0 ? std::min(ctas, per_sm) : per_sm) * sms;
-  }
-  const int64_t grid = std::min<int64_t>(steps, cap);
-  k_recursion_fact_pipe<M, B, CT><<<(unsigned)grid, kRfThreads, PC::SMEM, stream>>>(a);
-  g_launches++;
-  return cudaGetLastError();
-}
-
-template <int M, int B, int CT>
-static cudaError_t go_fact_v2(const RecFactArgs &a, cudaStream_t stream) {
-  static const bool pipe = getenv("BCG_RF_PIPE") && atoi(getenv("BCG_RF_PIPE")) > 0;  // A/B knob
-  if (pipe) return launch_v5<M, B, CT>(a, stream);
-  static const int forced = getenv("BCG_RF_RES") ? atoi(getenv("BCG_RF_RES")) : 0;
-  const size_t budget = 200 * 1024 - FactCfg<M, B, CT, 1>::TOFF_BYTES;
-  const size_t c2 = (size_t)a.cum_len[2] * 8, c3 = M >= 5 ? (size_t)a.cum_len[3] * 8 : 0;
-  const int res = forced;
-  if (res == 3 && M >= 5 && c2 + c3 <= budget) return launch_v2<M, B, CT, 3>(a, stream);
-  if (res >= 1 && c2 <= budget) return launch_v2<M, B, CT, 1>(a, stream);
-  return launch_v2<M, B, CT, 0>(a, stream);
 }
 
 template <int M, int B>
 cudaError_t go_fact(const RecFactArgs &a, cudaStream_t stream) {
-  // A/B knob: BCG_RF_VARIANT=2 (v2), 3 (v3 staged), 4 (v4 pipelined)
+  // A/B knob: BCG_RF_VARIANT=2 (v2), 3 (v3 staged), 6 (v6 slab-staged, m = 6)
   static const int variant = getenv("BCG_RF_VARIANT") ? atoi(getenv("BCG_RF_VARIANT")) : 0;
-  static const bool no_staged = getenv("BCG_RF_NO_STAGED") != nullptr || variant == 2 || variant == 4;
-  if constexpr (Pipe<M, B>::ok) {
-    if (variant == 4) {  // measured slower than v2/v3 everywhere (profiles/r01_recursion_v4_sweep.log)
-      if (a.nkeys <= 0) return cudaSuccess;
-      using P = Pipe<M, B>;
-      static int grid_cap = 0;
-      if (!grid_cap) {
-        cudaError_t e = cudaFuncSetAttribute(k_recursion_pipe<M, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)P::SMEM);
-        if (e != cudaSuccess) return e;
-        int per_sm = 0, dev = 0, sms = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_recursion_pipe<M, B>, P::NTH, P::SMEM);
-        if (e != cudaSuccess) return e;
-        grid_cap = std::max(1, per_sm) * sms;
-      }
-      const int64_t grid = std::min<int64_t>(a.nkeys, grid_cap);
-      k_recursion_pipe<M, B><<<(unsigned)grid, P::NTH, P::SMEM, stream>>>(a);
-      g_launches++;
-      return cudaGetLastError();
-    }
-  }
+  static const bool no_staged = getenv("BCG_RF_NO_STAGED") != nullptr || variant == 2 || variant == 6;
   if constexpr (M == 6 && Slab6<B>::ok) {
-    static const bool slab = getenv("BCG_RF_SLAB") ? atoi(getenv("BCG_RF_SLAB")) > 0 : false;  // A/B knob
-    if ((slab && variant == 0) || variant == 6) {
+    if (variant == 6) {  // measured equal to v2 at cfg5, slower at cfg4 (profiles/r01_recursion_ncu.txt)
       if (a.nkeys <= 0) return cudaSuccess;
       using SL = Slab6<B>;
       static bool attr = false;

@@ -464,11 +464,8 @@ _VARIANT_SHAPES = [(16, 4, 8, 300), (12, 5, 4, 400), (9, 6, 3, 300), (12, 6, 6, 
 
 
 @pytest.mark.parametrize("env", [{"BCG_RF_VARIANT": "2", "BCG_RF_TILE": "-1"}, {"BCG_RF_VARIANT": "2", "BCG_RF_TILE": "0"},
-                                 {"BCG_RF_VARIANT": "2", "BCG_RF_RES": "0"}, {"BCG_RF_VARIANT": "2", "BCG_RF_RES": "1"},
-                                 {"BCG_RF_VARIANT": "2", "BCG_RF_RES": "3"},
                                  {"BCG_RF_VARIANT": "2", "BCG_RF_TILE": "1"}, {"BCG_RF_VARIANT": "3"},
-                                 {"BCG_RF_VARIANT": "4"}, {"BCG_RF_VARIANT": "6"}, {"BCG_RF_VARIANT": "2", "BCG_RF_PIPE": "1"},
-                                 {"BCG_RF_VARIANT": "2", "BCG_RF_PIPE": "1", "BCG_RF_TILE": "-1"}, {}])
+                                 {"BCG_RF_VARIANT": "6"}, {"BCG_RF_VARIANT": "2", "BCG_RF_STEPS": "7"}, {}])
 def test_recursion_variants_match_oracle(env, tmp_path):
     """Every factored-recursion kernel variant (the knobs are read once per
     process, so each runs in a subprocess) gives the oracle's cumulants,
