@@ -216,13 +216,14 @@ def moment_variant() -> int:
 def plan(n: int, m: int, b: int, fused: bool = False) -> Plan:
     """Cached device plan for (n, m, b), the current kernel variant and
     whether it is the fused multi-order plan."""
-    key = (int(n), int(m), int(b), -1 if fused else moment_variant(), bool(fused),
+    torch = torch_cuda()
+    # plans hold device tables: one per (device, n, m, b, kernel knobs)
+    key = (torch.cuda.current_device(), int(n), int(m), int(b), -1 if fused else moment_variant(), bool(fused),
            os.environ.get("BCG_TILE", ""), os.environ.get("BCG_MB", ""), os.environ.get("BCG_NO_HYBRID", ""))
     with _lock:
         p = _plans.get(key)
         if p is None:
-            torch_cuda()
-            p = _plans[key] = Plan(key[0], key[1], key[2], variant=key[3], fused=key[4])
+            p = _plans[key] = Plan(key[1], key[2], key[3], variant=key[4], fused=key[5])
         return p
 
 

@@ -536,13 +536,10 @@ cudaError_t go_fact(const RecFactArgs &a, cudaStream_t stream) {
     if (variant == 6) {  // measured equal to v2 at cfg5, slower at cfg4 (profiles/r01_recursion_ncu.txt)
       if (a.nkeys <= 0) return cudaSuccess;
       using SL = Slab6<B>;
-      static bool attr = false;
-      if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_recursion_slab6<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)SL::SMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-      }
+      // per launch: the attribute is per device
+      cudaError_t e = cudaFuncSetAttribute(k_recursion_slab6<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)SL::SMEM);
+      if (e != cudaSuccess) return e;
       k_recursion_slab6<B><<<(unsigned)a.nkeys, SL::NTH * SL::G, SL::SMEM, stream>>>(a);
       g_launches++;
       return cudaGetLastError();
