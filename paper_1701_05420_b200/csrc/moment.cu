@@ -124,8 +124,14 @@ __device__ __forceinline__ double2 kr_pair(const double *const (&row)[8], const 
 #pragma unroll
     for (int q = 1; q < NQ; ++q) {
       const double2 v = xs_pair(row[q], sw[q], j);
+#ifdef BCG_EXP_NODMUL
+      // timing experiment only (results are wrong): the same loads and stores, no FP64 multiply
+      p.x = __longlong_as_double(__double_as_longlong(p.x) ^ __double_as_longlong(v.x));
+      p.y = __longlong_as_double(__double_as_longlong(p.y) ^ __double_as_longlong(v.y));
+#else
       p.x *= v.x;
       p.y *= v.y;
+#endif
     }
   } else {
 #pragma unroll
@@ -218,6 +224,9 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
 
   auto build = [&](int c) {  // Khatri-Rao factors of chunk c -> kra/krb[c & 1]
     mbar_wait(&bar[c & 1], (uint32_t)((c >> 1) & 1));
+#ifdef BCG_EXP_NOBUILD
+    return;  // timing experiment only (results are wrong): the kernel without the Khatri-Rao build
+#endif
     const double *xst = xs + (c & 1) * xrows * LDX;
     {
       const double *ra[8];
