@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  auto build = [&](int c) {  // Khatri-Rao factors of chunk c -> kra/krb[c & 1]
+  auto build_a = [&](int c) {  // row factors of chunk c -> kra[c & 1] (waits for the chunk)
     mbar_wait(&bar[c & 1], (uint32_t)((c >> 1) & 1));
 #ifdef BCG_EXP_NOBUILD
     return;  // timing experiment only (results are wrong): the kernel without the Khatri-Rao build
@@ -245,6 +245,12 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
         *reinterpret_cast<double2 *>(wa + ((2 * j) ^ swa)) = p;
       }
     }
+  };
+  auto build_b = [&](int c) {  // column factors of chunk c -> krb[c & 1]
+#ifdef BCG_EXP_NOBUILD
+    return;
+#endif
+    const double *xst = xs + (c & 1) * xrows * LDX;
     {
       const double *rb[8];
       int sb[8];
@@ -263,6 +269,10 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
       }
     }
   };
+  auto build = [&](int c) {  // Khatri-Rao factors of chunk c -> kra/krb[c & 1]
+    build_a(c);
+    build_b(c);
+  };
 
   if (nch > 0) {
     issue(0);
@@ -272,24 +282,38 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
     if (nch > 2) issue(2);
   }
   for (int c = 0; c < nch; ++c) {
-    if (c + 1 < nch) build(c + 1);
     // ---- DMMA over chunk c ----
     // fragment rows = gid (mod 4 after the 8-row and warp offsets): swizzle (gid & 3) << 2
     const int swf = (gid & 3) << 2;
     const double *ka = kra + (c & 1) * TM * LDK + (wm * SH::WM + gid) * LDK + tig;
     const double *kb = krb + (c & 1) * TN * LDK + (wn * SH::WN + gid) * LDK + tig;
+    auto ksteps = [&](int k0, int k1) {
 #pragma unroll
-    for (int k = 0; k < KC; k += 4) {
-      double fa[MT], fb[NT];
-      const int ks = k ^ swf;
+      for (int k = k0; k < k1; k += 4) {
+        double fa[MT], fb[NT];
+        const int ks = k ^ swf;
 #pragma unroll
-      for (int i = 0; i < MT; ++i) fa[i] = ka[8 * i * LDK + ks];
+        for (int i = 0; i < MT; ++i) fa[i] = ka[8 * i * LDK + ks];
 #pragma unroll
-      for (int j = 0; j < NT; ++j) fb[j] = kb[8 * j * LDK + ks];
+        for (int j = 0; j < NT; ++j) fb[j] = kb[8 * j * LDK + ks];
 #pragma unroll
-      for (int i = 0; i < MT; ++i)
+        for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < NT; ++j) dmma884(acc[i][j], fa[i], fb[j]);
+          for (int j = 0; j < NT; ++j) dmma884(acc[i][j], fa[i], fb[j]);
+      }
+    };
+    if constexpr (H >= 3 && R >= 3) {
+      // three-mode factors (m = 6): the column factors of chunk c+1 are built
+      // between the two halves of chunk c's DMMAs (+0.6 points of DMMA peak at
+      // cfg4; -0.5 at cfg2's two-mode factors, which keep one build phase;
+      // profiles/r01_moment_schedule_experiments.log (5))
+      if (c + 1 < nch) build_a(c + 1);
+      ksteps(0, KC / 2);
+      if (c + 1 < nch) build_b(c + 1);
+      ksteps(KC / 2, KC);
+    } else {
+      if (c + 1 < nch) build(c + 1);
+      ksteps(0, KC);
     }
     __syncthreads();  // KR[c+1] complete, KR[c] and xs[(c+1) & 1] free
     if (c + 3 < nch) issue(c + 3);
