@@ -516,3 +516,34 @@ def test_concurrent_order_schedule_is_bitwise_serial(tmp_path):
     cs = bcg.cumulants_upto(x, 6, b=3)
     for k in range(2, 7):
         np.testing.assert_array_equal(cs[k].packed_host(), serial[f"c{k}"])
+
+
+@pytest.mark.parametrize("n,m,b", [(12, 6, 3), (13, 5, 2), (16, 4, 4), (10, 6, 2)])
+def test_recursion_key_ranges_compose_bitwise(n, m, b, rng):
+    """The block-range recursion the multi-GPU paths run per rank
+    (CudaOps.recursion_range -> bcg_cumulant_recursion_ex on [k0, k1)) over a
+    split of the key list equals the full-range recursion bit for bit,
+    incl. partial-edge blocks (n % b != 0)."""
+    import torch
+
+    from paper_1701_05420_b200.cumulants import cumulants_device
+    from paper_1701_05420_b200.distributed import CudaOps, block_bounds
+    from paper_1701_05420_b200.layout import layout
+    from paper_1701_05420_b200.moments import _center_transposed, _moment_device_t
+
+    x = torch.from_numpy(rng.exponential(1.0, (2000, n)) + rng.standard_normal((2000, n))).cuda()
+    _, lower_t = cumulants_device(x, m - 1, b, c1_host=False)
+    lower = {t.m: t.data for t in lower_t if t.m <= m - 2}
+    xt = _center_transposed(x, x.mean(0))
+    central = {k: _moment_device_t(xt, x.shape[0], k, b).data for k in range(4, m - 1)}
+    mk = _moment_device_t(xt, x.shape[0], m, b).data
+    K = layout(n, m, b).K
+    ops = CudaOps()
+    full = mk.clone()
+    ops.recursion_range(full, n, m, b, lower, 0, K, central)
+    for world in (2, 3, 5):
+        part = mk.clone()
+        for r in range(world):
+            k0, k1 = block_bounds(K, world, r)
+            ops.recursion_range(part, n, m, b, lower, k0, k1, central)
+        assert torch.equal(part, full), world
