@@ -219,7 +219,7 @@ def plan(n: int, m: int, b: int, fused: bool = False) -> Plan:
     torch = torch_cuda()
     # plans hold device tables: one per (device, n, m, b, kernel knobs)
     key = (torch.cuda.current_device(), int(n), int(m), int(b), -1 if fused else moment_variant(), bool(fused),
-           os.environ.get("BCG_TILE", ""), os.environ.get("BCG_MB", ""), os.environ.get("BCG_NO_HYBRID", ""))
+           os.environ.get("BCG_TILE", ""), os.environ.get("BCG_NO_HYBRID", ""))
     with _lock:
         p = _plans.get(key)
         if p is None:

@@ -1,9 +1,9 @@
 """Time the order-m moment GEMM of the bench configs under several plan
 settings (environment knobs read when a plan is built: BCG_TILE=TMxTN,
-BCG_MB=TMxTNxLA, BCG_NO_HYBRID=1), checking every setting bitwise against the
+BCG_NO_HYBRID=1), checking every setting bitwise against the
 first on the same data.
 
-    python tools/tune_moment.py --configs cfg2 cfg3 --settings "" BCG_MB=64x64x1 [--t 0] [--order 0]
+    python tools/tune_moment.py --configs cfg2 cfg3 --settings "" BCG_TILE=16x128 [--t 0] [--order 0]
 """
 
 import argparse
@@ -18,7 +18,7 @@ import torch  # noqa: E402
 import workloads  # noqa: E402
 from paper_1701_05420_b200.moments import _moment_device, center  # noqa: E402
 
-KNOBS = ("BCG_TILE", "BCG_MB", "BCG_NO_HYBRID")
+KNOBS = ("BCG_TILE", "BCG_NO_HYBRID")
 
 
 def apply(setting):
