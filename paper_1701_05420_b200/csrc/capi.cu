@@ -552,7 +552,6 @@ static int recursion_common(const bcg_plan *plan, double *mk, const double *cons
   a.k0 = std::max<int64_t>(0, k0);
   a.k1 = std::min<int64_t>(a.K, k1);
   a.klist = klist;
-  if ((size_t)p.nslots * 8 > 200 * 1024) return fail(BCG_EINVAL, "cumulant order too high for the recursion kernel");
   CUDA_TRY(bcg::launch_recursion(a, s), "recursion kernel");
   return BCG_OK;
 }

@@ -20,6 +20,10 @@
 
 namespace bcg {
 
+// SMEM_SLOTS: the block's slot offsets staged in shared memory (nslots <=
+// 25600, i.e. m <= 9); otherwise (m = 10..12: up to 2.5e6 slots per block)
+// each factor's lower-block offset is looked up in the plan tables directly
+template <bool SMEM_SLOTS>
 __global__ void __launch_bounds__(256) k_recursion(RecursionArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int64_t *slot_base = reinterpret_cast<int64_t *>(smem_raw);  // nslots
@@ -34,7 +38,7 @@ __global__ void __launch_bounds__(256) k_recursion(RecursionArgs a) {
     edges[tid] = (int)(hi - (j - 1) * a.b);
   }
   // slot s -> offset of its lower block (the slot's order = popcount(mask))
-  {
+  if constexpr (SMEM_SLOTS) {
     int s = 0;
     for (int p = 0; p < a.p_end; ++p) {
       for (int i = 0; i < 8; ++i) {
@@ -80,7 +84,13 @@ __global__ void __launch_bounds__(256) k_recursion(RecursionArgs a) {
             mask &= mask - 1;
             lin = lin * edges[q] + o[q];
           }
-          const double v = __ldg(a.lower[ord] + slot_base[s] + lin);
+          int64_t base;
+          if constexpr (SMEM_SLOTS) {
+            base = slot_base[s];
+          } else {
+            base = a.lower_offs[ord][a.sub_rank[k * a.nslots + s]];
+          }
+          const double v = __ldg(a.lower[ord] + base + lin);
           prod = i == 0 ? v : __dmul_rn(prod, v);
         }
         bsum = __dadd_rn(bsum, prod);
@@ -92,13 +102,16 @@ __global__ void __launch_bounds__(256) k_recursion(RecursionArgs a) {
 }
 
 cudaError_t launch_recursion(const RecursionArgs &args, cudaStream_t stream) {
-  const size_t smem = (size_t)args.nslots * sizeof(int64_t);
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(k_recursion, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
   if (args.K <= 0) return cudaSuccess;
   if (args.k1 <= args.k0) return cudaSuccess;
-  k_recursion<<<(unsigned)(args.k1 - args.k0), 256, smem, stream>>>(args);
+  const size_t smem = (size_t)args.nslots * sizeof(int64_t);
+  if (smem <= 200 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_recursion<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_recursion<true><<<(unsigned)(args.k1 - args.k0), 256, smem, stream>>>(args);
+  } else {
+    k_recursion<false><<<(unsigned)(args.k1 - args.k0), 256, 0, stream>>>(args);
+  }
   g_launches++;
   return cudaGetLastError();
 }

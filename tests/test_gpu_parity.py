@@ -547,3 +547,32 @@ def test_recursion_key_ranges_compose_bitwise(n, m, b, rng):
             k0, k1 = block_bounds(K, world, r)
             ops.recursion_range(part, n, m, b, lower, k0, k1, central)
         assert torch.equal(part, full), world
+
+
+@pytest.mark.parametrize("n,m,b,t", [(3, 8, 2, 300), (5, 7, 3, 400), (2, 9, 1, 200), (2, 10, 1, 200)])
+def test_high_order_cumulants_match_oracle(n, m, b, t, rng):
+    """Orders past the factored kernel's range (m >= 7: the partition-table
+    recursion) against the oracle, including partial blocks."""
+    x = rng.exponential(1.0, (t, n)) + rng.standard_normal((t, n))
+    cs = bcg.cumulants_upto(x, m, b=b)
+    c1, want = orc.cumulants_upto(x, m, b)
+    np.testing.assert_allclose(cs[1], c1, rtol=1e-12, atol=1e-15)
+    for k in range(2, m + 1):
+        np.testing.assert_allclose(packed(cs[k]), want[k], rtol=1e-9, atol=1e-12, err_msg=f"k={k}")
+
+
+def test_order_12_runs_with_exact_properties(rng):
+    """MAX_M = 12 (bc/partitions.py:16): the partition recursion with its
+    2.5e6 slots per block (plan-table lookups, not shared memory) runs, and
+    the exact properties hold: constant data gives exact zeros, power-of-two
+    scaling scales every order bitwise."""
+    x = rng.exponential(1.0, (150, 2))
+    cs = bcg.cumulants_upto(x, 12, b=1)
+    cs2 = bcg.cumulants_upto(2.0 * x, 12, b=1)
+    for k in range(2, 13):
+        a = packed(cs[k])
+        assert np.all(np.isfinite(a))
+        np.testing.assert_array_equal(packed(cs2[k]), (2.0 ** k) * a)
+    const = bcg.cumulants_upto(np.full((50, 2), 3.25), 12, b=1)
+    for k in range(2, 13):
+        assert np.max(np.abs(packed(const[k]))) == 0.0
