@@ -576,3 +576,17 @@ def test_order_12_runs_with_exact_properties(rng):
     const = bcg.cumulants_upto(np.full((50, 2), 3.25), 12, b=1)
     for k in range(2, 13):
         assert np.max(np.abs(packed(const[k]))) == 0.0
+
+
+def test_blocksymtensor_arithmetic_errors_and_bitwise_commutation(rng):
+    """pkg/tests/test_symtensor.py:172-199: a + b elementwise, shape mismatch
+    rejected, addition commutes bitwise (device axpby)."""
+    from conftest import random_sym_dense
+
+    a = bcg.BlockSymTensor.from_dense(random_sym_dense(4, 3, rng), b=2)
+    c = bcg.BlockSymTensor.from_dense(random_sym_dense(4, 3, rng), b=2)
+    np.testing.assert_array_equal((a + c).to_dense(), (c + a).to_dense())
+    assert (a + c).get((1, 2, 3)) == a.get((1, 2, 3)) + c.get((1, 2, 3))
+    d = bcg.BlockSymTensor.from_dense(random_sym_dense(4, 3, rng), b=1)
+    with pytest.raises(bcg.ValidationError, match="mismatch"):
+        a + d

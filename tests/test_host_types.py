@@ -127,3 +127,13 @@ def test_constructor_validation():
         BlockSymTensor(0, 2, 2, {})
     with pytest.raises(ValidationError):
         BlockSymTensor.from_packed(4, 2, 2, np.zeros(3))
+
+
+def test_get_index_errors():
+    """Element access errors as the reference (pkg/tests/test_symtensor.py:143-147)."""
+    t = BlockSymTensor.zeros(3, 2, 2)
+    with pytest.raises(ValidationError, match="out of range"):
+        t.get((1, 4))
+    with pytest.raises(ValidationError, match="entries"):
+        t.get((1, 2, 3))
+    assert BlockSymTensor.from_dense(np.ones((3, 3, 3)), b=2).get((1, 2, 2)) == 1.0
