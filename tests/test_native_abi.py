@@ -105,3 +105,24 @@ def test_native_partitions_match_python():
         keys, _, _, _ = plan.layout(k)
         lay = orc.block_layout(9, k, 2)
         assert [tuple(r) for r in keys.tolist()] == lay[0]
+
+
+def test_no_cpu_fallback_without_a_device():
+    """The compute entry points fail loudly when no CUDA device is visible
+    (there is no CPU fallback): run in a subprocess with CUDA hidden."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, numpy as np; sys.path.insert(0, %r)\n"
+            "import paper_1701_05420_b200 as bcg\n"
+            "try:\n"
+            "    bcg.cumulants_upto(np.ones((10, 2)), 3, b=1)\n"
+            "except bcg.NativeUnavailableError as e:\n"
+            "    print('raised:', e)\n"
+            "else:\n"
+            "    print('no error')\n" % root)
+    out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "CUDA_VISIBLE_DEVICES": ""},
+                         capture_output=True, text=True, timeout=300)
+    assert "raised:" in out.stdout, out.stdout + out.stderr
