@@ -590,3 +590,47 @@ def test_blocksymtensor_arithmetic_errors_and_bitwise_commutation(rng):
     d = bcg.BlockSymTensor.from_dense(random_sym_dense(4, 3, rng), b=1)
     with pytest.raises(bcg.ValidationError, match="mismatch"):
         a + d
+
+
+def _gloo_gpu_worker(rank, world, port, x, m, b, out):
+    import os
+
+    import torch.distributed as dist
+
+    from paper_1701_05420_b200.distributed import cumulants_upto_block_split, cumulants_upto_sharded, shard_bounds
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = shard_bounds(x.shape[0], world, rank)
+    mean, ts = cumulants_upto_sharded(torch.from_numpy(x[lo:hi]).cuda(), m, b)
+    _, ts2 = cumulants_upto_block_split(torch.from_numpy(x).cuda(), m, b)
+    np.savez(f"{out}_{rank}.npz", mean=mean.cpu().numpy(), **{f"c{k}": t.cpu().numpy() for k, t in enumerate(ts, 2)},
+             **{f"d{k}": t.cpu().numpy() for k, t in enumerate(ts2, 2)})
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("t,n,m,b", [(5001, 9, 6, 3), (3000, 16, 4, 8)])
+def test_two_ranks_on_one_gpu_over_gloo(t, n, m, b, tmp_path, rng):
+    """World size 2 through the real CUDA per-rank ops (both ranks on cuda:0,
+    host-staged gloo collectives, so no kernel waits on another rank): the
+    sample split (all-reduce, reduce-scatter -> block-range recursion ->
+    all-gather) matches cumulants_upto, the block split bit for bit."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    x = rng.exponential(1.0, (t, n)) + rng.standard_normal((t, n))
+    out = str(tmp_path / "r")
+    mp.spawn(_gloo_gpu_worker, args=(2, port, x, m, b, out), nprocs=2, join=True)
+    cs = bcg.cumulants_upto(x, m, b=b)
+    for r in range(2):
+        got = np.load(f"{out}_{r}.npz")
+        np.testing.assert_allclose(got["mean"], cs[1], rtol=1e-13)
+        for k in range(2, m + 1):
+            want = cs[k].packed_host()
+            np.testing.assert_allclose(got[f"c{k}"], want, rtol=1e-9, atol=1e-12)
+            np.testing.assert_array_equal(got[f"d{k}"], want)
