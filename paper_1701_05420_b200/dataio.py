@@ -1,4 +1,12 @@
-"""Tensor I/O: the reference's JSON document codec and a packed binary format.
+"""Data and tensor I/O: CSV ingestion, the reference's JSON document codec and
+a packed binary format.
+
+* ``ingest_csv`` / ``write_csv`` -- the reference's CSV contract
+  (bc/dataio.py:23-86: '.' decimals, optional single header line, ragged /
+  non-numeric / non-finite cells rejected with 1-based row and column), with
+  a vectorised parse (numpy's C reader) and the reference's line-by-line
+  parser kept for the error messages; ``device="cuda"`` lands the matrix in
+  HBM through a pinned buffer (the host ingest path).
 
 * ``emit_tensor`` / ``load_tensor`` -- the reference's JSON document
   (bc/dataio.py:89-106 over BlockSymTensor.to_doc/from_doc,
@@ -33,6 +41,95 @@ from .layout import layout
 from .symtensor import BlockSymTensor
 
 MAGIC = b"BCGPACK1"
+
+
+def _ingest_slow(path, lines):
+    """The reference's parser (bc/dataio.py:36-76), for exact diagnostics."""
+    def parse_line(line):
+        try:
+            return [float(c) for c in line.split(",")]
+        except ValueError:
+            return None
+
+    first = parse_line(lines[0])
+    start = 0 if first is not None else 1
+    if first is None and len(lines) == 1:
+        raise ValidationError(f"{path}: no numeric rows")
+    rows = []
+    width = None
+    for lineno, line in enumerate(lines[start:], start=1):
+        cells = line.split(",")
+        if width is None:
+            width = len(cells)
+        elif len(cells) != width:
+            raise ValidationError(f"{path}: row {lineno} has {len(cells)} cells, expected {width}")
+        values = []
+        for col, cell in enumerate(cells, start=1):
+            try:
+                v = float(cell)
+            except ValueError:
+                raise ValidationError(
+                    f"{path}: non-numeric cell at row {lineno}, column {col}: {cell.strip()!r}") from None
+            if not np.isfinite(v):
+                raise ValidationError(f"{path}: non-finite value at row {lineno}, column {col}")
+            values.append(v)
+        rows.append(values)
+    if not rows:
+        raise ValidationError(f"{path}: no numeric rows")
+    return np.array(rows, dtype=np.float64)
+
+
+def ingest_csv(path, device=None):
+    """Read a t x n observation matrix from a CSV file (bc/dataio.py:23-76).
+
+    Returns a C-contiguous float64 numpy array, or with ``device="cuda"`` a
+    CUDA tensor uploaded through page-locked memory."""
+    from pathlib import Path
+
+    path = Path(path)
+    try:
+        text = path.read_text(encoding="utf-8")
+    except OSError as exc:
+        raise ValidationError(f"cannot read {path}: {exc}") from exc
+    lines = [ln for ln in text.splitlines() if ln.strip()]
+    if not lines:
+        raise ValidationError(f"{path}: file is empty")
+    try:
+        [float(c) for c in lines[0].split(",")]
+        start = 0
+    except ValueError:
+        start = 1
+    arr = None
+    if len(lines) > start:
+        try:
+            arr = np.loadtxt(lines[start:], delimiter=",", dtype=np.float64, comments=None, ndmin=2)
+        except ValueError:
+            arr = None  # ragged or non-numeric: the reference parser names the cell
+    if arr is None or not np.isfinite(arr).all():
+        arr = _ingest_slow(path, lines)  # raises with the reference's message
+    arr = np.ascontiguousarray(arr)
+    if device is None:
+        return arr
+    from ._native import torch_cuda
+
+    torch = torch_cuda()
+    pinned = torch.from_numpy(arr).pin_memory()
+    return pinned.to(device)
+
+
+def write_csv(path, data, header=None) -> None:
+    """Write an observation matrix as CSV with round-trip-exact floats
+    (bc/dataio.py:79-86)."""
+    arr = data.detach().cpu().numpy() if hasattr(data, "detach") else np.asarray(data, dtype=np.float64)
+    if arr.ndim != 2:
+        raise ValidationError(f"data must be 2-D, got shape {arr.shape}")
+    with open(path, "w", encoding="utf-8") as fh:
+        if header is not None:
+            fh.write(",".join(header) + "\n")
+        for row in arr:
+            fh.write(",".join(repr(float(v)) for v in row) + "\n")
+
+
 CHUNK_BYTES = 256 << 20  # pinned staging chunk for device tensors
 
 

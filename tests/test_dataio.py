@@ -99,3 +99,55 @@ def test_packed_roundtrip_device(rng, tmp_path, monkeypatch):
     back = load_packed(p)
     assert back._data is not None and back._data.is_cuda
     np.testing.assert_array_equal(back.data.cpu().numpy(), cs[4].packed_host())
+
+
+def test_csv_roundtrip_exact_with_header(rng, tmp_path):
+    from paper_1701_05420_b200.dataio import ingest_csv, write_csv
+
+    x = rng.standard_normal((37, 5)) * 10.0 ** rng.integers(-5, 5, (37, 5))
+    write_csv(tmp_path / "a.csv", x, header=["v1", "v2", "v3", "v4", "v5"])
+    np.testing.assert_array_equal(ingest_csv(tmp_path / "a.csv"), x)
+    write_csv(tmp_path / "b.csv", x)
+    np.testing.assert_array_equal(ingest_csv(tmp_path / "b.csv"), x)
+
+
+@pytest.mark.parametrize("text,match", [
+    ("1,2\n3\n", "row 2 has 1 cells, expected 2"),
+    ("a,b\n1,2\n3,x\n", "non-numeric cell at row 2, column 2: 'x'"),
+    ("1,2\n3,nan\n", "non-finite value at row 2, column 2"),
+    ("1,inf\n", "non-finite value at row 1, column 2"),
+    ("a,b\n", "no numeric rows"),
+    ("\n\n", "file is empty"),
+])
+def test_csv_errors_match_reference_messages(text, match, tmp_path):
+    """bc/dataio.py:36-76 diagnostics (1-based rows, header excluded)."""
+    from paper_1701_05420_b200.dataio import ingest_csv
+
+    p = tmp_path / "bad.csv"
+    p.write_text(text)
+    with pytest.raises(ValidationError, match=match):
+        ingest_csv(p)
+
+
+def test_csv_blank_lines_and_spaces(tmp_path):
+    from paper_1701_05420_b200.dataio import ingest_csv
+
+    p = tmp_path / "s.csv"
+    p.write_text("x,y\n\n 1.5, 2\n3,4e-3\n\n")
+    np.testing.assert_array_equal(ingest_csv(p), np.array([[1.5, 2.0], [3.0, 4e-3]]))
+
+
+@pytest.mark.gpu
+def test_csv_ingest_to_device_then_cumulants(rng, tmp_path):
+    """CSV -> pinned -> HBM ingest path feeding cumulants_upto (same result as
+    from the in-memory array)."""
+    import paper_1701_05420_b200 as bcg
+    from paper_1701_05420_b200.dataio import ingest_csv, write_csv
+
+    x = rng.exponential(1.0, (500, 4))
+    write_csv(tmp_path / "x.csv", x, header=["a", "b", "c", "d"])
+    X = ingest_csv(tmp_path / "x.csv", device="cuda")
+    assert X.is_cuda and X.shape == (500, 4)
+    a, b = bcg.cumulants_upto(X, 4, b=2), bcg.cumulants_upto(x, 4, b=2)
+    for k in range(2, 5):
+        np.testing.assert_array_equal(a[k].packed_host(), b[k].packed_host())
