@@ -85,3 +85,15 @@ def test_fullsize_top_moment_blocks_match_host_gemm(name):
         want = _host_block(xc, key, b, m // 2)
         scale = float(np.max(np.abs(want)))
         np.testing.assert_allclose(got, want, rtol=1e-11, atol=1e-13 * scale, err_msg=f"{name} block {key}")
+
+
+@pytest.mark.parametrize("name", _CFGS)
+def test_fullsize_rerun_is_bitwise(name):
+    """Deterministic reductions everywhere (fixed split-K slices, ordered
+    partial sums, no float atomics, concurrent order schedule): a rerun at
+    full size reproduces every element of every order bit for bit."""
+    cfg, x, cs = _data(name)
+    again = bcg.cumulants_upto(x, cfg.m, b=cfg.b)
+    np.testing.assert_array_equal(again[1], cs[1])
+    for k in range(2, cfg.m + 1):
+        np.testing.assert_array_equal(again[k].packed_host(), cs[k].packed_host(), err_msg=f"C{k}")
