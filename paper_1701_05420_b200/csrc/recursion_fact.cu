@@ -153,6 +153,9 @@ __device__ __forceinline__ void apply_terms(double (&acc)[rf::ipow(B, M - CT)], 
 
 constexpr int kRfThreads = 128;
 
+#ifndef BCG_RF_STREAM
+#define BCG_RF_STREAM 1  // cfg5 14.0 -> 13.5 ms (profiles/r01_recursion_res.log)
+#endif
 template <int M, int B, int CT>
 __global__ void __launch_bounds__(kRfThreads, (rf::ipow(B, M - CT) > 32 ? 3 : 4)) k_recursion_fact(RecFactArgs a) {
   constexpr int NT = rf::term_count(M);
@@ -200,10 +203,21 @@ __global__ void __launch_bounds__(kRfThreads, (rf::ipow(B, M - CT) > 32 ? 3 : 4)
     double *blk = a.mk + __ldg(a.blk_off + kb) + c;
     double acc[ROWS];
 #pragma unroll
+#if BCG_RF_STREAM
+    // M_m is read once and C_m written once: streaming (evict-first) accesses
+    // keep them from displacing the factor blocks the neighbouring outputs
+    // re-read from L1
+    for (int row = 0; row < ROWS; ++row) acc[row] = __ldcs(blk + (int64_t)row * W);
+#else
     for (int row = 0; row < ROWS; ++row) acc[row] = blk[(int64_t)row * W];
+#endif
     apply_terms<M, B, CT>(acc, dig, a, toff, std::make_integer_sequence<int, NT>{});
 #pragma unroll
+#if BCG_RF_STREAM
+    for (int row = 0; row < ROWS; ++row) __stcs(blk + (int64_t)row * W, acc[row]);
+#else
     for (int row = 0; row < ROWS; ++row) blk[(int64_t)row * W] = acc[row];
+#endif
   }
 }
 
