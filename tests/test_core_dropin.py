@@ -1,0 +1,95 @@
+"""paper_1701_05420_b200.core_dropin against the reference's own compiled
+module (blockcumulants._core, built from /root/reference into oracle/_ref by
+oracle/build_ref.sh; the CPU oracle's restatement where it is absent): same
+arguments, accumulate semantics, key ranges and errors (bc/_core.pyx:126-175)."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _reference_core():
+    path = os.path.join(ROOT, "oracle", "_ref")
+    if not os.path.isdir(os.path.join(path, "blockcumulants")):
+        return None
+    sys.path.insert(0, path)
+    try:
+        from blockcumulants import _core  # the unmodified reference's Cython kernel
+        return _core
+    except ImportError:
+        return None
+    finally:
+        sys.path.remove(path)
+
+
+@pytest.mark.parametrize("n,m,b,t", [(7, 4, 3, 513), (9, 3, 2, 1000), (5, 6, 2, 300), (12, 5, 4, 257)])
+def test_moment_blocks_matches_reference_core(n, m, b, t, rng):
+    from paper_1701_05420_b200 import core_dropin
+
+    ref = _reference_core()
+    x = rng.standard_normal((t, n))
+    xt = np.ascontiguousarray(x.T)
+    keys, col0, edges, offs = orc.block_layout(n, m, b)
+    K = len(keys)
+    got = np.zeros(int(offs[-1]))
+    for k0, k1 in ((0, K // 3), (K // 3, K)):  # disjoint key ranges, like moment_parallel_blocks
+        core_dropin.moment_blocks(xt, col0, edges, got, offs, k0, k1)
+    want = np.zeros_like(got)
+    if ref is not None:
+        ref.moment_blocks(xt, col0, edges, want, offs, 0, K)
+    else:
+        want = orc.moment_raw_sums(x, m, b)
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12)
+    # accumulate semantics: a second full call adds the sums again
+    core_dropin.moment_blocks(xt, col0, edges, got, offs, 0, K)
+    np.testing.assert_allclose(got, 2 * want, rtol=1e-12, atol=1e-12)
+    # a key range touches only its slice of out
+    part = np.full_like(got, 7.0)
+    core_dropin.moment_blocks(xt, col0, edges, part, offs, 1, 2)
+    lo, hi = int(offs[1]), int(offs[2])
+    assert np.all(part[:lo] == 7.0) and np.all(part[hi:] == 7.0)
+    np.testing.assert_allclose(part[lo:hi], 7.0 + want[lo:hi], rtol=1e-12, atol=1e-12)
+
+
+def test_moment_blocks_errors_match_reference(rng):
+    from paper_1701_05420_b200 import core_dropin
+
+    x = rng.standard_normal((50, 4))
+    xt = np.ascontiguousarray(x.T)
+    keys, col0, edges, offs = orc.block_layout(4, 3, 2)
+    out = np.zeros(int(offs[-1]))
+    with pytest.raises(ValueError, match="Buffer dtype mismatch"):
+        core_dropin.moment_blocks(xt, col0.astype(np.int32), edges, out, offs, 0, len(keys))
+    with pytest.raises(ValueError, match="C-contiguous"):
+        core_dropin.moment_blocks(x.T, col0, edges, out, offs, 0, len(keys))
+    wide = np.zeros((len(keys), 17), dtype=np.int64)
+    with pytest.raises(ValueError, match="2 <= m <= 16"):
+        core_dropin.moment_blocks(xt, wide, wide, out, offs, 0, len(keys))
+    ref = _reference_core()
+    if ref is not None:
+        with pytest.raises(ValueError, match="2 <= m <= 16"):
+            ref.moment_blocks(xt, wide, wide, out, offs, 0, len(keys))
+
+
+def test_naive_moment4_matches_reference_core(rng):
+    from paper_1701_05420_b200 import core_dropin
+
+    x = rng.standard_normal((400, 5))
+    xt = np.ascontiguousarray(x.T)
+    got = np.ones((5, 5, 5, 5))
+    core_dropin.naive_moment4(xt, got)
+    ref = _reference_core()
+    want = np.ones((5, 5, 5, 5))
+    if ref is not None:
+        ref.naive_moment4(xt, want)
+    else:
+        want += np.einsum("ta,tb,tc,td->abcd", x, x, x, x)
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-11)
