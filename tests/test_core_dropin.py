@@ -93,3 +93,40 @@ def test_naive_moment4_matches_reference_core(rng):
     else:
         want += np.einsum("ta,tb,tc,td->abcd", x, x, x, x)
     np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-11)
+
+
+def _reference_package():
+    path = os.path.join(ROOT, "oracle", "_ref")
+    if not os.path.isdir(os.path.join(path, "blockcumulants")):
+        return None
+    sys.path.insert(0, path)
+    try:
+        import blockcumulants as bc  # the unmodified reference, built by oracle/build_ref.sh
+        return bc
+    except ImportError:
+        return None
+    finally:
+        sys.path.remove(path)
+
+
+@pytest.mark.parametrize("name,t,m", [("cfg2", 20000, 4), ("cfg3", 4000, 5), ("cfg4", 1500, 6)])
+def test_live_differential_against_the_reference(name, t, m):
+    """The unmodified reference's cumulants_upto run live on the same seeded
+    BASELINE recipe rows as ours (bc/cumulants.py:173-193): every element of
+    C1..Cm within the reference's own 1e-9 criterion."""
+    import paper_1701_05420_b200 as bcg
+    import workloads
+
+    bc = _reference_package()
+    if bc is None:
+        pytest.skip("reference not built (oracle/build_ref.sh)")
+    cfg = workloads.CONFIGS[name]
+    x = workloads.generate(name, t)
+    want = bc.cumulants_upto(x, m, b=cfg.b)
+    got = bcg.cumulants_upto(x, m, b=cfg.b)
+    np.testing.assert_allclose(got[1], want[1], rtol=1e-12, atol=1e-14)
+    for k in range(2, m + 1):
+        lay_keys = list(want[k].blocks)
+        for key in lay_keys:
+            np.testing.assert_allclose(got[k].blocks[key], want[k].blocks[key], rtol=1e-9, atol=1e-12,
+                                       err_msg=f"{name} C{k} block {key}")
