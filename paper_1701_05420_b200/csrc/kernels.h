@@ -56,6 +56,18 @@ cudaError_t launch_pad_rows(const double *src, int64_t n, int64_t t, int64_t lds
 cudaError_t launch_rowstats(const double *xt, int64_t n, int64_t t, int64_t ldt, double *sums, double *sumsq,
                             double *ws, int P, cudaStream_t stream);
 int rowstats_parts(int64_t n, int64_t t);
+// Staging of a chunk's n variables by 2-D TMA boxes of <= 256 rows: n <= 256
+// is one box of exactly n rows; wider data takes ceil(n / 256) boxes of equal
+// height (a multiple of 8 rows, so every box starts 1024-byte aligned for the
+// 128-byte swizzle).  The ones row follows the staged rows.
+__host__ __device__ inline int xbox_count(int n) { return (n + 255) / 256; }
+__host__ __device__ inline int xbox_rows(int n) {
+  if (n <= 256) return n;
+  const int nb = xbox_count(n);
+  return ((n + nb - 1) / nb + 7) / 8 * 8;
+}
+__host__ __device__ inline int xstaged_rows(int n) { return xbox_count(n) * xbox_rows(n); }
+
 // padded sample count of the transposed layout the moment kernel reads
 inline int64_t padded_t(int64_t t) { return (t + 15) / 16 * 16; }
 cudaError_t launch_div(int64_t len, const double *x, double d, double *out, cudaStream_t stream);

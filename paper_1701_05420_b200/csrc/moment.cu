@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
   constexpr int LDK = SH::LDK, MT = SH::MT, NT = SH::NT;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int n = a.n;
-  const int xrows = (n + 1 + 7) / 8 * 8;               // n variables + the ones row, 1024-byte stages
+  const int xstaged = xstaged_rows(n);                 // TMA-staged variable rows (>= n)
+  const int xrows = (xstaged + 1 + 7) / 8 * 8;         // + the ones row, 1024-byte stages
   double *xs = reinterpret_cast<double *>(smem_raw);   // [2][xrows][16], swizzled
   double *kra = xs + 2 * xrows * LDX;                  // [2][TM][LDK]
   double *krb = kra + 2 * TM * LDK;                    // [2][TN][LDK]
@@ -186,10 +187,10 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
     for (int q = 0; q < 8; ++q) {
       int ca = (okA && q < a.h) ? a.rowcols[grow * a.h + q] : 0;
       int cb = (okB && q < a.r) ? a.colcols[gcol * a.r + q] : 0;
-      colA[q] = ca < 0 ? n : ca;  // -1: the ones row
-      colB[q] = cb < 0 ? n : cb;
-      BCG_CHECK(colA[q] >= 0 && colA[q] <= n, "colA", colA[q]);
-      BCG_CHECK(colB[q] >= 0 && colB[q] <= n, "colB", colB[q]);
+      colA[q] = ca < 0 ? xstaged : ca;  // -1: the ones row
+      colB[q] = cb < 0 ? xstaged : cb;
+      BCG_CHECK(colA[q] >= 0 && colA[q] <= xstaged, "colA", colA[q]);
+      BCG_CHECK(colB[q] >= 0 && colB[q] <= xstaged, "colB", colB[q]);
     }
   }
 
@@ -199,17 +200,19 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // the ones rows of both stages (all ones: the swizzle does not matter)
-  for (int k = tid; k < 2 * LDX; k += kThreads) xs[(k / LDX) * xrows * LDX + n * LDX + (k % LDX)] = 1.0;
+  for (int k = tid; k < 2 * LDX; k += kThreads) xs[(k / LDX) * xrows * LDX + xstaged * LDX + (k % LDX)] = 1.0;
   __syncthreads();
 
   // thread 0 stages chunk c: one 2-D tensor copy per 256 variables
   auto issue = [&](int c) {
     if (tid == 0) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      mbar_expect(&bar[c & 1], (uint32_t)(n * KC * sizeof(double)));
+      // every box transfers its full height (rows past n are zero-filled)
+      mbar_expect(&bar[c & 1], (uint32_t)(xstaged * KC * sizeof(double)));
       double *dst = xs + (c & 1) * xrows * LDX;
       const int s0 = (int)(sbeg + (int64_t)c * KC);
-      for (int v0 = 0; v0 < n; v0 += 256) tma_load_2d(dst + v0 * LDX, &tmap, s0, v0, &bar[c & 1]);
+      const int bh = xbox_rows(n);
+      for (int v0 = 0; v0 < xstaged; v0 += bh) tma_load_2d(dst + v0 * LDX, &tmap, s0, v0, &bar[c & 1]);
     }
   };
 
@@ -364,7 +367,7 @@ __global__ void k_reduce_slices(const double *__restrict__ ws, int nslices, int6
 }
 
 size_t moment_smem_bytes(int KC, int n, int tm, int tn) {
-  const size_t xrows = (size_t)(n + 1 + 7) / 8 * 8;
+  const size_t xrows = (size_t)(xstaged_rows(n) + 1 + 7) / 8 * 8;
   return sizeof(double) * (2 * xrows * KC + 2 * (size_t)(tm + tn) * KC) + 2 * sizeof(uint64_t) +
          1024;  // + alignment slack for the 1024-byte swizzle atoms
 }
@@ -439,7 +442,7 @@ static cudaError_t make_xt_map(const MomentArgs &a, CUtensorMap *map) {
   if (!enc) return cudaErrorNotSupported;
   cuuint64_t dims[2] = {(cuuint64_t)a.ldx, (cuuint64_t)a.n};
   cuuint64_t strides[1] = {(cuuint64_t)a.ldx * sizeof(double)};
-  cuuint32_t box[2] = {16, (cuuint32_t)(a.n < 256 ? a.n : 256)};
+  cuuint32_t box[2] = {16, (cuuint32_t)xbox_rows(a.n)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(a.x), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,

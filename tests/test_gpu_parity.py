@@ -634,3 +634,15 @@ def test_two_ranks_on_one_gpu_over_gloo(t, n, m, b, tmp_path, rng):
             want = cs[k].packed_host()
             np.testing.assert_allclose(got[f"c{k}"], want, rtol=1e-9, atol=1e-12)
             np.testing.assert_array_equal(got[f"d{k}"], want)
+
+
+@pytest.mark.parametrize("n,m,b,t", [(300, 2, 7, 700), (600, 2, 16, 300), (260, 3, 5, 300), (513, 2, 1, 200), (257, 4, 64, 100),
+                                     (700, 2, 50, 150)])
+def test_wide_data_matrices(n, m, b, t, rng):
+    """n > 256 variables: the chunk is staged by several 2-D TMA boxes (256
+    variables each) -- moments and cumulants against the oracle."""
+    x = rng.standard_normal((t, n)) + rng.exponential(1.0, (t, n))
+    np.testing.assert_allclose(packed(bcg.moment(x, m, b)), orc.moment(x, m, b), rtol=1e-12, atol=1e-12)
+    cs = bcg.cumulants_upto(x, m, b=b)
+    _, want = orc.cumulants_upto(x, m, b)
+    np.testing.assert_allclose(packed(cs[m]), want[m], rtol=1e-9, atol=1e-12)
