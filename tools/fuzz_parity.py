@@ -34,14 +34,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", type=int, default=200)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--wide", action="store_true", help="wide matrices: n up to 400 (m=2), 120 (m=3), 40 (m=4)")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     fails = 0
     t0 = time.time()
     for case in range(a.cases):
-        m = int(rng.integers(2, 9))
-        b = int(rng.integers(1, 9))
-        n = int(rng.integers(1, {2: 70, 3: 40, 4: 24, 5: 14, 6: 10, 7: 7, 8: 5}[m]))
+        m = int(rng.integers(2, 5 if a.wide else 9))
+        b = int(rng.integers(1, 17 if a.wide else 9))
+        nmax = {2: 400, 3: 120, 4: 40} if a.wide else {2: 70, 3: 40, 4: 24, 5: 14, 6: 10, 7: 7, 8: 5}
+        n = int(rng.integers(1, nmax[m]))
         # a quarter of the cases span several 16384-sample split-K slices
         t = int(rng.integers(2, 3000)) if rng.random() < 0.75 or m > 4 else int(rng.integers(16000, 70000))
         x = draw(rng, t, n)
