@@ -133,7 +133,11 @@ def cumulant(x_centered, m: int, lower: Sequence[BlockSymTensor], b: int = 2,
         return _moment_device(X, m, b)
     _lower_by_order(lower, range(2, m - 1))
     result = _moment_device(X, m, b)
-    _recursion_inplace(result, lower)
+    # m >= 6: the factored recursion needs the central moments M_4..M_{m-2}
+    # of the complement; they are lower-order GEMMs (cheap next to M_m) and
+    # replace the partition-sum kernel (bc/cumulants.py:119-136 either way)
+    central = {k: _moment_device(X, k, b).data for k in range(4, m - 1)} if m >= 6 else None
+    _recursion_inplace(result, lower, central)
     return result
 
 

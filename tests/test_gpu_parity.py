@@ -646,3 +646,18 @@ def test_wide_data_matrices(n, m, b, t, rng):
     cs = bcg.cumulants_upto(x, m, b=b)
     _, want = orc.cumulants_upto(x, m, b)
     np.testing.assert_allclose(packed(cs[m]), want[m], rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("n,m,b,t", [(9, 6, 3, 700), (8, 6, 2, 500), (6, 7, 2, 400), (10, 5, 4, 600)])
+def test_single_order_cumulant_api_matches_oracle(n, m, b, t, rng):
+    """cumulant(x_centered, m, lower) (bc/cumulants.py:119-136) with the lower
+    cumulants from cumulants_upto: the factored recursion (central moments
+    computed on the fly for m >= 6) against the oracle and against
+    cumulants_upto's own C_m."""
+    x = rng.exponential(1.0, (t, n)) + rng.standard_normal((t, n))
+    cs = bcg.cumulants_upto(x, m, b=b)
+    xc = bcg.center(x)
+    got = bcg.cumulant(xc, m, [cs[k] for k in range(2, m - 1)], b=b)
+    _, want = orc.cumulants_upto(x, m, b)
+    np.testing.assert_allclose(packed(got), want[m], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(packed(got), packed(cs[m]), rtol=1e-9, atol=1e-12)
