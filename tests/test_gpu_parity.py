@@ -636,7 +636,7 @@ def test_two_ranks_on_one_gpu_over_gloo(t, n, m, b, tmp_path, rng):
             np.testing.assert_array_equal(got[f"d{k}"], want)
 
 
-@pytest.mark.parametrize("n,m,b,t", [(300, 2, 7, 700), (600, 2, 16, 300), (260, 3, 5, 300), (513, 2, 1, 200), (257, 4, 64, 100),
+@pytest.mark.parametrize("n,m,b,t", [(300, 2, 7, 700), (600, 2, 16, 300), (260, 3, 5, 300), (513, 2, 1, 200), (257, 3, 32, 100),
                                      (700, 2, 50, 150)])
 def test_wide_data_matrices(n, m, b, t, rng):
     """n > 256 variables: the chunk is staged by several 2-D TMA boxes (256
