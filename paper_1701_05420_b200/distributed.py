@@ -96,9 +96,14 @@ class CudaOps:
         rest of the buffer stays zero)."""
         from . import _native
 
+        from .moments import WIDE_N, _moment_raw_wide
+
         xt, t = centered
         n, ldt = xt.shape
         out = torch.zeros(layout(n, k, b).size, dtype=torch.float64, device=xt.device)
+        if n > WIDE_N:
+            _moment_raw_wide(xt, t, k, b, out, key_range)
+            return out
         plan = _native.plan(n, k, b)
         wsb = plan.ws_bytes(t)
         ws = torch.empty(wsb, dtype=torch.uint8, device=xt.device) if wsb else None

@@ -106,10 +106,67 @@ def center(x):
 # -- moments ---------------------------------------------------------------------
 
 
+# The moment kernel stages a sample chunk of ALL variables in shared memory,
+# which bounds n (K2).  Wider data is decomposed by variable groups:
+# the key set splits by which groups its blocks fall in; every set S of at
+# most m groups is one sub-problem over the columns of S's blocks (<= WIDE_N
+# variables), whose keys that touch exactly the groups of S are scattered into
+# the global packed buffer.  Per element the products, their association and
+# the sample order are those of a kernel launch over the sub-matrix, so the
+# result is deterministic and the same for every caller (moment, cumulants_upto,
+# the multi-GPU paths) -- the bitwise invariants hold.
+WIDE_N = 720
+
+
+def _moment_raw_wide(xt, t: int, m: int, b: int, out, key_range=None) -> None:
+    """Accumulate packed RAW order-m sums of the transposed data xt (n > WIDE_N)
+    into out, via variable-group sub-problems (keys in ``key_range`` only)."""
+    import itertools
+
+    torch = _native.torch_cuda()
+    n = xt.shape[0]
+    nb = -(-n // b)
+    gsz = WIDE_N // (m * b)
+    if gsz < 1:
+        raise ValidationError(f"block size b={b} too large for order {m} on {n} variables "
+                              f"(m * b must be <= {WIDE_N})")
+    groups = [list(range(g0 + 1, min(nb, g0 + gsz) + 1)) for g0 in range(0, nb, gsz)]
+    glay = layout(n, m, b)
+    k0, k1 = (0, glay.K) if key_range is None else (int(key_range[0]), int(key_range[1]))
+    for size in range(1, m + 1):
+        for S in itertools.combinations(range(len(groups)), size):
+            blocks = [j for g in S for j in groups[g]]          # ascending global block ids
+            group_of = {j: g for g in S for j in groups[g]}
+            cols = np.concatenate([np.arange((j - 1) * b, min(j * b, n)) for j in blocks])
+            sub_n = len(cols)
+            slay = layout(sub_n, m, b)
+            keep_src, keep_dst = [], []
+            for sk, skey in enumerate(slay.keys):
+                gkey = tuple(blocks[s - 1] for s in skey)
+                if len({group_of[j] for j in gkey}) != size:
+                    continue  # computed by the sub-problem of fewer groups
+                gk = glay.key_index(gkey)
+                if not k0 <= gk < k1:
+                    continue
+                keep_src.append(np.arange(slay.offs[sk], slay.offs[sk + 1]))
+                keep_dst.append(np.arange(glay.offs[gk], glay.offs[gk + 1]))
+            if not keep_src:
+                continue
+            sub_xt = xt[torch.from_numpy(cols).to(xt.device)]
+            sub = torch.zeros(slay.size, dtype=torch.float64, device=xt.device)
+            _moment_raw_t_into(sub_xt, t, m, b, sub)
+            src = torch.from_numpy(np.concatenate(keep_src)).to(xt.device)
+            dst = torch.from_numpy(np.concatenate(keep_dst)).to(xt.device)
+            out.index_put_((dst,), sub[src], accumulate=True)  # unique targets: deterministic
+
+
 def _moment_raw_into(X, m: int, b: int, out, key_range=None) -> None:
     """Accumulate packed RAW order-m sums of X into out (bcg_moment_raw)."""
     torch = _native.torch_cuda()
     t, n = X.shape
+    if n > WIDE_N:
+        _moment_raw_wide(_center_transposed(X, None), t, m, b, out, key_range)
+        return
     plan = _native.plan(n, m, b)
     wsb = plan.ws_bytes(t)
     ws = torch.empty(wsb, dtype=torch.uint8, device=X.device) if wsb else None
@@ -154,6 +211,9 @@ def _moment_raw_t_into(xt, t: int, m: int, b: int, out) -> None:
     """Accumulate packed RAW order-m sums from the transposed layout."""
     torch = _native.torch_cuda()
     n, ldt = xt.shape
+    if n > WIDE_N:
+        _moment_raw_wide(xt, t, m, b, out)
+        return
     plan = _native.plan(n, m, b)
     wsb = plan.ws_bytes(t)
     ws = torch.empty(wsb, dtype=torch.uint8, device=xt.device) if wsb else None

@@ -661,3 +661,19 @@ def test_single_order_cumulant_api_matches_oracle(n, m, b, t, rng):
     _, want = orc.cumulants_upto(x, m, b)
     np.testing.assert_allclose(packed(got), want[m], rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(packed(got), packed(cs[m]), rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("n,m,b,t", [(800, 2, 4, 300), (1500, 2, 1, 200), (760, 3, 40, 150), (731, 2, 731, 100)])
+def test_wider_than_one_stage(n, m, b, t, rng):
+    """n > 720 variables (one sample chunk of all of them no longer fits the
+    kernel's shared-memory stage): the variable-group decomposition against
+    the oracle, and bitwise consistent between moment() and cumulants_upto()."""
+    x = rng.standard_normal((t, n)) + rng.exponential(1.0, (t, n))
+    if b > 720 // m:
+        with pytest.raises(bcg.ValidationError, match="too large"):
+            bcg.moment(x, m, b)
+        return
+    got = packed(bcg.moment(x, m, b))
+    np.testing.assert_allclose(got, orc.moment(x, m, b), rtol=1e-12, atol=1e-12)
+    cs = bcg.cumulants_upto(x, m, b=b)
+    np.testing.assert_array_equal(packed(cs[m]), packed(bcg.moment(bcg.center(x), m, b)))
