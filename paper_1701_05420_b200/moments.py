@@ -118,6 +118,34 @@ def center(x):
 WIDE_N = 720
 
 
+def _multiset_ranks(keys: np.ndarray, N: int) -> np.ndarray:
+    """Lexicographic rank of sorted 1-based keys (rows) among all size-m
+    multisets over 1..N: sum over positions of the multisets that branch off
+    below (hockey-stick sums of C(N - v + L, L))."""
+    K, m = keys.shape
+    comb = np.zeros((N + m + 2, m + 1), dtype=np.int64)
+    cap = 1 << 62  # entries this large are never reached by a layout that fits in memory
+    for a in range(N + m + 2):
+        comb[a, 0] = 1
+        for k in range(1, min(a, m) + 1):
+            comb[a, k] = min(cap, int(comb[a - 1, k - 1]) + int(comb[a - 1, k]))
+    rank = np.zeros(K, dtype=np.int64)
+    prev = np.ones(K, dtype=np.int64)
+    for q in range(m):
+        L = m - q - 1
+        j = keys[:, q]
+        rank += comb[N - prev + L + 1, L + 1] - comb[N - j + L + 1, L + 1]
+        prev = j
+    return rank
+
+
+def _ranges(starts: np.ndarray, lengths: np.ndarray) -> np.ndarray:
+    """Concatenation of arange(s, s + l) over (s, l) pairs."""
+    total = int(lengths.sum())
+    first = np.repeat(np.cumsum(lengths) - lengths, lengths)
+    return np.repeat(starts, lengths) + (np.arange(total, dtype=np.int64) - first)
+
+
 def _moment_raw_wide(xt, t: int, m: int, b: int, out, key_range=None) -> None:
     """Accumulate packed RAW order-m sums of the transposed data xt (n > WIDE_N)
     into out, via variable-group sub-problems (keys in ``key_range`` only)."""
@@ -130,33 +158,31 @@ def _moment_raw_wide(xt, t: int, m: int, b: int, out, key_range=None) -> None:
     if gsz < 1:
         raise ValidationError(f"block size b={b} too large for order {m} on {n} variables "
                               f"(m * b must be <= {WIDE_N})")
-    groups = [list(range(g0 + 1, min(nb, g0 + gsz) + 1)) for g0 in range(0, nb, gsz)]
-    glay = layout(n, m, b)
-    k0, k1 = (0, glay.K) if key_range is None else (int(key_range[0]), int(key_range[1]))
+    groups = [np.arange(g0 + 1, min(nb, g0 + gsz) + 1) for g0 in range(0, nb, gsz)]
+    goffs = layout(n, m, b).offs
+    k0, k1 = (0, len(goffs) - 1) if key_range is None else (int(key_range[0]), int(key_range[1]))
     for size in range(1, m + 1):
         for S in itertools.combinations(range(len(groups)), size):
-            blocks = [j for g in S for j in groups[g]]          # ascending global block ids
-            group_of = {j: g for g in S for j in groups[g]}
+            blocks = np.concatenate([groups[g] for g in S])          # ascending global block ids
+            group_of = np.concatenate([np.full(len(groups[g]), i) for i, g in enumerate(S)])
             cols = np.concatenate([np.arange((j - 1) * b, min(j * b, n)) for j in blocks])
-            sub_n = len(cols)
-            slay = layout(sub_n, m, b)
-            keep_src, keep_dst = [], []
-            for sk, skey in enumerate(slay.keys):
-                gkey = tuple(blocks[s - 1] for s in skey)
-                if len({group_of[j] for j in gkey}) != size:
-                    continue  # computed by the sub-problem of fewer groups
-                gk = glay.key_index(gkey)
-                if not k0 <= gk < k1:
-                    continue
-                keep_src.append(np.arange(slay.offs[sk], slay.offs[sk + 1]))
-                keep_dst.append(np.arange(glay.offs[gk], glay.offs[gk + 1]))
-            if not keep_src:
+            slay = layout(len(cols), m, b)
+            skeys = np.asarray(slay.keys, dtype=np.int64).reshape(-1, m)
+            gkeys = blocks[skeys - 1]
+            # keys touching every group of S (fewer: another sub-problem's)
+            gsets = np.sort(group_of[skeys - 1], axis=1)
+            ndist = 1 + (np.diff(gsets, axis=1) != 0).sum(axis=1)
+            gk = _multiset_ranks(gkeys, nb)
+            keep = (ndist == size) & (gk >= k0) & (gk < k1)
+            if not keep.any():
                 continue
+            sk = np.nonzero(keep)[0]
+            lengths = slay.offs[sk + 1] - slay.offs[sk]
+            src = torch.from_numpy(_ranges(slay.offs[sk], lengths)).to(xt.device)
+            dst = torch.from_numpy(_ranges(goffs[gk[keep]], lengths)).to(xt.device)
             sub_xt = xt[torch.from_numpy(cols).to(xt.device)]
             sub = torch.zeros(slay.size, dtype=torch.float64, device=xt.device)
             _moment_raw_t_into(sub_xt, t, m, b, sub)
-            src = torch.from_numpy(np.concatenate(keep_src)).to(xt.device)
-            dst = torch.from_numpy(np.concatenate(keep_dst)).to(xt.device)
             out.index_put_((dst,), sub[src], accumulate=True)  # unique targets: deterministic
 
 

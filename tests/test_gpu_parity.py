@@ -677,3 +677,4 @@ def test_wider_than_one_stage(n, m, b, t, rng):
     np.testing.assert_allclose(got, orc.moment(x, m, b), rtol=1e-12, atol=1e-12)
     cs = bcg.cumulants_upto(x, m, b=b)
     np.testing.assert_array_equal(packed(cs[m]), packed(bcg.moment(bcg.center(x), m, b)))
+    np.testing.assert_array_equal(packed(bcg.moment_parallel_blocks(x, m, b, p=3)), got)
