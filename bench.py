@@ -48,12 +48,16 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=0, help="rows of the CPU baseline sample (0 = auto)")
+    ap.add_argument("--t", type=int, default=0,
+                    help="rows per GPU instead of the config's t (exploration only: the line then says so; "
+                         "e.g. cfg5 at its BASELINE t=4e6 takes ~13 min per step on one B200)")
     return ap.parse_args()
 
 
 def config_dict(cfg, t_total, world):
+    note = "" if t_total == cfg.t * world else f"; t overridden, BASELINE t={cfg.t} per GPU"
     return {
-        "workload": f"{cfg.name}: cumulants_upto C1..C{cfg.m}, t={t_total} x n={cfg.n}, b={cfg.b} ({cfg.desc})",
+        "workload": f"{cfg.name}: cumulants_upto C1..C{cfg.m}, t={t_total} x n={cfg.n}, b={cfg.b} ({cfg.desc}){note}",
         "t": t_total, "n": cfg.n, "b": cfg.b, "m_max": cfg.m,
         "parallelism": f"t-shard x{world}" if world > 1 else "single GPU",
         "l2": "inputs larger than L2 (X = %.0f MB per GPU vs 126 MB L2)" % (cfg.t * cfg.n * 8 / 1e6),
@@ -245,7 +249,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    t_local = cfg.t
+    t_local = args.t or cfg.t
     t_total = t_local * world
     x_host = workloads.generate(cfg.name, t_local, shard=rank)
     X = torch.from_numpy(x_host).cuda()
