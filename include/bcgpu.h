@@ -70,19 +70,29 @@ int bcg_moment_blocks(const double *xt, int64_t n, int64_t t,
  * ------------------------------------------------------------------------- */
 typedef struct bcg_plan bcg_plan;
 
+/* Symmetric plan (the default): inside a block whose key repeats a block
+ * index j (e.g. key (1,1,2,...)), the elements whose in-block digits differ
+ * only by a permutation within that run are equal (the moment tensor is
+ * super-symmetric).  The moment GEMM then produces only the elements whose
+ * digits are non-decreasing within the runs of its row / column tuple and a
+ * fill pass copies the sorted element to its permutations (K2):
+ * 58% of the stored elements at order 6 (cfg4, cfg5), 70% at order 4 (cfg2).
+ * Every stored element is still written; accumulate semantics hold for an
+ * `out` that is already symmetric within blocks (e.g. zero).  The reference
+ * computes every stored element directly (bc/_core.pyx:60-123); values agree
+ * to rounding (the permuted products are formed in another order). */
 int bcg_plan_create(int64_t n, int32_t m, int32_t b, bcg_plan **plan);
 /* Same with an explicit moment-kernel variant (-1 = default, 0 = the DMMA
  * kernel of DESIGN.md K2; other values are rejected). */
 int bcg_plan_create_ex(int64_t n, int32_t m, int32_t b, int32_t variant,
                        bcg_plan **plan);
-/* Fused multi-order plan: ONE staircase GEMM over the block alphabet extended
- * by a constant "ones" block yields the raw sums of every order 2..m (a key
- * with z ones is the order-(m - z) key of its other entries) -- a single pass
- * over X for cumulants_upto's moments (bc/cumulants.py:187-192 computes one
- * moment per order).  bcg_moment_raw on it accumulates into a buffer of
- * S_2 + ... + S_m elements, order o's packed tensor at order_base[o]
- * (bcg_plan_output).  host_only != 0: tables only (layout / selfcheck). */
-int bcg_plan_create_fused(int64_t n, int32_t m, int32_t b, int32_t host_only,
+/* Plan flags: BCG_PLAN_FULL -- the moment GEMM produces every stored element
+ * directly, element-wise accumulate semantics for any prior `out` (what the
+ * drop-in bcg_moment_blocks uses); BCG_PLAN_HOST -- tables only, nothing
+ * uploaded (layout queries / selfcheck without a GPU). */
+#define BCG_PLAN_FULL 1
+#define BCG_PLAN_HOST 2
+int bcg_plan_create_flags(int64_t n, int32_t m, int32_t b, int32_t flags,
                           bcg_plan **plan);
 /* Moment-kernel choice of the plan: variant (0 = v1), CTA tile tm x tn of
  * its first GEMM (picked per GEMM by the staircase tile model) and the number
@@ -95,17 +105,19 @@ int bcg_plan_kernel(const bcg_plan *plan, int32_t *variant, int32_t *tm,
  * tn and *ntiles; pass i < 0 to query only *ngemm and *split_T. */
 int bcg_plan_gemm(const bcg_plan *plan, int32_t i, int32_t *ngemm, int32_t *split_T,
                   int32_t *info, int64_t *ntiles);
-/* Output size of bcg_moment_raw on this plan (S_m, or S_2 + ... + S_m for a
- * fused plan) and, if order_base != NULL (m + 2 entries), each order's start
- * offset in it (fused plans; zeros otherwise, order_base[m + 1] = S_out). */
-int bcg_plan_output(const bcg_plan *plan, int64_t *S_out, int64_t *order_base);
+/* Output size of bcg_moment_raw on this plan (S_m) and the number of
+ * elements its GEMMs compute (S_m for a full plan, fewer for a symmetric one:
+ * 2 * t * produced is the FP64 work the DMMA kernel executes). */
+int bcg_plan_output(const bcg_plan *plan, int64_t *S_out, int64_t *produced);
 /* Host-only plan (tables built, nothing uploaded): layout queries work
  * without a GPU; compute calls on it fail with BCG_EINVAL. */
 int bcg_plan_create_host(int64_t n, int32_t m, int32_t b, bcg_plan **plan);
 int bcg_plan_destroy(bcg_plan *plan);
-/* Host-side verification of the moment GEMM mapping: every stored element of
- * order m is produced by exactly one (tile, row, col) and reads exactly the
- * data columns of its (key, offsets).  BCG_OK or BCG_EINVAL with a message. */
+/* Host-side verification of the moment GEMM mapping: every element the GEMMs
+ * produce comes from exactly one (tile, row, col) and reads exactly the data
+ * columns of its (key, offsets); every stored element is produced or (symmetric
+ * plan) is a within-run permutation of a produced one in a fill-listed block.
+ * BCG_OK or BCG_EINVAL with a message. */
 int bcg_plan_selfcheck(const bcg_plan *plan);
 /* K = number of stored blocks, S = stored elements (offs[K]) of order `order`
  * (1 <= order <= m). */
@@ -114,8 +126,12 @@ int bcg_plan_sizes(const bcg_plan *plan, int32_t order, int64_t *K, int64_t *S);
  * order; offs: K+1) into caller HOST buffers (bc/_engines.py:46-54). */
 int bcg_plan_layout(const bcg_plan *plan, int32_t order, int64_t *keys,
                     int64_t *col0, int64_t *edges, int64_t *offs);
-/* Workspace bytes bcg_moment_raw needs for t samples (0 = none). */
+/* Workspace bytes bcg_moment_raw(_range) needs for t samples (0 = none):
+ * the transposed copy of x plus the split-K partials. */
 int bcg_moment_ws_bytes(const bcg_plan *plan, int64_t t, size_t *bytes);
+/* Workspace bytes of the transposed-input entries bcg_moment_raw_t(_range):
+ * the split-K partials only. */
+int bcg_moment_t_ws_bytes(const bcg_plan *plan, int64_t t, size_t *bytes);
 
 /* ---------------------------------------------------------------------------
  * Column statistics of x (t x n row-major, leading dimension ldx >= n):
@@ -147,7 +163,7 @@ int bcg_moment_raw(const bcg_plan *plan, const double *x, int64_t t,
 /* Same from the TRANSPOSED layout the reference's own kernel takes
  * (bc/_engines.py:95): xt has n rows of stride ldt (even, >= bcg_padded_t(t)),
  * 16-byte aligned, zero-padded in [t, ldt).  No transpose pass; `ws` needs
- * only the split-K part (bcg_moment_ws_bytes is always enough). */
+ * bcg_moment_t_ws_bytes(plan, t) bytes (the split-K partials). */
 int bcg_moment_raw_t(const bcg_plan *plan, const double *xt, int64_t t,
                      int64_t ldt, double *out, void *ws, size_t ws_bytes,
                      void *stream);

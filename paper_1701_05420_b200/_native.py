@@ -35,8 +35,8 @@ SIGNATURES = [
     ("bcg_moment_blocks", ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp]),
     ("bcg_plan_create", ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(_vp)]),
     ("bcg_plan_create_ex", ctypes.c_int, [_i64, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
-    ("bcg_plan_create_fused", ctypes.c_int, [_i64, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
-    ("bcg_plan_output", ctypes.c_int, [_vp, ctypes.POINTER(_i64), _vp]),
+    ("bcg_plan_create_flags", ctypes.c_int, [_i64, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
+    ("bcg_plan_output", ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     ("bcg_plan_kernel", ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                                        ctypes.POINTER(_i64)]),
     ("bcg_plan_gemm", ctypes.c_int, [_vp, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32), _vp,
@@ -47,6 +47,7 @@ SIGNATURES = [
     ("bcg_plan_sizes", ctypes.c_int, [_vp, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     ("bcg_plan_layout", ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp]),
     ("bcg_moment_ws_bytes", ctypes.c_int, [_vp, _i64, ctypes.POINTER(_sz)]),
+    ("bcg_moment_t_ws_bytes", ctypes.c_int, [_vp, _i64, ctypes.POINTER(_sz)]),
     ("bcg_colstats", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     ("bcg_colstats_ws_bytes", _sz, [_i64, _i64]),
     ("bcg_center", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
@@ -124,22 +125,26 @@ def ptr(tensor) -> int:
     return tensor.data_ptr()
 
 
+PLAN_FULL = 1  # BCG_PLAN_FULL: every stored element computed directly
+PLAN_HOST = 2  # BCG_PLAN_HOST: tables only
+
+
 class Plan:
-    """Host-built index tables for one (n, m, b) (bcg_plan_create)."""
+    """Host-built index tables for one (n, m, b) (bcg_plan_create_flags).
+    ``full``: the moment GEMM computes every stored element directly instead
+    of the sorted ones within runs of equal block indices plus the fill."""
 
     def __init__(self, n: int, m: int, b: int, host_only: bool = False, variant: int = -1,
-                 fused: bool = False):
+                 full: bool = False):
         self.n, self.m, self.b = int(n), int(m), int(b)
         self.host_only = host_only
         self.variant = int(variant)
-        self.fused = bool(fused)
+        self.full = bool(full)
+        if self.variant > 0:
+            raise ValidationError(f"unknown moment kernel variant {self.variant}")
         h = _vp()
-        if fused:
-            check(lib().bcg_plan_create_fused(self.n, self.m, self.b, int(host_only), ctypes.byref(h)), "plan")
-        elif host_only:
-            check(lib().bcg_plan_create_host(self.n, self.m, self.b, ctypes.byref(h)), "plan")
-        else:
-            check(lib().bcg_plan_create_ex(self.n, self.m, self.b, self.variant, ctypes.byref(h)), "plan")
+        flags = (PLAN_FULL if full else 0) | (PLAN_HOST if host_only else 0)
+        check(lib().bcg_plan_create_flags(self.n, self.m, self.b, flags, ctypes.byref(h)), "plan")
         self._h = h
         self._lib = lib()
 
@@ -164,12 +169,11 @@ class Plan:
         return keys, col0, edges, offs
 
     def output(self):
-        """(S_out, order_base): output size of bcg_moment_raw and, for a fused
-        plan, each order's offset in it."""
-        S = _i64()
-        base = np.zeros(self.m + 2, dtype=np.int64)
-        check(self._lib.bcg_plan_output(self._h, ctypes.byref(S), base.ctypes.data))
-        return S.value, base
+        """(S_out, produced): output size of bcg_moment_raw and the number of
+        elements the moment GEMMs compute (S_out for a full plan)."""
+        S, prod = _i64(), _i64()
+        check(self._lib.bcg_plan_output(self._h, ctypes.byref(S), ctypes.byref(prod)))
+        return S.value, prod.value
 
     def kernel(self):
         """(variant, tm, tn, ntiles) of the moment GEMM this plan launches."""
@@ -190,8 +194,15 @@ class Plan:
         return T.value, out
 
     def ws_bytes(self, t: int) -> int:
+        """Workspace of the row-major entries (transposed copy + split-K)."""
         out = _sz()
         check(self._lib.bcg_moment_ws_bytes(self._h, int(t), ctypes.byref(out)))
+        return out.value
+
+    def t_ws_bytes(self, t: int) -> int:
+        """Workspace of the transposed-input entries (split-K partials only)."""
+        out = _sz()
+        check(self._lib.bcg_moment_t_ws_bytes(self._h, int(t), ctypes.byref(out)))
         return out.value
 
     def __del__(self):
@@ -213,17 +224,22 @@ def moment_variant() -> int:
     return int(v) if v.strip() else -1
 
 
-def plan(n: int, m: int, b: int, fused: bool = False) -> Plan:
-    """Cached device plan for (n, m, b), the current kernel variant and
-    whether it is the fused multi-order plan."""
+def full_blocks() -> bool:
+    """$BCG_MOMENT_FULL=1: plans compute every stored element directly (A/B knob)."""
+    return os.environ.get("BCG_MOMENT_FULL", "0") not in ("", "0")
+
+
+def plan(n: int, m: int, b: int, full: bool | None = None) -> Plan:
+    """Cached device plan for (n, m, b) and the current kernel knobs."""
     torch = torch_cuda()
+    full = full_blocks() if full is None else bool(full)
     # plans hold device tables: one per (device, n, m, b, kernel knobs)
-    key = (torch.cuda.current_device(), int(n), int(m), int(b), -1 if fused else moment_variant(), bool(fused),
+    key = (torch.cuda.current_device(), int(n), int(m), int(b), moment_variant(), full,
            os.environ.get("BCG_TILE", ""), os.environ.get("BCG_NO_HYBRID", ""))
     with _lock:
         p = _plans.get(key)
         if p is None:
-            p = _plans[key] = Plan(key[1], key[2], key[3], variant=key[4], fused=key[5])
+            p = _plans[key] = Plan(key[1], key[2], key[3], variant=key[4], full=full)
         return p
 
 

@@ -102,7 +102,6 @@ int run_moment(const bcg::Plan &p, const double *xt, int64_t t, int64_t ldt, dou
   a.ldx = ldt;
   a.n = (int)p.n;
   a.offs = p.d_koff;
-  a.ones = p.fused ? 1 : 0;
   a.nslices_total = sl.nslices;
   a.slice_len = sl.slice_len;
   a.out = out;
@@ -112,7 +111,7 @@ int run_moment(const bcg::Plan &p, const double *xt, int64_t t, int64_t ldt, dou
   a.kmax_sel = k1 - 1 >= INT32_MAX ? INT32_MAX : (int32_t)(k1 - 1);
   if (k0 == 0 && k1 >= p.lay[p.m].K) a.kmax_sel = INT32_MAX;
   const auto &offs = p.lay[p.m].offs;
-  const int64_t lo = p.fused ? 0 : offs[k0], hi = p.fused ? p.S_out : offs[k1];
+  const int64_t lo = offs[k0], hi = offs[k1];
   for (int g0 = 0; g0 < sl.nslices; g0 += sl.group) {
     a.slice0 = g0;
     a.nslices = std::min(sl.group, sl.nslices - g0);
@@ -147,6 +146,17 @@ int run_moment(const bcg::Plan &p, const double *xt, int64_t t, int64_t ldt, dou
       bcg::g_launches++;
     }
   }
+  if (p.sym && !p.fill_keys.empty()) {
+    // permuted copies inside blocks with repeated block indices
+    const auto f0 = std::lower_bound(p.fill_keys.begin(), p.fill_keys.end(), (int32_t)k0) - p.fill_keys.begin();
+    const auto f1 = std::lower_bound(p.fill_keys.begin(), p.fill_keys.end(), k1 > INT32_MAX ? INT32_MAX : (int32_t)k1) -
+                    p.fill_keys.begin();
+    if (f1 > f0) {
+      CUDA_TRY(bcg::launch_sym_fill(p.d_fill_keys + f0, f1 - f0, p.d_keys32, p.d_offs, p.m, p.b, p.n, out, stream),
+               "symmetric fill");
+      bcg::g_launches++;
+    }
+  }
   return BCG_OK;
 }
 
@@ -162,40 +172,21 @@ int bcg_version(void) { return 100; }
 int64_t bcg_launch_count(void) { return bcg::g_launches; }
 
 int bcg_plan_create(int64_t n, int32_t m, int32_t b, bcg_plan **plan) {
-  return bcg_plan_create_ex(n, m, b, -1, plan);
+  return bcg_plan_create_flags(n, m, b, 0, plan);
 }
 
 int bcg_plan_create_ex(int64_t n, int32_t m, int32_t b, int32_t variant, bcg_plan **plan) {
-  if (!plan) return fail(BCG_EINVAL, "plan pointer is NULL");
   if (variant > 0) return fail(BCG_EINVAL, "unknown moment kernel variant " + std::to_string(variant));
-  auto pl = std::make_unique<bcg_plan>();
-  std::string err = bcg::build_plan(n, m, b, pl->p, variant);
-  if (!err.empty()) return fail(BCG_EINVAL, err);
-  err = bcg::upload_plan(pl->p);
-  if (!err.empty()) {
-    bcg::free_plan(pl->p);
-    return fail(BCG_ECUDA, err);
-  }
-  *plan = pl.release();
-  return BCG_OK;
+  return bcg_plan_create_flags(n, m, b, 0, plan);
 }
 
-int bcg_plan_create_host(int64_t n, int32_t m, int32_t b, bcg_plan **plan) {
+int bcg_plan_create_flags(int64_t n, int32_t m, int32_t b, int32_t flags, bcg_plan **plan) {
   if (!plan) return fail(BCG_EINVAL, "plan pointer is NULL");
+  if (flags & ~(BCG_PLAN_FULL | BCG_PLAN_HOST)) return fail(BCG_EINVAL, "unknown plan flags");
   auto pl = std::make_unique<bcg_plan>();
-  std::string err = bcg::build_plan(n, m, b, pl->p);
+  std::string err = bcg::build_plan(n, m, b, pl->p, -1, !(flags & BCG_PLAN_FULL));
   if (!err.empty()) return fail(BCG_EINVAL, err);
-  *plan = pl.release();
-  return BCG_OK;
-}
-
-int bcg_plan_create_fused(int64_t n, int32_t m, int32_t b, int32_t host_only, bcg_plan **plan) {
-  if (!plan) return fail(BCG_EINVAL, "plan pointer is NULL");
-  if (m < 2 || m > 16) return fail(BCG_EINVAL, "kernel supports 2 <= m <= 16");
-  auto pl = std::make_unique<bcg_plan>();
-  std::string err = bcg::build_plan(n, m, b, pl->p, 0, true);
-  if (!err.empty()) return fail(BCG_EINVAL, err);
-  if (!host_only) {
+  if (!(flags & BCG_PLAN_HOST)) {
     err = bcg::upload_plan(pl->p);
     if (!err.empty()) {
       bcg::free_plan(pl->p);
@@ -204,6 +195,10 @@ int bcg_plan_create_fused(int64_t n, int32_t m, int32_t b, int32_t host_only, bc
   }
   *plan = pl.release();
   return BCG_OK;
+}
+
+int bcg_plan_create_host(int64_t n, int32_t m, int32_t b, bcg_plan **plan) {
+  return bcg_plan_create_flags(n, m, b, BCG_PLAN_HOST, plan);
 }
 
 int bcg_plan_kernel(const bcg_plan *plan, int32_t *variant, int32_t *tm, int32_t *tn, int64_t *ntiles) {
@@ -239,13 +234,11 @@ int bcg_plan_gemm(const bcg_plan *plan, int32_t i, int32_t *ngemm, int32_t *spli
   return BCG_OK;
 }
 
-int bcg_plan_output(const bcg_plan *plan, int64_t *S_out, int64_t *order_base) {
+int bcg_plan_output(const bcg_plan *plan, int64_t *S_out, int64_t *produced) {
   if (!plan) return fail(BCG_EINVAL, "plan is NULL");
   const bcg::Plan &p = plan->p;
   if (S_out) *S_out = p.S_out;
-  if (order_base)
-    for (int o = 0; o <= p.m + 1; ++o)
-      order_base[o] = p.fused ? (o < (int)p.order_base.size() ? p.order_base[o] : 0) : (o == p.m + 1 ? p.S_out : 0);
+  if (produced) *produced = p.m < 2 ? 0 : p.produced;
   return BCG_OK;
 }
 
@@ -254,7 +247,10 @@ int bcg_plan_selfcheck(const bcg_plan *plan) {
   const bcg::Plan &p = plan->p;
   if (p.m < 2) return BCG_OK;
   const int64_t S = p.S_out;
+  const int o = p.m;
+  const bcg::Layout &L = p.lay[o];
   std::vector<uint8_t> seen(S, 0);
+  int64_t count = 0;
   for (const bcg::Gemm &g : p.gemm)
   for (const bcg::Tile &tl : g.tiles) {
     for (int64_t r = tl.row0; r < std::min<int64_t>(tl.row0 + g.tm, g.R); ++r) {
@@ -262,41 +258,51 @@ int bcg_plan_selfcheck(const bcg_plan *plan) {
         if (c < g.row_cstart[r]) continue;
         const int64_t kg = g.row_keybase[r] + g.col_rank[c];
         if (kg < 0 || kg >= (int64_t)p.koff.size()) return fail(BCG_EINVAL, "selfcheck: key index out of range");
-        if (p.koff[kg] < 0) continue;  // fused: order 0 / 1 element
         const int64_t lin = (int64_t)g.row_olin[r] * g.col_size[c] + g.col_olin[c];
         const int64_t addr = p.koff[kg] + lin;
-        // locate (order, block) of addr and check the element's data columns
-        int o = p.m;
-        if (p.fused)
-          while (o > 2 && addr < p.order_base[o]) --o;
-        const bcg::Layout &L = p.lay[o];
-        const int64_t local = addr - (p.fused ? p.order_base[o] : 0);
-        const int64_t k = std::upper_bound(L.offs.begin(), L.offs.end(), local) - L.offs.begin() - 1;
-        if (k < 0 || k >= L.K || local >= L.offs[k + 1]) return fail(BCG_EINVAL, "selfcheck: offset outside block");
-        if (p.koff[kg] != (p.fused ? p.order_base[o] : 0) + L.offs[k])
-          return fail(BCG_EINVAL, "selfcheck: element outside its key's block");
+        const int64_t k = std::upper_bound(L.offs.begin(), L.offs.end(), addr) - L.offs.begin() - 1;
+        if (k < 0 || k >= L.K || addr >= L.offs[k + 1]) return fail(BCG_EINVAL, "selfcheck: offset outside block");
+        if (p.koff[kg] != L.offs[k]) return fail(BCG_EINVAL, "selfcheck: element outside its key's block");
         if (seen[addr]) return fail(BCG_EINVAL, "selfcheck: element produced twice");
         seen[addr] = 1;
-        int64_t rem = local - L.offs[k], cols[16];
+        ++count;
+        int64_t rem = addr - L.offs[k], cols[16];
         for (int q = o - 1; q >= 0; --q) {
           const int64_t e = L.edges[k * o + q];
           cols[q] = L.col0[k * o + q] + rem % e;
           rem /= e;
         }
-        // the GEMM element's columns, ones (-1) removed, must equal (key, offsets)'s
+        // the GEMM element's columns must equal (key, offsets)'s
         int64_t got[16], ng = 0;
-        for (int q = 0; q < g.h; ++q)
-          if (g.rowcols[r * g.h + q] >= 0) got[ng++] = g.rowcols[r * g.h + q];
-        for (int q = 0; q < g.r; ++q)
-          if (g.colcols[c * g.r + q] >= 0) got[ng++] = g.colcols[c * g.r + q];
+        for (int q = 0; q < g.h; ++q) got[ng++] = g.rowcols[r * g.h + q];
+        for (int q = 0; q < g.r; ++q) got[ng++] = g.colcols[c * g.r + q];
         if (ng != o) return fail(BCG_EINVAL, "selfcheck: order mismatch");
         for (int q = 0; q < o; ++q)
           if (got[q] != cols[q]) return fail(BCG_EINVAL, "selfcheck: column mismatch");
       }
     }
   }
-  for (int64_t i = 0; i < S; ++i)
-    if (!seen[i]) return fail(BCG_EINVAL, "selfcheck: element never produced");
+  if (count != p.produced) return fail(BCG_EINVAL, "selfcheck: produced-element count mismatch");
+  // every element must be produced, or (symmetric plan) be a permuted copy of
+  // a produced element with digits sorted within runs of equal block indices
+  for (int64_t k = 0; k < L.K; ++k) {
+    const int64_t *key = &L.keys[k * o];
+    const int64_t *e = &L.edges[k * o];
+    for (int64_t i = L.offs[k]; i < L.offs[k + 1]; ++i) {
+      if (seen[i]) continue;
+      if (!p.sym) return fail(BCG_EINVAL, "selfcheck: element never produced");
+      int64_t d[16], rem = i - L.offs[k];
+      for (int q = o - 1; q >= 0; --q) {
+        d[q] = rem % e[q];
+        rem /= e[q];
+      }
+      bool sorted = true;
+      for (int q = 1; q < o; ++q) sorted = sorted && !(key[q] == key[q - 1] && d[q] < d[q - 1]);
+      if (sorted) return fail(BCG_EINVAL, "selfcheck: sorted element never produced");
+      if (!std::binary_search(p.fill_keys.begin(), p.fill_keys.end(), (int32_t)k))
+        return fail(BCG_EINVAL, "selfcheck: block with permuted copies missing from the fill list");
+    }
+  }
   return BCG_OK;
 }
 
@@ -333,6 +339,12 @@ int bcg_moment_ws_bytes(const bcg_plan *plan, int64_t t, size_t *bytes) {
     return BCG_OK;
   }
   *bytes = xt_bytes_for(plan->p, t) + ws_bytes_for(plan->p, choose_slicing(plan->p, t));
+  return BCG_OK;
+}
+
+int bcg_moment_t_ws_bytes(const bcg_plan *plan, int64_t t, size_t *bytes) {
+  if (!plan || !bytes) return fail(BCG_EINVAL, "NULL argument");
+  *bytes = plan->p.m < 2 ? 0 : ws_bytes_for(plan->p, choose_slicing(plan->p, t));
   return BCG_OK;
 }
 
@@ -467,7 +479,9 @@ int bcg_moment_blocks(const double *xt, int64_t n, int64_t t, const int64_t *col
     auto it = g_cache.find(key);
     if (it == g_cache.end()) {
       bcg_plan *np = nullptr;
-      int rc = bcg_plan_create(n, (int32_t)m, (int32_t)b, &np);
+      // every element computed directly: the reference's per-element
+      // accumulate semantics for any prior content of `out`
+      int rc = bcg_plan_create_flags(n, (int32_t)m, (int32_t)b, BCG_PLAN_FULL, &np);
       if (rc) return rc;
       it = g_cache.emplace(key, std::unique_ptr<bcg_plan>(np)).first;
     }

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.h"
@@ -293,6 +294,68 @@ cudaError_t launch_rowstats(const double *xt, int64_t n, int64_t t, int64_t ldt,
     k_rowstats_final<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(ws, n, P, sums, sumsq);
     g_launches++;
   }
+  return cudaGetLastError();
+}
+
+// ---- symmetric plans: fill the permuted copies inside blocks with repeated
+// block indices.  The packed tensor is super-symmetric, so an element whose
+// in-block digits are not sorted within a run of equal block indices equals
+// the element with those digits sorted (bc/symtensor.py:143-151 reads every
+// position through its sorted index the same way); the symmetric moment GEMM
+// produces the sorted ones.  One CTA per listed block; reads touch only
+// sorted positions, writes only unsorted ones (no hazard).
+__global__ void __launch_bounds__(256) k_sym_fill(const int32_t *__restrict__ fill_keys, int64_t nfill,
+                                                  const int32_t *__restrict__ keys, const int64_t *__restrict__ offs,
+                                                  int m, int b, int64_t n, double *__restrict__ out) {
+  for (int64_t w = blockIdx.x; w < nfill; w += gridDim.x) {
+    const int32_t k = fill_keys[w];
+    const int32_t *key = keys + (int64_t)k * m;
+    int e[16], kv[16];
+    int size = 1;
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      if (q < m) {
+        kv[q] = key[q];
+        e[q] = (int)(min((int64_t)kv[q] * b, n) - (int64_t)(kv[q] - 1) * b);
+        size *= e[q];
+      }
+    double *blk = out + offs[k];
+    for (int i = threadIdx.x; i < size; i += blockDim.x) {
+      int d[16];
+      int rem = i;
+#pragma unroll
+      for (int q = 15; q >= 0; --q)
+        if (q < m) {
+          d[q] = rem % e[q];
+          rem /= e[q];
+        }
+      // insertion sort of the digits within runs of equal block indices
+      bool moved = false;
+#pragma unroll
+      for (int q = 1; q < 16; ++q)
+        if (q < m) {
+          for (int j = q; j > 0 && kv[j] == kv[j - 1] && d[j] < d[j - 1]; --j) {
+            const int tmp = d[j];
+            d[j] = d[j - 1];
+            d[j - 1] = tmp;
+            moved = true;
+          }
+        }
+      if (!moved) continue;
+      int lin = 0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (q < m) lin = lin * e[q] + d[q];
+      blk[i] = blk[lin];
+    }
+  }
+}
+
+cudaError_t launch_sym_fill(const int32_t *fill_keys, int64_t nfill, const int32_t *keys, const int64_t *offs, int m,
+                            int b, int64_t n, double *out, cudaStream_t stream) {
+  if (nfill <= 0) return cudaSuccess;
+  const int64_t grid = std::min<int64_t>(nfill, 148 * 8);
+  k_sym_fill<<<(int)grid, 256, 0, stream>>>(fill_keys, nfill, keys, offs, m, b, n, out);
   return cudaGetLastError();
 }
 

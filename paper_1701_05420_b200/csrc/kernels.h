@@ -13,7 +13,6 @@ struct MomentArgs {
   int64_t t, ldx;
   int n, h, r;
   int bulk_ok;  // rows contiguous and 16-byte aligned: TMA bulk staging
-  int ones;     // fused multi-order plan: column -1 is the constant-ones column
   // x is the TRANSPOSED data (n rows, row stride ldx >= padded_t(t)), zero-padded past t
   const int16_t *rowcols, *colcols;
   const int32_t *row_keybase, *row_olin, *row_cstart;
@@ -59,7 +58,7 @@ int rowstats_parts(int64_t n, int64_t t);
 // Staging of a chunk's n variables by 2-D TMA boxes of <= 256 rows: n <= 256
 // is one box of exactly n rows; wider data takes ceil(n / 256) boxes of equal
 // height (a multiple of 8 rows, so every box starts 1024-byte aligned for the
-// 128-byte swizzle).  The ones row follows the staged rows.
+// 128-byte swizzle).
 __host__ __device__ inline int xbox_count(int n) { return (n + 255) / 256; }
 __host__ __device__ inline int xbox_rows(int n) {
   if (n <= 256) return n;
@@ -70,6 +69,8 @@ __host__ __device__ inline int xstaged_rows(int n) { return xbox_count(n) * xbox
 
 // padded sample count of the transposed layout the moment kernel reads
 inline int64_t padded_t(int64_t t) { return (t + 15) / 16 * 16; }
+cudaError_t launch_sym_fill(const int32_t *fill_keys, int64_t nfill, const int32_t *keys, const int64_t *offs, int m,
+                            int b, int64_t n, double *out, cudaStream_t stream);
 cudaError_t launch_div(int64_t len, const double *x, double d, double *out, cudaStream_t stream);
 cudaError_t launch_axpby(int64_t len, double a, const double *x, double c, const double *y, double *out,
                          cudaStream_t stream);

@@ -16,8 +16,7 @@
 //      tensor copy (cp.async.bulk.tensor, box 16 samples x n variables, SASS
 //      UTMALDG) with 128-byte swizzle (8 consecutive rows at the same sample
 //      pair hit 8 distinct 16-byte bank groups), double buffered, on an
-//      mbarrier; a constant row of ones follows the n data rows (the "ones"
-//      column of fused multi-order plans);
+//      mbarrier;
 //   2. the chunk's Khatri-Rao factors A[i][k] = prod_q X[s+k, rowcols[i][q]]
 //      and B[j][k] are built in shared memory (never in HBM), two samples per
 //      LDS.128 / DMUL pair / STS.128, at compile-time offsets;
@@ -154,7 +153,7 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int n = a.n;
   const int xstaged = xstaged_rows(n);                 // TMA-staged variable rows (>= n)
-  const int xrows = (xstaged + 1 + 7) / 8 * 8;         // + the ones row, 1024-byte stages
+  const int xrows = (xstaged + 7) / 8 * 8;             // 1024-byte stages
   double *xs = reinterpret_cast<double *>(smem_raw);   // [2][xrows][16], swizzled
   double *kra = xs + 2 * xrows * LDX;                  // [2][TM][LDK]
   double *krb = kra + 2 * TM * LDK;                    // [2][TN][LDK]
@@ -185,12 +184,10 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
     const bool okA = grow < a.R, okB = gcol < a.C;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      int ca = (okA && q < a.h) ? a.rowcols[grow * a.h + q] : 0;
-      int cb = (okB && q < a.r) ? a.colcols[gcol * a.r + q] : 0;
-      colA[q] = ca < 0 ? xstaged : ca;  // -1: the ones row
-      colB[q] = cb < 0 ? xstaged : cb;
-      BCG_CHECK(colA[q] >= 0 && colA[q] <= xstaged, "colA", colA[q]);
-      BCG_CHECK(colB[q] >= 0 && colB[q] <= xstaged, "colB", colB[q]);
+      colA[q] = (okA && q < a.h) ? a.rowcols[grow * a.h + q] : 0;
+      colB[q] = (okB && q < a.r) ? a.colcols[gcol * a.r + q] : 0;
+      BCG_CHECK(colA[q] >= 0 && colA[q] < xstaged, "colA", colA[q]);
+      BCG_CHECK(colB[q] >= 0 && colB[q] < xstaged, "colB", colB[q]);
     }
   }
 
@@ -199,8 +196,6 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  // the ones rows of both stages (all ones: the swizzle does not matter)
-  for (int k = tid; k < 2 * LDX; k += kThreads) xs[(k / LDX) * xrows * LDX + xstaged * LDX + (k % LDX)] = 1.0;
   __syncthreads();
 
   // thread 0 stages chunk c: one 2-D tensor copy per 256 variables
@@ -339,7 +334,6 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
         const int32_t key = kb0 + a.col_rank[col];
         if (key < a.kmin_sel || key > a.kmax_sel) continue;
         const int64_t base = a.offs[key];  // output offset of the key's block
-        if (base < 0) continue;            // fused plan: orders 0 / 1 are not produced
         const int64_t addr = base + (int64_t)ro * a.col_size[col] + a.col_olin[col];
         BCG_CHECK(addr >= 0 && addr < a.S, "epilogue address", addr);
         if (accumulate)
@@ -367,7 +361,7 @@ __global__ void k_reduce_slices(const double *__restrict__ ws, int nslices, int6
 }
 
 size_t moment_smem_bytes(int KC, int n, int tm, int tn) {
-  const size_t xrows = (size_t)(xstaged_rows(n) + 1 + 7) / 8 * 8;
+  const size_t xrows = (size_t)(xstaged_rows(n) + 7) / 8 * 8;
   return sizeof(double) * (2 * xrows * KC + 2 * (size_t)(tm + tn) * KC) + 2 * sizeof(uint64_t) +
          1024;  // + alignment slack for the 1024-byte swizzle atoms
 }

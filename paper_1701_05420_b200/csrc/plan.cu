@@ -111,8 +111,8 @@ int default_variant() {  // only the v1 kernel family (variant 0) remains
   return 0;
 }
 
-// Staircase tile list of GEMM g for a tm x tn CTA tile (tiles whose elements
-// all map to orders < 2 are dropped).  Returns the number of tiles.
+// Staircase tile list of GEMM g for a tm x tn CTA tile.  Returns the number
+// of tiles.
 static int64_t build_tiles(const Plan &p, const Gemm &g, int tm, int tn, std::vector<Tile> *tiles,
                            std::vector<int32_t> *kmin_out, std::vector<int32_t> *kmax_out) {
   if (tiles) tiles->clear();
@@ -124,7 +124,6 @@ static int64_t build_tiles(const Plan &p, const Gemm &g, int tm, int tn, std::ve
     for (int64_t c0 = g.row_cstart[r0]; c0 < g.C; c0 += tn) {
       const int64_t c1 = std::min<int64_t>(c0 + tn, g.C);
       int64_t kmin = INT64_MAX, kmax = -1;
-      bool live = false;
       for (int64_t rr = r0; rr < r1; ++rr) {
         int64_t cs = std::max<int64_t>(c0, g.row_cstart[rr]);
         if (cs >= c1) continue;
@@ -132,9 +131,8 @@ static int64_t build_tiles(const Plan &p, const Gemm &g, int tm, int tn, std::ve
         const int64_t khi = g.row_keybase[rr] + g.col_rank[c1 - 1];
         kmin = std::min<int64_t>(kmin, klo);
         kmax = std::max<int64_t>(kmax, khi);
-        for (int64_t kk = klo; kk <= khi && !live; ++kk) live = p.koff[kk] >= 0;
       }
-      if (kmax < 0 || !live) continue;  // below the staircase / only orders 0, 1
+      if (kmax < 0) continue;  // below the staircase
       ++ntiles;
       if (tiles) tiles->push_back(Tile{(int32_t)r0, (int32_t)c0});
       if (kmin_out) kmin_out->push_back((int32_t)kmin);
@@ -178,10 +176,35 @@ static void choose_shape(const Plan &p, Gemm &g) {
   }
 }
 
-// GEMM tables over the symbol alphabet 1..N (sym_edge / sym_col0, col0 < 0:
-// the ones column): rows = sorted h-tuples grouped by last entry v <= vmax,
-// cols = sorted (m-h)-tuples, row group v valid from the first column whose
-// tuple starts with >= max(v, tcol).
+// In-block offsets of a sorted block tuple T (len k) that a GEMM row / column
+// produces, row-major over its edges: all of them, or (sym) those whose digits
+// are non-decreasing within every run of equal block indices -- the other
+// offsets of such a run are permutations of one of these (the tensor is
+// super-symmetric) and are filled from it after the GEMM (k_sym_fill).
+static void tuple_offsets(const int64_t *T, int k, const std::vector<int64_t> &sym_edge, bool sym,
+                          std::vector<int64_t> &out) {
+  out.clear();
+  int64_t e[16], sz = 1;
+  for (int q = 0; q < k; ++q) sz *= (e[q] = sym_edge[T[q]]);
+  int64_t d[16] = {0};
+  for (int64_t o = 0; o < sz; ++o) {
+    bool canon = true;
+    if (sym)
+      for (int q = 1; q < k && canon; ++q) canon = !(T[q] == T[q - 1] && d[q] < d[q - 1]);
+    if (canon) out.push_back(o);
+    for (int q = k - 1; q >= 0; --q) {  // row-major odometer
+      if (++d[q] < e[q]) break;
+      d[q] = 0;
+    }
+  }
+}
+
+// GEMM tables over the block alphabet 1..N (sym_edge / sym_col0): rows =
+// sorted h-tuples grouped by last entry v <= vmax, cols = sorted (m-h)-tuples,
+// row group v valid from the first column whose tuple starts with >=
+// max(v, tcol).  Each tuple contributes one row / column per produced in-block
+// offset (tuple_offsets); row_olin / col_olin keep the full row-major offset,
+// so the epilogue address of an element is the same for every plan.
 static std::string build_gemm(Plan &p, Gemm &g, const std::vector<int64_t> &sym_edge,
                               const std::vector<int64_t> &sym_col0, int64_t N, int h, int64_t vmax,
                               int64_t tcol) {
@@ -189,7 +212,7 @@ static std::string build_gemm(Plan &p, Gemm &g, const std::vector<int64_t> &sym_
   g.h = h;
   g.r = m - h;
   const int r = g.r;
-  std::vector<int64_t> lt, rt;
+  std::vector<int64_t> lt, rt, offs;
   enum_sorted(N, h, lt);
   enum_sorted(N, r, rt);
   const int64_t NL = (int64_t)lt.size() / h, NR = (int64_t)rt.size() / r;
@@ -201,9 +224,8 @@ static std::string build_gemm(Plan &p, Gemm &g, const std::vector<int64_t> &sym_
   // right columns, lexicographic
   std::vector<int64_t> rstart(NR + 1, 0);
   for (int64_t i = 0; i < NR; ++i) {
-    int64_t sz = 1;
-    for (int q = 0; q < r; ++q) sz *= sym_edge[rt[i * r + q]];
-    rstart[i + 1] = rstart[i] + sz;
+    tuple_offsets(&rt[i * r], r, sym_edge, p.sym, offs);
+    rstart[i + 1] = rstart[i] + (int64_t)offs.size();
   }
   g.C = rstart[NR];
   g.colcols.resize(g.C * r);
@@ -212,14 +234,14 @@ static std::string build_gemm(Plan &p, Gemm &g, const std::vector<int64_t> &sym_
   g.col_size.resize(g.C);
   for (int64_t i = 0; i < NR; ++i) {
     const int64_t *Rt = &rt[i * r];
-    int64_t e[16];
-    for (int q = 0; q < r; ++q) e[q] = sym_edge[Rt[q]];
-    const int64_t sz = rstart[i + 1] - rstart[i];
-    for (int64_t o = 0; o < sz; ++o) {
-      int64_t c = rstart[i] + o, rem = o;
+    int64_t e[16], sz = 1;
+    for (int q = 0; q < r; ++q) sz *= (e[q] = sym_edge[Rt[q]]);
+    tuple_offsets(Rt, r, sym_edge, p.sym, offs);
+    for (size_t j = 0; j < offs.size(); ++j) {
+      const int64_t c = rstart[i] + (int64_t)j, o = offs[j];
+      int64_t rem = o;
       for (int q = r - 1; q >= 0; --q) {
-        const int64_t c0 = sym_col0[Rt[q]];
-        g.colcols[c * r + q] = (int16_t)(c0 < 0 ? -1 : c0 + rem % e[q]);
+        g.colcols[c * r + q] = (int16_t)(sym_col0[Rt[q]] + rem % e[q]);
         rem /= e[q];
       }
       g.col_rank[c] = (int32_t)i;
@@ -241,9 +263,8 @@ static std::string build_gemm(Plan &p, Gemm &g, const std::vector<int64_t> &sym_
     const int64_t *L = &lt[lorder[i] * h];
     const int64_t v = L[h - 1];
     if (v > vmax || cstart_v[std::max(v, tcol)] >= g.C) continue;
-    int64_t sz = 1;
-    for (int q = 0; q < h; ++q) sz *= sym_edge[L[q]];
-    g.R += sz;
+    tuple_offsets(L, h, sym_edge, p.sym, offs);
+    g.R += (int64_t)offs.size();
   }
   g.rowcols.resize(g.R * h);
   g.row_keybase.resize(g.R);
@@ -259,17 +280,16 @@ static std::string build_gemm(Plan &p, Gemm &g, const std::vector<int64_t> &sym_
     for (int q = 0; q < h; ++q) full[q] = L[q];
     for (int q = h; q < m; ++q) full[q] = v;
     const int64_t kbase = multiset_rank(full, m, N) - rank_first_v[v];
-    int64_t sz = 1;
-    for (int q = 0; q < h; ++q) sz *= (e[q] = sym_edge[L[q]]);
-    for (int64_t o = 0; o < sz; ++o, ++row) {
-      int64_t rem = o;
+    for (int q = 0; q < h; ++q) e[q] = sym_edge[L[q]];
+    tuple_offsets(L, h, sym_edge, p.sym, offs);
+    for (size_t j = 0; j < offs.size(); ++j, ++row) {
+      int64_t rem = offs[j];
       for (int q = h - 1; q >= 0; --q) {
-        const int64_t c0 = sym_col0[L[q]];
-        g.rowcols[row * h + q] = (int16_t)(c0 < 0 ? -1 : c0 + rem % e[q]);
+        g.rowcols[row * h + q] = (int16_t)(sym_col0[L[q]] + rem % e[q]);
         rem /= e[q];
       }
       g.row_keybase[row] = (int32_t)kbase;
-      g.row_olin[row] = (int32_t)o;
+      g.row_olin[row] = (int32_t)offs[j];
       g.row_cstart[row] = (int32_t)cstart_v[vc];
     }
   }
@@ -277,9 +297,15 @@ static std::string build_gemm(Plan &p, Gemm &g, const std::vector<int64_t> &sym_
   return "";
 }
 
-std::string build_plan(int64_t n, int m, int b, Plan &p, int variant, bool fused) {
+static int64_t gemm_produced(const Gemm &g) {
+  int64_t s = 0;
+  for (int64_t r = 0; r < g.R; ++r) s += g.C - g.row_cstart[r];
+  return s;
+}
+
+std::string build_plan(int64_t n, int m, int b, Plan &p, int variant, bool sym) {
   if (n < 1 || m < 1 || b < 1) return "n, m and b must all be >= 1";
-  p.fused = fused;
+  p.sym = sym;
   p.variant = variant < 0 ? default_variant() : variant;
   if (m > 16) return "kernel supports 2 <= m <= 16";
   p.n = n;
@@ -293,56 +319,20 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant, bool fused
   if (LM.offs.back() > (int64_t)INT32_MAX * 64) return "tensor too large";
   if (LM.K > INT32_MAX) return "too many blocks";
   if (m < 2) return "";
+  for (int64_t k = 0; k < LM.K; ++k)
+    if (LM.offs[k + 1] - LM.offs[k] > INT32_MAX) return "block too large";
 
-  // ---- moment GEMM tables over a block alphabet ----
-  // Unfused: symbols 1..nbar are the data blocks.  Fused (single pass over all
-  // orders 2..m): symbol 1 is a "ones" block (edge 1, constant column), symbols
-  // 2..nbar+1 are the data blocks; a key with z ones is the order-(m - z) key
-  // of its remaining entries, so one staircase GEMM yields M_2..M_m.
-  std::vector<int64_t> sym_edge, sym_col0;  // 1-based
-  const int64_t N = p.fused ? p.nbar + 1 : p.nbar;
-  sym_edge.assign(N + 1, 0);
-  sym_col0.assign(N + 1, 0);
-  for (int64_t sidx = 1; sidx <= N; ++sidx) {
-    const int64_t j = p.fused ? sidx - 1 : sidx;  // data block, 0 = ones
-    sym_edge[sidx] = j == 0 ? 1 : edge_of(j, n, b);
-    sym_col0[sidx] = j == 0 ? -1 : (j - 1) * b;
+  // ---- moment GEMM tables over the block alphabet 1..nbar ----
+  const int64_t N = p.nbar;
+  std::vector<int64_t> sym_edge(N + 1, 0), sym_col0(N + 1, 0);  // 1-based
+  for (int64_t j = 1; j <= N; ++j) {
+    sym_edge[j] = edge_of(j, n, b);
+    sym_col0[j] = (j - 1) * b;
   }
-  // target offset of every GEMM key (m-tuple of symbols, lexicographic)
-  {
-    std::vector<int64_t> keys;
-    enum_sorted(N, m, keys);
-    const int64_t KG = (int64_t)keys.size() / m;
-    p.koff.assign(KG, -1);
-    p.order_base.assign(m + 2, 0);
-    if (p.fused) {
-      int64_t base = 0;
-      for (int o = 2; o <= m; ++o) {
-        p.order_base[o] = base;
-        base += p.lay[o].offs.back();
-      }
-      p.order_base[m + 1] = base;
-      p.S_out = base;
-    } else {
-      p.S_out = LM.offs.back();
-    }
-    for (int64_t k = 0; k < KG; ++k) {
-      const int64_t *key = &keys[k * m];
-      if (!p.fused) {
-        p.koff[k] = LM.offs[k];
-        continue;
-      }
-      int z = 0;
-      while (z < m && key[z] == 1) ++z;
-      const int o = m - z;
-      if (o < 2) continue;  // orders 0 and 1 are not produced
-      int64_t sub[16];
-      for (int q = 0; q < o; ++q) sub[q] = key[z + q] - 1;  // data block j
-      p.koff[k] = p.order_base[o] + p.lay[o].offs[multiset_rank(sub, o, p.nbar)];
-    }
-  }
+  p.koff.assign(LM.offs.begin(), LM.offs.end() - 1);  // GEMM key k = layout key k
+  p.S_out = LM.offs.back();
   // ---- the GEMM(s) ----
-  // odd m, unfused: try the hybrid split of the keys by their middle entry
+  // odd m: try the hybrid split of the keys by their middle entry
   // (key[h] < T: (h+1 | r-1) GEMM; else (h | r)), pick the T whose 64 x 64
   // tiling covers the staircase with the least area (independent of the tile
   // shapes chosen below, so every shape gives the same factorization)
@@ -353,7 +343,7 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant, bool fused
     std::string err = build_gemm(p, p.gemm[0], sym_edge, sym_col0, N, h0, N, 1);
     if (!err.empty()) return err;
   }
-  if (!p.fused && (m % 2) == 1 && m >= 3 && !std::getenv("BCG_NO_HYBRID")) {
+  if ((m % 2) == 1 && m >= 3 && !std::getenv("BCG_NO_HYBRID")) {
     double best = gemm_cost(p, p.gemm[0], 64, 64);
     for (int64_t T = 2; T <= N; ++T) {
       Gemm ga, gb;
@@ -374,10 +364,22 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant, bool fused
     }
   }
   // per-GEMM CTA tile shape (tile model) and tile lists
+  p.produced = 0;
   for (Gemm &g : p.gemm) {
     choose_shape(p, g);
     build_tiles(p, g, g.tm, g.tn, &g.tiles, &g.tile_kmin, &g.tile_kmax);
+    p.produced += gemm_produced(g);
   }
+  // symmetric plan: blocks with a repeated block index of edge > 1 hold
+  // permuted copies to fill after the GEMM
+  p.fill_keys.clear();
+  if (p.sym)
+    for (int64_t k = 0; k < LM.K; ++k)
+      for (int q = 1; q < m; ++q)
+        if (LM.keys[k * m + q] == LM.keys[k * m + q - 1] && LM.edges[k * m + q] > 1) {
+          p.fill_keys.push_back((int32_t)k);
+          break;
+        }
 
   // ---- recursion tables ----
   p.part_mask.clear();
@@ -499,6 +501,7 @@ std::string upload_plan(Plan &p) {
   UP(d_full_offs, full_offs);
   UP(d_full_keys, full_keys);
   UP(d_partial_keys, partial_keys);
+  UP(d_fill_keys, fill_keys);
 #undef UP
   if (e == cudaSuccess) e = up(&p.d_offs, p.lay[p.m].offs);
   if (e == cudaSuccess && p.m >= 1) {
@@ -518,7 +521,7 @@ void free_plan(Plan &p) {
       if (q) cudaFree(q);
   }
   void *ptrs[] = {p.d_offs, p.d_keys32, p.d_sub_rank, p.d_part_mask, p.d_koff, p.d_term_off,
-                  p.d_full_offs, p.d_full_keys, p.d_partial_keys};
+                  p.d_full_offs, p.d_full_keys, p.d_partial_keys, p.d_fill_keys};
   for (void *q : ptrs)
     if (q) cudaFree(q);
   for (auto &q : p.d_lower_offs)

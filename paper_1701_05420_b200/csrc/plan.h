@@ -31,7 +31,7 @@ struct Gemm {
   int h = 0, r = 0;
   int tm = kTM, tn = kTN;               // CTA tile
   int64_t R = 0, C = 0;                 // left rows, right cols
-  std::vector<int16_t> rowcols;         // R x h X-column per mode (-1: ones)
+  std::vector<int16_t> rowcols;         // R x h X-column per mode
   std::vector<int16_t> colcols;         // C x r
   std::vector<int32_t> row_keybase;     // key index of (L, R) = row_keybase + col_rank
   std::vector<int32_t> row_olin;        // within-block linear offset of L's modes
@@ -52,7 +52,12 @@ struct Gemm {
 struct Plan {
   int64_t n = 0;
   int variant = 0;          // moment kernel variant (0: the DMMA kernel)
-  bool fused = false;       // one GEMM for all orders 2..m (ones block), output concatenated
+  // symmetric plan (default): within every run of equal block indices of a
+  // GEMM row (left) or column (right) tuple only the in-block offsets with
+  // non-decreasing digits are produced; the permuted copies are filled from
+  // them afterwards (k_sym_fill).  false: every stored element is produced
+  // directly (the reference's per-element semantics, bc/_core.pyx:60-123).
+  bool sym = true;
   int m = 0, b = 0;
   int64_t nbar = 0;
   std::vector<Layout> lay;  // index = order, 0..m (0 unused)
@@ -63,9 +68,11 @@ struct Plan {
   // (h+1 | r-1) GEMM (both staircases nearly rectangular, K2).
   std::vector<Gemm> gemm;
   int split_T = 0;                      // 0: single GEMM
-  std::vector<int64_t> koff;           // key -> output offset of its block (-1: not produced)
-  std::vector<int64_t> order_base;     // fused: order o's packed buffer starts at order_base[o]
-  int64_t S_out = 0;                   // output elements (S_m, or S_2 + ... + S_m fused)
+  std::vector<int64_t> koff;           // key -> output offset of its block
+  int64_t S_out = 0;                   // output elements (S_m)
+  int64_t produced = 0;                // elements the GEMMs produce (S_m unless sym)
+  // sym: blocks whose key repeats a block index (edge > 1) -- the fill list
+  std::vector<int32_t> fill_keys;
 
   // --- recursion (order m) ---
   // partition table: for sigma = 2..m/2, partitions in reference order
@@ -91,11 +98,12 @@ struct Plan {
   int32_t *d_term_off = nullptr;
   int64_t *d_full_offs = nullptr;
   int32_t *d_full_keys = nullptr, *d_partial_keys = nullptr;
+  int32_t *d_fill_keys = nullptr;
   int64_t *d_lower_offs[16] = {nullptr};  // offs of orders 2..m-2
 };
 
 // Builders (plan.cu).
-std::string build_plan(int64_t n, int m, int b, Plan &p, int variant = -1, bool fused = false);
+std::string build_plan(int64_t n, int m, int b, Plan &p, int variant = -1, bool sym = true);
 int default_variant();
 std::string upload_plan(Plan &p);
 void free_plan(Plan &p);

@@ -105,7 +105,7 @@ class CudaOps:
             _moment_raw_wide(xt, t, k, b, out, key_range)
             return out
         plan = _native.plan(n, k, b)
-        wsb = plan.ws_bytes(t)
+        wsb = plan.t_ws_bytes(t)  # split-K partials only: xt is already transposed
         ws = torch.empty(wsb, dtype=torch.uint8, device=xt.device) if wsb else None
         wsp = ws.data_ptr() if ws is not None else None
         lib = _native.lib()

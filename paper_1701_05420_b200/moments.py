@@ -241,7 +241,7 @@ def _moment_raw_t_into(xt, t: int, m: int, b: int, out) -> None:
         _moment_raw_wide(xt, t, m, b, out)
         return
     plan = _native.plan(n, m, b)
-    wsb = plan.ws_bytes(t)
+    wsb = plan.t_ws_bytes(t)  # split-K partials only: xt is already transposed
     ws = torch.empty(wsb, dtype=torch.uint8, device=xt.device) if wsb else None
     _native.check(_native.lib().bcg_moment_raw_t(plan.handle, xt.data_ptr(), t, ldt, out.data_ptr(),
                                                  ws.data_ptr() if ws is not None else None, wsb,

@@ -70,9 +70,44 @@ def test_native_layout_config_digests(golden):
 @pytest.mark.parametrize("n,m,b", [(4, 3, 2), (5, 4, 2), (5, 4, 3), (3, 5, 2), (6, 2, 4), (2, 6, 1),
                                    (3, 3, 5), (6, 6, 2), (7, 4, 3), (24, 4, 4), (64, 4, 8), (48, 5, 4),
                                    (36, 6, 3), (13, 7, 3), (11, 8, 5), (1, 3, 1), (100, 2, 7)])
-def test_gemm_mapping_selfcheck(n, m, b):
-    plan = _native.Plan(n, m, b, host_only=True)
+@pytest.mark.parametrize("full", [False, True])
+def test_gemm_mapping_selfcheck(n, m, b, full):
+    plan = _native.Plan(n, m, b, host_only=True, full=full)
     _native.check(_native.lib().bcg_plan_selfcheck(plan.handle))
+    S, produced = plan.output()
+    assert S == orc.block_layout(n, m, b)[3][-1]
+    assert produced == S if full else produced <= S
+
+
+def _sorted_within_runs_count(n, m, b, h):
+    """Elements a symmetric plan's (h | m-h) GEMM produces: per key, the
+    in-block offsets whose digits are non-decreasing within each run of equal
+    block indices of the left h-tuple and of the right (m-h)-tuple."""
+    from itertools import combinations_with_replacement, groupby
+    from math import comb
+
+    nb = -(-n // b)
+    edge = lambda j: min(j * b, n) - (j - 1) * b  # noqa: E731
+
+    def part(t):
+        r = 1
+        for j, g in groupby(t):
+            L = len(list(g))
+            r *= comb(edge(j) + L - 1, L)
+        return r
+
+    return sum(part(k[:h]) * part(k[h:]) for k in combinations_with_replacement(range(1, nb + 1), m))
+
+
+@pytest.mark.parametrize("n,m,b", [(36, 6, 3), (64, 4, 8), (24, 4, 4), (7, 4, 3)])
+def test_symmetric_plan_produced_count(n, m, b):
+    # even orders run one balanced (m/2 | m/2) GEMM: the produced count is the
+    # closed form (cfg4: 58.5% of S_6, cfg2: 70.3% of S_4)
+    plan = _native.Plan(n, m, b, host_only=True)
+    S, produced = plan.output()
+    assert produced == _sorted_within_runs_count(n, m, b, m // 2)
+    if (n, m, b) == (36, 6, 3):
+        assert abs(produced / S - 0.585) < 1e-3
 
 
 def test_hybrid_odd_order_plan():
