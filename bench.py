@@ -1,15 +1,22 @@
 """Benchmark: cumulants_upto (center -> packed moments of orders 2..m -> recursion)
 on BASELINE.json's configs, B200 sm_100a path vs the reference's CPU path.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
 
 A "step" is one full cumulants_upto pass over the config's synthetic matrix.
 ``value`` times it with the matrix already resident in HBM; ``e2e`` times the
 public call on a pinned HOST matrix (H2D of X and D2H of C_1..C_m inside the
-timed region).  The metric is algorithmic FP64 TFLOP/s, sum_k 2 t S_k over
-k = 2..m (SURVEY.md §8 d), plus ms per step.  N > 1 (torchrun): each rank holds
-its own t-row shard (weak scaling), partial moments are all-reduced over NCCL
-(distributed.py).  Prints ONE JSON line on rank 0.
+timed region).  The metric is reference-equivalent FP64 TFLOP/s: the
+algorithmic work sum_k 2 t S_k over k = 2..m (SURVEY.md §8 d: one multiply-add
+per sample per STORED element, the work the reference's kernel performs) per
+second, plus ms per step.  The roofline is on the FLOPs the DMMA kernel
+actually executes (2 t x the elements its symmetric plan computes, K2).
+
+N > 1: ``--gpus N`` re-launches itself under torch.distributed.run (one rank
+per GPU, NCCL).  Default strong scaling: rank r holds rows [t r/N, t (r+1)/N)
+of the config's canonical matrix (bc/moments.py:66-68 bounds; rank 0 draws it
+and broadcasts it); ``--weak`` gives every rank t rows of its own seed instead.
+Prints ONE JSON line on rank 0.
 """
 
 from __future__ import annotations
@@ -17,6 +24,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -31,36 +39,60 @@ import workloads  # noqa: E402
 
 METRIC = "moment+cumulant time & FP64 TFLOP/s at (n,m,t); % of DMMA / HBM roofline"
 # FP64 DMMA peak measured on this pool's B200 (tools/fp64_peak.cu,
-# profiles/r01_fp64_peak.log: mma.sync m8n8k4 f64 = 37.1 TFLOP/s at 1965 MHz).
-# MEASURED_PEAKS.json carries no FP64 figure.
+# profiles/r02_fp64_peak.log: mma.sync m8n8k4 f64 at 1965 MHz, clocks sampled
+# under load).  MEASURED_PEAKS.json carries no FP64 figure.
 FP64_PEAK_TFLOPS = 37.1
-FP64_PEAK_SOURCE = "measured DMMA.8x8x4 microbenchmark (tools/fp64_peak.cu, profiles/r01_fp64_peak.log)"
-DEFAULT_WORKLOAD = "cfg2"  # configs[1]: the single-GPU headline case
+FP64_PEAK_SOURCE = "measured DMMA.8x8x4 microbenchmark (tools/fp64_peak.cu, profiles/r02_fp64_peak.log)"
+DEFAULT_WORKLOAD = "cfg4"  # the largest single-GPU BASELINE config (C2..C6), also its 1/2/4/8-GPU config
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=DEFAULT_WORKLOAD, choices=sorted(workloads.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--weak", action="store_true", help="N > 1: t rows per GPU (own seed) instead of a t-row split")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample-rows", type=int, default=0, help="rows of the CPU baseline sample (0 = auto)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch / rendezvous / shard bookkeeping only (gloo, no GPU): one JSON line")
     ap.add_argument("--t", type=int, default=0,
-                    help="rows per GPU instead of the config's t (exploration only: the line then says so; "
-                         "e.g. cfg5 at its BASELINE t=4e6 takes ~13 min per step on one B200)")
+                    help="total rows instead of the config's t (exploration only: the line then says so)")
     return ap.parse_args()
 
 
-def config_dict(cfg, t_total, world):
-    note = "" if t_total == cfg.t * world else f"; t overridden, BASELINE t={cfg.t} per GPU"
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_if_needed(args) -> bool:
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run with
+    N ranks on this node (the driver's own launch line).  Returns True when
+    this process was the launcher."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    rc = subprocess.call(cmd)
+    if rc:
+        sys.exit(rc)
+    return True
+
+
+def config_dict(cfg, t_total, world, weak, overridden):
+    note = f"; t overridden, BASELINE t={cfg.t}" if overridden else ""
+    split = (f"weak: {t_total // world} rows per GPU, own seed per rank" if weak
+             else f"strong: rows [t r/N, t (r+1)/N) of the canonical matrix")
     return {
         "workload": f"{cfg.name}: cumulants_upto C1..C{cfg.m}, t={t_total} x n={cfg.n}, b={cfg.b} ({cfg.desc}){note}",
         "t": t_total, "n": cfg.n, "b": cfg.b, "m_max": cfg.m,
-        "parallelism": f"t-shard x{world}" if world > 1 else "single GPU",
-        "l2": "inputs larger than L2 (X = %.0f MB per GPU vs 126 MB L2)" % (cfg.t * cfg.n * 8 / 1e6),
+        "parallelism": f"t-shard x{world} ({split}), NCCL reduce-scatter/all-gather" if world > 1 else "single GPU",
+        "l2": "inputs larger than L2 (X = %.0f MB per GPU vs 126 MB L2)" % (t_total / world * cfg.n * 8 / 1e6),
     }
 
 
@@ -119,14 +151,33 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU (reference)
+#
+# The reference's own CPU path (the unmodified package built by
+# oracle/build_ref.sh into oracle/_ref; the oracle port only if that build is
+# missing), on the host's cores.  Engines tried, best reported:
+#   compiled     cumulants_upto(engine="compiled"): the Cython kernel, 1 thread
+#   gram         cumulants_upto(engine="gram"): KR columns + BLAS GEMMs, BLAS
+#                threads swept over {1, all} (threadpoolctl)
+#   blocks-p     the reference's public API composed with its parallel kernel:
+#                center, moment_parallel_blocks(p = all cores, compiled) per
+#                order, minus outer_prod_cum per sigma -- cumulant()'s own
+#                arithmetic (bc/cumulants.py:119-136, bc/moments.py:99-131)
+# The work is linear in t plus a t-independent recursion (Python einsum per
+# block), so the rate of a small t-sample understates the CPU: every engine is
+# timed at two sample sizes, time = a + b t is fitted, and the reported rate is
+# the fit's full-t rate (SURVEY.md §8 d extrapolation, labelled as such).
+
+CPU_SAMPLES = {  # (t1, t2) rows: ~1-15 s per pass of the best engine
+    "cfg1": (5_000, 20_000), "cfg2": (5_000, 25_000), "cfg3": (1_000, 5_000),
+    "cfg4": (500, 2_500), "cfg5": (100, 400),
+}
 
 
 def _load_reference():
-    """The unmodified reference built by oracle/build_ref.sh (kind
-    "reference"), else the oracle port (kind "port")."""
     ref_dir = os.path.join(ROOT, "oracle", "_ref")
     if os.path.isdir(os.path.join(ref_dir, "blockcumulants")):
-        sys.path.insert(0, ref_dir)
+        if ref_dir not in sys.path:
+            sys.path.insert(0, ref_dir)
         import blockcumulants as bc
 
         if bc.HAVE_COMPILED:
@@ -134,52 +185,102 @@ def _load_reference():
     return "port", None
 
 
-def _cpu_cores():
+def _cpu_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
 
 
-def _reference_run(kind, bc, x, cfg, engine):
-    if kind == "reference":
-        bc.cumulants_upto(x, cfg.m, b=cfg.b, engine=engine)
-    else:
-        from oracle import oracle as orc
+def _cgroup_quota() -> str:
+    for path in ("/sys/fs/cgroup/cpu.max", "/sys/fs/cgroup/cpu/cpu.cfs_quota_us"):
+        try:
+            with open(path) as f:
+                return f"{path}: {f.read().strip()}"
+        except OSError:
+            continue
+    return "no cgroup cpu quota file"
+
+
+def _blocks_parallel(bc, x, m, b, p):
+    arr = np.ascontiguousarray(x, dtype=np.float64)
+    xc = bc.center(arr)
+    tensors = []
+    for k in range(2, m + 1):
+        res = bc.moment_parallel_blocks(xc, k, b, p=p, engine="compiled")
+        if k >= 4:
+            for sigma in range(2, k // 2 + 1):
+                res = res - bc.outer_prod_cum(k, sigma, tensors)
+        tensors.append(res)
+    return arr.mean(axis=0), tensors
+
+
+def _cpu_engines(kind, cfg):
+    cores = _cpu_cores()
+    if kind != "reference":
+        return [("port", 1)]
+    engs = [("compiled", 1), ("blocks-p", cores)]
+    if cfg.name != "cfg5":  # gram is refused by its 2e8 guard at cfg5
+        engs += [("gram", 1), ("gram", cores)]
+    return engs
+
+
+def _cpu_run(kind, bc, x, cfg, eng, threads):
+    if kind != "reference":
+        from oracle import oracle as orc  # the port: bench/test infrastructure only
 
         orc.cumulants_upto(x, cfg.m, cfg.b)
+        return
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=threads):
+        if eng == "blocks-p":
+            _blocks_parallel(bc, x, cfg.m, cfg.b, threads)
+        else:
+            bc.cumulants_upto(x, cfg.m, b=cfg.b, engine=eng)
 
 
-def cpu_sample_rows(cfg, requested: int) -> int:
-    if requested:
-        return requested
-    # ~2-5 s per pass of the reference's best engine (SURVEY.md §6 rates)
-    return {"cfg1": 20_000, "cfg2": 20_000, "cfg3": 4_000, "cfg4": 1_000, "cfg5": 400}[cfg.name]
-
-
-def cpu_baseline(cfg, rows: int):
-    """Reference cumulants_upto on a bounded t-row sample of the same recipe,
-    best of its compiled (1 thread) and gram (BLAS threads) engines."""
+def cpu_calibrate(cfg):
+    """Time every engine at t2, fit time = a + b t for the best one from t1 and
+    t2, return the description the bench line carries."""
     kind, bc = _load_reference()
-    x = workloads.generate(cfg.name, rows)
-    flops = workloads.moment_flops(rows, cfg.n, cfg.b, cfg.m)
-    best = None
-    engines = ("compiled", "gram") if kind == "reference" else ("port",)
-    if cfg.name == "cfg5":
-        engines = tuple(e for e in engines if e != "gram")  # refused by its 2e8 guard
-    for eng in engines:
+    t1, t2 = CPU_SAMPLES[cfg.name]
+    x2 = workloads.generate(cfg.name, t2)
+    times = {}
+    for eng, thr in _cpu_engines(kind, cfg):
         t0 = time.perf_counter()
-        _reference_run(kind, bc, x, cfg, eng)
-        dt = time.perf_counter() - t0
-        if best is None or dt < best[1]:
-            best = (eng, dt)
-    eng, dt = best
-    cores = 1 if eng in ("compiled", "port") else _cpu_cores()
+        _cpu_run(kind, bc, x2, cfg, eng, thr)
+        times[(eng, thr)] = time.perf_counter() - t0
+    best = min(times, key=times.get)
+    x1 = x2[:t1].copy()
+    t0 = time.perf_counter()
+    _cpu_run(kind, bc, x1, cfg, *best)
+    dt1 = time.perf_counter() - t0
+    dt2 = times[best]
+    slope = max((dt2 - dt1) / (t2 - t1), 1e-12)
+    icept = max(dt2 - slope * t2, 0.0)
+    t_full = cfg.t
+    full_s = icept + slope * t_full
+    flops_full = workloads.moment_flops(t_full, cfg.n, cfg.b, cfg.m)
     return {
-        "value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": kind,
-        "sample": f"cumulants_upto(X[:{rows}], {cfg.m}, b={cfg.b}, engine={eng!r}) of the {cfg.name} recipe, "
-                  f"{dt:.2f} s (best of {', '.join(engines)}; host has {_cpu_cores()} cores)",
-        "ms_per_sample": dt * 1e3,
+        "kind": kind, "bc": bc, "engine": best, "x2": x2, "t2": t2,
+        "value": flops_full / full_s / 1e12,
+        "fit": {"a_s": icept, "b_s_per_row": slope, "t1": t1, "t2": t2, "time_t1_s": dt1, "time_t2_s": dt2,
+                "full_t": t_full, "full_t_s_extrapolated": full_s},
+        "sample_rate_t2": workloads.moment_flops(t2, cfg.n, cfg.b, cfg.m) / dt2 / 1e12,
+        "engines_s_at_t2": {f"{e}@{th}thr": round(v, 3) for (e, th), v in times.items()},
+    }
+
+
+def cpu_baseline_dict(cal, value=None):
+    eng, thr = cal["engine"]
+    return {
+        "value": cal["value"] if value is None else value, "unit": "TFLOP/s", "cores": thr, "kind": cal["kind"],
+        "sample": (f"{eng} engine, {thr} thread(s): cumulants_upto on X[:t1], X[:t2] of the recipe, "
+                   f"time = a + b t fitted and extrapolated to the full t (rate at t2 alone: "
+                   f"{cal['sample_rate_t2']:.3g} TFLOP/s)"),
+        "fit": cal["fit"], "threads": {"host_cores": _cpu_cores(), "cgroup": _cgroup_quota()},
+        "engines_s_at_t2": cal["engines_s_at_t2"],
     }
 
 
@@ -188,40 +289,61 @@ def run_reference_arm(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    kind, bc = _load_reference()
-    rows = cpu_sample_rows(cfg, args.cpu_sample_rows)
-    x = workloads.generate(cfg.name, rows)
-    flops = workloads.moment_flops(rows, cfg.n, cfg.b, cfg.m)
-    engines = ("compiled", "gram") if kind == "reference" else ("port",)
-    if cfg.name == "cfg5":
-        engines = ("compiled",) if kind == "reference" else engines
-    # calibrate: the faster engine is the reference's best CPU path on this host
-    times = {}
-    for eng in engines:
-        t0 = time.perf_counter()
-        _reference_run(kind, bc, x, cfg, eng)
-        times[eng] = time.perf_counter() - t0
-    eng = min(times, key=times.get)
+    cal = cpu_calibrate(cfg)
+    kind, bc, x2 = cal["kind"], cal["bc"], cal["x2"]
     for _ in range(max(0, args.warmup - 1)):
-        _reference_run(kind, bc, x, cfg, eng)
+        _cpu_run(kind, bc, x2, cfg, *cal["engine"])
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        _reference_run(kind, bc, x, cfg, eng)
+        _cpu_run(kind, bc, x2, cfg, *cal["engine"])
     dt = (time.perf_counter() - t0) / args.steps
-    value = flops / dt / 1e12
-    cores = 1 if eng in ("compiled", "port") else _cpu_cores()
+    # the timed steps re-measure the t2 point of the fit
+    fit = dict(cal["fit"])
+    slope = max((dt - fit["time_t1_s"]) / (fit["t2"] - fit["t1"]), 1e-12)
+    icept = max(dt - slope * fit["t2"], 0.0)
+    full_s = icept + slope * cfg.t
+    fit.update(a_s=icept, b_s_per_row=slope, time_t2_s=dt, full_t_s_extrapolated=full_s)
+    cal["fit"] = fit
+    value = workloads.moment_flops(cfg.t, cfg.n, cfg.b, cfg.m) / full_s / 1e12
+    cal["sample_rate_t2"] = workloads.moment_flops(fit["t2"], cfg.n, cfg.b, cfg.m) / dt / 1e12
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic ({cfg.name} recipe, workloads.py), bounded sample of {rows} rows per step",
-        "config": config_dict(cfg, rows, 1),
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": kind,
-                         "sample": f"cumulants_upto(X[:{rows}], {cfg.m}, b={cfg.b}, engine={eng!r}); "
-                                   f"calibration {', '.join(f'{k}={v:.2f}s' for k, v in times.items())}"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": full_s * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": (f"synthetic ({cfg.name} recipe, workloads.py); each step = one pass on a {fit['t2']}-row sample "
+                 f"({dt:.2f} s), value and ms_per_step extrapolated to t={cfg.t} by the a + b t fit"),
+        "config": config_dict(cfg, cfg.t, 1, False, False),
+        "cpu_baseline": cpu_baseline_dict(cal, value),
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- dry run (CPU)
+
+
+def run_dry(args, cfg):
+    """Rendezvous and shard bookkeeping of the N-rank launch over gloo (no GPU)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1701_05420_b200.distributed import shard_bounds
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    t_total = args.t or cfg.t
+    lo, hi = shard_bounds(t_total, world, rank) if not args.weak else (0, t_total)
+    v = torch.tensor([1.0, float(hi - lo)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(v)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_seen": int(v[0]), "rows_total": int(v[1]),
+                          "config": config_dict(cfg, t_total if not args.weak else t_total * world, world,
+                                                args.weak, bool(args.t))}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------- GPU (ours)
@@ -230,8 +352,13 @@ def run_reference_arm(args, cfg):
 def main():
     args = parse()
     cfg = workloads.CONFIGS[args.config]
+    if relaunch_if_needed(args):
+        return
     if args.impl == "reference":
         run_reference_arm(args, cfg)
+        return
+    if args.dry_run:
+        run_dry(args, cfg)
         return
 
     import torch
@@ -240,7 +367,7 @@ def main():
     import paper_1701_05420_b200 as bcg
     from paper_1701_05420_b200 import _native
     from paper_1701_05420_b200.cumulants import cumulants_device
-    from paper_1701_05420_b200.distributed import cumulants_upto_sharded
+    from paper_1701_05420_b200.distributed import cumulants_upto_sharded, shard_bounds
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -249,14 +376,33 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    t_local = args.t or cfg.t
-    t_total = t_local * world
-    x_host = workloads.generate(cfg.name, t_local, shard=rank)
-    X = torch.from_numpy(x_host).cuda()
+    if args.weak:
+        t_local = args.t or cfg.t
+        t_total = t_local * world
+        x_host = workloads.generate(cfg.name, t_local, shard=rank)
+        X = torch.from_numpy(x_host).cuda()
+    else:
+        t_total = args.t or cfg.t
+        lo, hi = shard_bounds(t_total, world, rank)
+        t_local = hi - lo
+        if world == 1:
+            x_host = workloads.generate(cfg.name, t_total)
+            X = torch.from_numpy(x_host).cuda()
+        else:
+            # rank 0 draws the canonical matrix once; NCCL broadcast; every
+            # rank keeps its contiguous row shard (bc/moments.py:66-68)
+            full = (torch.from_numpy(workloads.generate(cfg.name, t_total)).cuda() if rank == 0 else
+                    torch.empty((t_total, cfg.n), dtype=torch.float64, device="cuda"))
+            dist.broadcast(full, 0)
+            X = full[lo:hi].clone()
+            del full
+            x_host = X.cpu().numpy()
     x_pinned = torch.from_numpy(x_host).pin_memory()
     flops_total = workloads.moment_flops(t_total, cfg.n, cfg.b, cfg.m)
     S_top = workloads.stored_elements(cfg.n, cfg.m, cfg.b)
-    top_flops_local = 2.0 * t_local * S_top
+    _, produced_top = _native.plan(cfg.n, cfg.m, cfg.b).output()
+    algo_top_local = 2.0 * t_local * S_top
+    exec_top_local = 2.0 * t_local * produced_top
 
     def barrier():
         if world > 1:
@@ -307,7 +453,7 @@ def main():
     timed(step_device, max(2, min(5, args.steps)), timer)
     kern_ms = [a.elapsed_time(b) for a, b in timer.get("moment_top", [])]
     kern_avg = sum(kern_ms) / len(kern_ms) if kern_ms else float("nan")
-    achieved = top_flops_local / (kern_avg / 1e3) / 1e12
+    achieved = exec_top_local / (kern_avg / 1e3) / 1e12
 
     e2e = None
     if not args.no_e2e:
@@ -318,17 +464,20 @@ def main():
         d2h = 8 * (cfg.n + sum(workloads.stored_elements(cfg.n, k, cfg.b) for k in range(2, cfg.m + 1)))
         e2e = {"value": flops_total / (ms_e2e / 1e3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": int(x_host.nbytes), "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
-               "api": "paper_1701_05420_b200.cumulants_upto(pinned host tensor) + packed_host() per order"}
+               "api": ("paper_1701_05420_b200.cumulants_upto(pinned host tensor) + packed_host() per order"
+                       if world == 1 else "distributed.cumulants_upto_sharded(pinned host shard) + .cpu()")}
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            tr = json.load(f)
+        if tr.get("plan") == "symmetric":  # captured on the current plan
+            traffic = tr.get("dram_bytes_per_launch")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, cpu_sample_rows(cfg, args.cpu_sample_rows))
+        cpu = cpu_baseline_dict(cpu_calibrate(cfg))
 
     if rank == 0:
         line = {
@@ -340,17 +489,20 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": ms,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "weak" if args.weak else "strong",
             "vs_baseline": None,
             "dtype": "f64",
             "data": f"synthetic ({cfg.name} recipe, workloads.py; seeded PCG64), resident in HBM",
-            "config": config_dict(cfg, t_total, world),
+            "config": config_dict(cfg, t_total, world, args.weak, bool(args.t)),
+            "value_def": ("reference-equivalent rate: sum_k 2 t S_k (every stored element, as the reference "
+                          "computes) / step time; the symmetric plans execute fewer FLOPs (roofline)"),
             "roofline": {
-                "bound": "tensor", "kernel": f"k_moment_dmma (order {cfg.m}, incl. split-K reduce)",
+                "bound": "tensor", "kernel": f"k_moment_dmma (order {cfg.m}, incl. split-K reduce + fill)",
                 "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "algorithmic_flops_per_launch": top_flops_local, "avg_launch_ms": kern_avg,
-                "peak_source": FP64_PEAK_SOURCE,
+                "executed_flops_per_launch": exec_top_local, "algorithmic_flops_per_launch": algo_top_local,
+                "produced_elements": produced_top, "stored_elements": S_top,
+                "avg_launch_ms": kern_avg, "peak_source": FP64_PEAK_SOURCE,
             },
             "cpu_baseline": cpu,
             "e2e": e2e,

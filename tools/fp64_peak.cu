@@ -1,3 +1,4 @@
+#include <cstdlib>
 // FP64 pipe microbenchmark for B200 (sm_100a): DFMA vs DMMA (mma.sync f64) throughput.
 // Decides the moment-kernel MAC strategy.
 #include <cstdio>
@@ -105,11 +106,33 @@ float timeit(K kern, int grid, int block, int iters, double* d) {
   return best;
 }
 
-int main() {
+int main(int argc, char **argv) {
   double* d; CK(cudaMalloc(&d, 64));
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   printf("SMs %d, max clock %d MHz\n", sms, clk / 1000);
+  if (argc > 1) {  // sustained: the best DMMA configuration back to back for argv[1] seconds
+    const double secs = atof(argv[1]);
+    const int grid = sms * 2, threads = 256, it = 200000;
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    dmma884_kernel<8><<<grid, threads>>>(d, 10, 1.0000001, 1e-9);
+    cudaDeviceSynchronize();
+    double total_ms = 0, fl = 0;
+    int launches = 0;
+    cudaEventRecord(e0);
+    while (total_ms < secs * 1e3) {
+      for (int k = 0; k < 8; ++k) dmma884_kernel<8><<<grid, threads>>>(d, it, 1.0000001, 1e-9);
+      launches += 8;
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      total_ms = ms;
+    }
+    fl = 2.0 * 256 * 8 * (double)it * grid * (threads / 32) * launches;
+    printf("DMMA884 sustained %d launches, %.1f ms: %.2f TFLOP/s\n", launches, total_ms, fl / total_ms / 1e9);
+    CK(cudaGetLastError());
+    return 0;
+  }
   int iters = 20000;
   for (int bpsm : {1, 2, 4}) for (int threads : {128, 256, 512}) {
     int grid = sms * bpsm;
