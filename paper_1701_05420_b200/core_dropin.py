@@ -57,12 +57,45 @@ def moment_blocks(xt, col0, edges, out, offs, k0, k1) -> None:
     torch = _native.torch_cuda()
     n, t = xt.shape
     lo, hi = int(offs[k0]), int(offs[k1])
+    from .moments import WIDE_N
+
+    if n > WIDE_N:
+        _moment_blocks_wide(xt, col0, edges, out, offs, k0, k1)
+        return
     dxt = torch.from_numpy(xt).cuda()
     dc0, de, do = (torch.from_numpy(a).cuda() for a in (col0, edges, offs))
     dout = torch.from_numpy(out).cuda()
     _native.check(_native.lib().bcg_moment_blocks(dxt.data_ptr(), n, t, dc0.data_ptr(), de.data_ptr(), m, K,
                                                   dout.data_ptr(), do.data_ptr(), k0, k1, _native.stream_handle()),
                   "moment_blocks")
+    out[lo:hi] = dout[lo:hi].cpu().numpy()
+
+
+def _moment_blocks_wide(xt, col0, edges, out, offs, k0, k1) -> None:
+    """n > WIDE_N variables (one sample chunk of all of them exceeds the
+    moment kernel's shared-memory stage): the variable-group decomposition of
+    moments._moment_raw_wide, each sub-problem's sums computed from zero and
+    added element-wise into ``out`` -- the same accumulate semantics."""
+    from .layout import layout
+    from .moments import _moment_raw_wide
+
+    torch = _native.torch_cuda()
+    n, t = xt.shape
+    K, m = col0.shape
+    b = int(col0[1, m - 1]) if K >= 2 else n
+    lay = layout(n, m, b) if b >= 1 else None
+    if (lay is None or lay.K != K or not np.array_equal(np.asarray(lay.offs), offs)
+            or not np.array_equal(np.asarray(lay.col0).reshape(K, m), col0)
+            or not np.array_equal(np.asarray(lay.edges).reshape(K, m), edges)):
+        raise ValueError("layout does not match _block_layout(n, m, b)")
+    if t <= 0:
+        return
+    ldt = int(_native.lib().bcg_padded_t(t))
+    dxt = torch.zeros((n, ldt), dtype=torch.float64, device="cuda")
+    dxt[:, :t] = torch.from_numpy(xt).cuda()
+    dout = torch.from_numpy(out).cuda()
+    _moment_raw_wide(dxt, t, m, b, dout, key_range=(k0, k1))
+    lo, hi = int(offs[k0]), int(offs[k1])
     out[lo:hi] = dout[lo:hi].cpu().numpy()
 
 

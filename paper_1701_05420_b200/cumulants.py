@@ -46,6 +46,14 @@ def _check_centered_stats(sums, sumsq, t: int) -> None:
         raise ValidationError(f"data is not centered: column {col} has mean {means[col - 1]:.3e}")
 
 
+def central_orders(m: int, b: int) -> tuple:
+    """Central moments the order-m recursion reads besides the lower
+    cumulants: the factored kernel (recursion_fact.cu, 4 <= m <= 6, b <= 8)
+    at m = 6 reads M_4 of the complement (M_2 = C_2 and M_3 = C_3 are the
+    cumulants themselves); every other (m, b) runs the partition sum."""
+    return (4,) if m == 6 and b <= 8 else ()
+
+
 def _check_centered(X) -> None:
     st = _colstats(X, sums=True, sumsq=True)
     _check_centered_stats(st["sums"], st["sumsq"], X.shape[0])
@@ -133,10 +141,10 @@ def cumulant(x_centered, m: int, lower: Sequence[BlockSymTensor], b: int = 2,
         return _moment_device(X, m, b)
     _lower_by_order(lower, range(2, m - 1))
     result = _moment_device(X, m, b)
-    # m >= 6: the factored recursion needs the central moments M_4..M_{m-2}
-    # of the complement; they are lower-order GEMMs (cheap next to M_m) and
-    # replace the partition-sum kernel (bc/cumulants.py:119-136 either way)
-    central = {k: _moment_device(X, k, b).data for k in range(4, m - 1)} if m >= 6 else None
+    # m = 6: the factored recursion needs the central moment M_4 of the
+    # complement; it is a lower-order GEMM (cheap next to M_6) and replaces
+    # the partition-sum kernel (bc/cumulants.py:119-136 either way)
+    central = {k: _moment_device(X, k, b).data for k in central_orders(m, b)}
     _recursion_inplace(result, lower, central)
     return result
 
@@ -171,6 +179,12 @@ class CumulantSet:
         return f"CumulantSet(n={self.n}, b={self.b}, orders=1..{self.max_order})"
 
 
+def _central_kept(m_max: int, b: int) -> set:
+    """Central moments cumulants_upto keeps (cloned before their own order's
+    recursion overwrites them) for the recursions of the orders above."""
+    return {j for k in range(4, m_max + 1) for j in central_orders(k, b)}
+
+
 def cumulants_device(X, m_max: int, b: int, c1_host: bool = True, timer: dict | None = None):
     """Core of cumulants_upto on a device matrix: returns (c1, [C_2..C_m]).
 
@@ -191,7 +205,8 @@ def cumulants_device(X, m_max: int, b: int, c1_host: bool = True, timer: dict | 
         _check_centered_stats(sums, sq, t)
         if timer is None and m_max >= 3 and not _SERIAL_ORDERS:
             return (st["mean"].cpu().numpy() if c1_host else st["mean"]), _orders_concurrent(xt, t, m_max, b)
-        central: dict = {}  # central moments M_4.. kept for the factored recursion
+        central: dict = {}  # central moment M_4 kept for the factored order-6 recursion
+        keep = _central_kept(m_max, b)
         for k in range(2, m_max + 1):
             if timer is not None and k == m_max:
                 torch = _native.torch_cuda()
@@ -200,7 +215,7 @@ def cumulants_device(X, m_max: int, b: int, c1_host: bool = True, timer: dict | 
                 Mk = _moment_device_t(xt, t, k, b, events=ev)
             else:
                 Mk = _moment_device_t(xt, t, k, b)
-            if 4 <= k <= m_max - 2:
+            if k in keep:
                 central[k] = Mk.data.clone()
             if k >= 4:
                 _recursion_inplace(Mk, tensors, central)
@@ -243,11 +258,12 @@ def _orders_concurrent(xt, t: int, m_max: int, b: int) -> list:
     moments[m_max] = _moment_device_t(xt, t, m_max, b)
     tensors: list[BlockSymTensor] = []
     central: dict = {}
+    keep = _central_kept(m_max, b)
     for k in range(2, m_max + 1):
         if k in done:
             main.wait_event(done[k])
         Mk = moments[k]
-        if 4 <= k <= m_max - 2:
+        if k in keep:
             central[k] = Mk.data.clone()
         if k >= 4:
             _recursion_inplace(Mk, tensors, central)

@@ -143,6 +143,12 @@ class CudaOps:
             plan.handle, mk.data_ptr(), arr, cm, int(k0), int(k1), _native.stream_handle()), "recursion")
 
 
+def _central_kept(m_max: int, b: int) -> set:
+    from .cumulants import _central_kept as kept
+
+    return kept(m_max, b)
+
+
 def _check_centered(sums, sumsq, t: int):
     from .cumulants import _check_centered_stats
 
@@ -185,7 +191,8 @@ def cumulants_upto_sharded(x_local, m_max: int, b: int = 2, group=None, ops=None
         dist.all_reduce(both, group=group)
         _check_centered(both[:n], both[n:], t_total)
         lower: dict = {}
-        central: dict = {}  # central moments M_4..M_{m-2} (factored recursion)
+        central: dict = {}  # central moment M_4 (factored order-6 recursion)
+        keep = _central_kept(m_max, b)
         # all moment GEMMs only read Xc: issue them up front (lower orders on
         # side streams), so each order's collective overlaps the GEMMs still
         # running -- the top order's in particular
@@ -218,7 +225,7 @@ def cumulants_upto_sharded(x_local, m_max: int, b: int = 2, group=None, ops=None
                 if world > 1:
                     dist.all_reduce(mk, group=group)
                 ops.divide(mk, t_total)
-                if 4 <= k <= m_max - 2:
+                if k in keep:
                     central[k] = mk.clone()
                 if k >= 4:
                     ops.recursion_range(mk, n, k, b, lower, 0, lay.K, central)
@@ -254,6 +261,7 @@ def cumulants_upto_block_split(x_full, m_max: int, b: int = 2, group=None, ops=N
         _check_centered(csum, csq, t)
         lower: dict = {}
         central: dict = {}
+        keep = _central_kept(m_max, b)
         for k in range(2, m_max + 1):
             lay = layout(n, k, b)
             k0, k1 = block_bounds(lay.K, world, rank)
@@ -268,7 +276,7 @@ def cumulants_upto_block_split(x_full, m_max: int, b: int = 2, group=None, ops=N
                 timer.setdefault("moment_top", []).append((ev0, ev1))
             lo, hi = int(lay.offs[k0]), int(lay.offs[k1])
             ops.divide(mk[lo:hi], t)
-            if 4 <= k <= m_max - 2:
+            if k in keep:
                 # the factored recursion of higher orders reads the central
                 # moment of every block: gather it before correcting in place
                 if world > 1:

@@ -26,6 +26,15 @@ Contents (all float64 values are the reference's own results):
                       seeded sample of 4096 packed positions per order of the
                       reference's cumulants, plus per-order sum/sum-of-squares;
                       cfg1 at its full size (X regenerated from the recipe).
+* ``highorder.npz`` -- heavy-tailed data to order 6 (the Student-t(5)
+                      copula of cfg2 / cfg5, whose 6th moment does not exist:
+                      the sample cumulants cancel hardest there): the cfg5
+                      recipe's first 36 columns at b=6 and the cfg2 recipe's
+                      first 32 columns at b=8, t=3000 rows, m=6.  Stored: a
+                      checksum of X, 4096 sampled packed positions per order,
+                      and per-BLOCK sums / sums of squares of every C_k (a
+                      checksum of checksums over all 21.6 M / 22.0 M elements
+                      of C_6).
 """
 
 from __future__ import annotations
@@ -164,11 +173,45 @@ def configs_fixture():
     np.savez_compressed(os.path.join(HERE, "configs.npz"), **out)
 
 
+# (config recipe, columns kept, b, t, m): heavy tails to order 6 within the
+# CPU reference's reach (C_6 of 21-22 M elements)
+HIGHORDER = {"cfg5s": ("cfg5", 36, 6, 3000, 6), "cfg2s": ("cfg2", 32, 8, 3000, 6)}
+
+
+def highorder_input(tag: str) -> np.ndarray:
+    name, ncols, _, t, _ = HIGHORDER[tag]
+    return np.ascontiguousarray(workloads.generate(name, t)[:, :ncols])
+
+
+def highorder_fixture():
+    out = {}
+    for tag, (name, ncols, b, t, m) in HIGHORDER.items():
+        x = highorder_input(tag)
+        cs = bc.cumulants_upto(x, m, b=b)
+        out[f"{tag}_xsum"] = np.array([x.sum(), (x * x).sum(), np.abs(x).max()])
+        out[f"{tag}_c1"] = cs[1]
+        rng = np.random.default_rng(123)
+        for k in range(2, m + 1):
+            flat = packed(cs[k])
+            idx = np.sort(rng.choice(flat.size, size=min(4096, flat.size), replace=False))
+            out[f"{tag}_c{k}_idx"] = idx.astype(np.int64)
+            out[f"{tag}_c{k}_val"] = flat[idx]
+            blocks = list(cs[k].blocks.values())
+            out[f"{tag}_c{k}_bsum"] = np.array([blk.sum() for blk in blocks])
+            out[f"{tag}_c{k}_bsq"] = np.array([(blk * blk).sum() for blk in blocks])
+            out[f"{tag}_c{k}_bmax"] = np.array([np.abs(blk).max() for blk in blocks])
+        print("  ", tag, "done", flush=True)
+    np.savez_compressed(os.path.join(HERE, "highorder.npz"), **out)
+
+
 if __name__ == "__main__":
     import time
 
+    only = sys.argv[1:]
     for fn in (layout_fixture, partitions_fixture, moments_fixture,
-               cumulants_fixture, configs_fixture):
+               cumulants_fixture, configs_fixture, highorder_fixture):
+        if only and fn.__name__ not in only:
+            continue
         t0 = time.time()
         fn()
         print(fn.__name__, f"{time.time() - t0:.1f}s", flush=True)

@@ -130,3 +130,70 @@ def test_live_differential_against_the_reference(name, t, m):
         for key in lay_keys:
             np.testing.assert_allclose(got[k].blocks[key], want[k].blocks[key], rtol=1e-9, atol=1e-12,
                                        err_msg=f"{name} C{k} block {key}")
+
+
+@pytest.mark.parametrize("name,t", [("cfg2", 20000), ("cfg4", 1500)])
+def test_reference_runs_on_the_gpu_through_the_dropin(name, t, monkeypatch):
+    """INTEGRATION.md A for real: the unmodified reference with its compiled
+    module switched to core_dropin (the one-line change at bc/_engines.py:
+    26-31) runs its own cumulants_upto(engine="compiled") and its threaded
+    moment_parallel_blocks(p=4) (bc/moments.py:99-131, concurrent key ranges
+    into one shared buffer) on the B200; results match the unpatched reference
+    at 1e-9."""
+    import workloads
+    from paper_1701_05420_b200 import core_dropin
+
+    bc = _reference_package()
+    if bc is None:
+        pytest.skip("reference not built (oracle/build_ref.sh)")
+    cfg = workloads.CONFIGS[name]
+    x = workloads.generate(name, t)
+    want_cs = bc.cumulants_upto(x, cfg.m, b=cfg.b, engine="compiled")
+    want_pb = bc.moment_parallel_blocks(x, cfg.m, cfg.b, p=4, engine="compiled")
+    engines = sys.modules[bc.__name__ + "._engines"]
+    calls = []
+
+    class Counting:
+        def moment_blocks(self, *a):
+            calls.append(a[-2:])
+            core_dropin.moment_blocks(*a)
+
+        naive_moment4 = staticmethod(core_dropin.naive_moment4)
+
+    monkeypatch.setattr(engines, "_core", Counting())
+    got_cs = bc.cumulants_upto(x, cfg.m, b=cfg.b, engine="compiled")
+    n_cs = len(calls)
+    got_pb = bc.moment_parallel_blocks(x, cfg.m, cfg.b, p=4, engine="compiled")
+    assert n_cs == cfg.m - 1 and len(calls) == n_cs + 4  # one call per order; p key ranges
+    np.testing.assert_allclose(got_cs[1], want_cs[1], rtol=1e-12)
+    for k in range(2, cfg.m + 1):
+        for key, blk in want_cs[k].blocks.items():
+            np.testing.assert_allclose(got_cs[k].blocks[key], blk, rtol=1e-9, atol=1e-12, err_msg=f"C{k} {key}")
+    for key, blk in want_pb.blocks.items():
+        np.testing.assert_allclose(got_pb.blocks[key], blk, rtol=1e-12, atol=1e-14, err_msg=f"M{cfg.m} {key}")
+
+
+def test_moment_blocks_wide_data_accumulates(rng):
+    """n above the moment kernel's one-stage limit (WIDE_N): the drop-in
+    routes through the variable-group decomposition with the same
+    accumulate semantics and key ranges (partial last block: 745 = 106 * 7 + 3)."""
+    from paper_1701_05420_b200 import core_dropin
+
+    n, m, b, t = 745, 2, 7, 150
+    x = rng.standard_normal((t, n))
+    xt = np.ascontiguousarray(x.T)
+    keys, col0, edges, offs = (np.asarray(a) for a in orc.block_layout(n, m, b))
+    col0 = np.ascontiguousarray(col0, dtype=np.int64)
+    edges = np.ascontiguousarray(edges, dtype=np.int64)
+    offs = np.ascontiguousarray(offs, dtype=np.int64)
+    K = col0.shape[0]
+    prior = rng.standard_normal(int(offs[-1]))
+    out = prior.copy()
+    k0, k1 = K // 3, K - 5
+    core_dropin.moment_blocks(xt, col0, edges, out, offs, k0, k1)
+    want = prior.copy()
+    lo, hi = int(offs[k0]), int(offs[k1])
+    want[lo:hi] += orc.moment_raw_sums(x, m, b, key_range=(k0, k1))[lo:hi]
+    np.testing.assert_allclose(out, want, rtol=1e-12, atol=1e-11)
+    np.testing.assert_array_equal(out[:lo], prior[:lo])
+    np.testing.assert_array_equal(out[hi:], prior[hi:])

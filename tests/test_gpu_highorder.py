@@ -1,0 +1,230 @@
+"""Heavy-tailed data to order 6: where the cumulant recursion cancels hardest.
+
+The Student-t(5) copula of BASELINE cfg2 / cfg5 has no finite 6th moment, so
+the sample C_5 / C_6 are differences of large, nearly equal sums.  Three
+checks, all at the reference's 1e-9 criterion (pkg/tests/test_acceptance.py:
+44-66; north_star "within 1e-9 relative error"):
+
+* against the reference itself (tests/golden/highorder.npz, made by
+  make_golden.py from the unmodified package): the cfg5 recipe's first 36
+  columns at b = 6 and the cfg2 recipe's first 32 columns at b = 8, to order 6
+  -- sampled elements plus per-block sums / sums of squares over every element;
+* the factored recursion kernel (csrc/recursion_fact.cu, production for full
+  blocks) against the reference's partition sum (csrc/recursion.cu, forced by
+  BCG_RECURSION_PARTITION=1 in a subprocess) on the same data;
+* the full cfg5 layout (n = 96, b = 6, 54,264 order-6 blocks): sampled blocks
+  of C_4, C_5, C_6 recomputed on the host from the centered data -- each
+  block's central moment by a Khatri-Rao GEMM and the partition sum over the
+  reference's own partition list (bc/cumulants.py:53-136), with every lower
+  cumulant block it reads also recomputed on the host.
+Worst floored relative errors are written to $BCG_HIGHORDER_LOG when set.
+"""
+
+import itertools
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1701_05420_b200 as bcg  # noqa: E402
+from paper_1701_05420_b200.layout import enumerate_partitions_min2, layout  # noqa: E402
+import workloads  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HIGHORDER = {"cfg5s": ("cfg5", 36, 6, 3000, 6), "cfg2s": ("cfg2", 32, 8, 3000, 6)}  # = make_golden.HIGHORDER
+RTOL, ATOL = 1e-9, 1e-12
+
+
+def highorder_input(tag):
+    name, ncols, _, t, _ = HIGHORDER[tag]
+    return np.ascontiguousarray(workloads.generate(name, t)[:, :ncols])
+
+
+def _log(record):
+    path = os.environ.get("BCG_HIGHORDER_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(record) + "\n")
+
+
+def floored_rel(got, want, floor):
+    return float(np.max(np.abs(got - want) / np.maximum(np.abs(want), floor)))
+
+
+@pytest.mark.parametrize("tag", sorted(HIGHORDER))
+def test_heavy_tails_to_order_6_match_the_reference(tag, golden):
+    g = golden("highorder.npz")
+    _, _, b, _, m = HIGHORDER[tag]
+    x = highorder_input(tag)
+    np.testing.assert_allclose([x.sum(), (x * x).sum(), np.abs(x).max()], g[f"{tag}_xsum"], rtol=1e-13)
+    cs = bcg.cumulants_upto(x, m, b=b)
+    np.testing.assert_allclose(cs[1], g[f"{tag}_c1"], rtol=1e-12, atol=1e-15)
+    for k in range(2, m + 1):
+        flat = cs[k].packed_host()
+        idx, want = g[f"{tag}_c{k}_idx"], g[f"{tag}_c{k}_val"]
+        np.testing.assert_allclose(flat[idx], want, rtol=RTOL, atol=ATOL, err_msg=f"{tag} C{k}")
+        # every element, through per-block sums and sums of squares: an
+        # element-wise |a - b| <= rtol |b| + atol bounds the block sums by
+        # Cauchy-Schwarz (size = elements per block)
+        lay = layout(x.shape[1], k, b)
+        sizes = np.diff(lay.offs)
+        seg = np.repeat(np.arange(lay.K), sizes)
+        bsum = np.bincount(seg, weights=flat, minlength=lay.K)
+        bsq = np.bincount(seg, weights=flat * flat, minlength=lay.K)
+        ws, wq = g[f"{tag}_c{k}_bsum"], g[f"{tag}_c{k}_bsq"]
+        tol_s = RTOL * np.sqrt(sizes * wq) + ATOL * sizes
+        tol_q = 2.1 * RTOL * wq + 3 * ATOL * np.sqrt(sizes * wq) + sizes * ATOL * ATOL
+        assert np.all(np.abs(bsum - ws) <= tol_s), f"{tag} C{k} block sums"
+        assert np.all(np.abs(bsq - wq) <= tol_q), f"{tag} C{k} block sums of squares"
+        _log({"test": "vs_reference", "case": tag, "order": k,
+              "worst_floored_rel_sampled": floored_rel(flat[idx], want, 1e-3 * np.abs(want).max()),
+              "worst_blocksum_over_tol": float(np.max(np.abs(bsum - ws) / tol_s))})
+
+
+_PARTITION_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import paper_1701_05420_b200 as bcg
+from test_gpu_highorder import highorder_input, HIGHORDER
+import workloads
+cases = {cases!r}
+out = {{}}
+for name, (kind, arg) in cases.items():
+    if kind == "tag":
+        x = highorder_input(arg); b, m = HIGHORDER[arg][2], HIGHORDER[arg][4]
+    else:
+        n, m, b, t, seed = arg
+        rng = np.random.default_rng(seed)
+        x = rng.exponential(1.0, size=(t, n)) + rng.standard_normal((t, n))
+    cs = bcg.cumulants_upto(x, m, b=b)
+    for k in range(4, m + 1):
+        out[f"{{name}}_c{{k}}"] = cs[k].packed_host()
+np.savez({path!r}, **out)
+"""
+
+
+def test_factored_recursion_matches_the_partition_sum(tmp_path):
+    """K3 factored (production) vs the reference's partition sum (the same
+    moments; BCG_RECURSION_PARTITION=1 is read once per process, hence the
+    subprocess), on heavy-tailed order-6 data and small shapes incl. partial
+    edges (those blocks run the partition kernel in both)."""
+    cases = {"cfg5s": ("tag", "cfg5s"), "cfg2s": ("tag", "cfg2s")}
+    for i, (n, m, b, t) in enumerate([(9, 4, 3, 500), (8, 5, 2, 400), (7, 6, 1, 300), (6, 6, 2, 500),
+                                      (12, 6, 3, 600), (7, 6, 3, 500), (10, 5, 4, 700)]):
+        cases[f"s{i}"] = ("shape", (n, m, b, t, 1000 + i))
+    files = {}
+    for mode in ("factored", "partition"):
+        path = str(tmp_path / f"{mode}.npz")
+        code = _PARTITION_CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"), cases=cases, path=path)
+        env = dict(os.environ)
+        env.pop("BCG_RECURSION_PARTITION", None)
+        if mode == "partition":
+            env["BCG_RECURSION_PARTITION"] = "1"
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-3000:]
+        files[mode] = np.load(path)
+    fa, pa = files["factored"], files["partition"]
+    assert sorted(fa.files) == sorted(pa.files)
+    for key in fa.files:
+        a, p = fa[key], pa[key]
+        np.testing.assert_allclose(a, p, rtol=RTOL, atol=ATOL, err_msg=key)
+        _log({"test": "factored_vs_partition", "case": key,
+              "worst_floored_rel": floored_rel(a, p, 1e-3 * np.abs(p).max()),
+              "bitwise_equal_fraction": float(np.mean(a == p))})
+
+
+# ------------------------------------------------------------------ full cfg5 layout
+
+
+class HostCumulants:
+    """Host recomputation of single cumulant blocks from centered data:
+    M[key] by a Khatri-Rao GEMM over the samples, C[key] = M[key] - sum over
+    the reference's min-2 partitions (sigma ascending, bc/cumulants.py:119-136)
+    of outer products of lower cumulant blocks, themselves recomputed here."""
+
+    def __init__(self, xc, b):
+        self.xc, self.b, self.t = xc, b, xc.shape[0]
+        self.cache = {}
+
+    def cols(self, j):
+        return self.xc[:, (j - 1) * self.b: j * self.b]
+
+    def kr(self, key):
+        w = np.ones((self.t, 1))
+        for j in key:
+            c = self.cols(j)
+            w = (w[:, :, None] * c[:, None, :]).reshape(self.t, -1)
+        return w
+
+    def moment(self, key):
+        h = len(key) // 2
+        wl, wr = self.kr(key[:h]), self.kr(key[h:])
+        return (wl.T @ wr).reshape((self.b,) * len(key)) / self.t
+
+    def cumulant(self, key):
+        key = tuple(key)
+        if key in self.cache:
+            return self.cache[key]
+        m = len(key)
+        c = self.moment(key)
+        letters = "abcdefghijklmnop"[:m]
+        for sigma in range(2, m // 2 + 1):
+            for parts in enumerate_partitions_min2(m, sigma):
+                ops = [self.cumulant(tuple(key[q - 1] for q in part)) for part in parts]
+                spec = ",".join("".join(letters[q - 1] for q in part) for part in parts) + "->" + letters
+                c = c - np.einsum(spec, *ops)
+        self.cache[key] = c
+        return c
+
+
+def test_cfg5_full_layout_sampled_blocks():
+    cfg = workloads.CONFIGS["cfg5"]
+    t = 8192
+    x = workloads.generate("cfg5", t)
+    cs = bcg.cumulants_upto(x, 6, b=cfg.b)
+    host = HostCumulants(x - x.mean(axis=0), cfg.b)
+    rng = np.random.default_rng(5)
+    nb = cfg.n // cfg.b
+    for k, nkeys in ((4, 48), (5, 48), (6, 48)):
+        lay = layout(cfg.n, k, cfg.b)
+        # half the keys with repeated block indices (the symmetric plan fills
+        # their permuted copies), half drawn uniformly
+        rep = [i for i in rng.choice(lay.K, 4 * nkeys, replace=False)
+               if len(set(lay.keys[i])) < k][: nkeys // 2]
+        ids = sorted(set(rep) | set(rng.choice(lay.K, nkeys - len(rep), replace=False).tolist()))
+        data = cs[k].data
+        worst = 0.0
+        for i in ids:
+            key = tuple(int(j) for j in lay.keys[i])
+            got = data[int(lay.offs[i]):int(lay.offs[i + 1])].cpu().numpy().reshape((cfg.b,) * k)
+            want = host.cumulant(key)
+            np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL, err_msg=f"C{k} block {key}")
+            worst = max(worst, floored_rel(got, want, 1e-3 * np.abs(want).max()))
+        _log({"test": "cfg5_layout_sampled_blocks", "order": k, "blocks": len(ids), "t": t, "n": cfg.n,
+              "b": cfg.b, "worst_floored_rel": worst})
+    # the fully diagonal blocks (j, ..., j) have the most permuted copies:
+    # the moment is exactly symmetric there (the symmetric plan copies one
+    # computed element to all its permutations); the cumulant to rounding
+    # (the recursion forms each element's products in its own order, as the
+    # reference does)
+    m5 = bcg.moment(bcg.center(x), 5, cfg.b)
+    for k in (5, 6):
+        lay = layout(cfg.n, k, cfg.b)
+        for j in (1, nb):
+            i = lay.key_index((j,) * k)
+            got = cs[k].data[int(lay.offs[i]):int(lay.offs[i + 1])].cpu().numpy().reshape((cfg.b,) * k)
+            np.testing.assert_allclose(got, host.cumulant((j,) * k), rtol=RTOL, atol=ATOL)
+            mom = m5.blocks[(j,) * 5] if k == 5 else None
+            for perm in itertools.islice(itertools.permutations(range(k)), 1, 24):
+                np.testing.assert_allclose(got, got.transpose(perm), rtol=1e-12, atol=1e-14)
+                if mom is not None:
+                    np.testing.assert_array_equal(mom, mom.transpose(perm))

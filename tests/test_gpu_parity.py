@@ -371,13 +371,12 @@ def test_moment_kernel_ragged_shapes_match_oracle(rng):
 
 @pytest.mark.parametrize("n,m,b,t", [(9, 4, 3, 500), (8, 5, 2, 400), (7, 6, 1, 300), (6, 6, 2, 500), (12, 6, 3, 600),
                                      (7, 6, 3, 500), (10, 5, 4, 700)])
-def test_factored_recursion_matches_partition_sum(n, m, b, t, rng, monkeypatch):
-    """K3 v2 (factored, full blocks) vs K3 v1 (the reference's partition sum)
-    vs the oracle, incl. partial-edge blocks (n % b != 0)."""
+def test_factored_recursion_matches_oracle(n, m, b, t, rng):
+    """K3 factored (full blocks) + partition kernel (partial-edge blocks) vs
+    the oracle.  The kernel-vs-kernel A/B on the same moments is
+    test_gpu_highorder.test_factored_recursion_matches_the_partition_sum."""
     x = rng.exponential(1.0, size=(t, n)) + rng.standard_normal((t, n))
     fact = bcg.cumulants_upto(x, m, b=b)
-    monkeypatch.setenv("BCG_RECURSION_PARTITION", "1")
-    # fresh process-wide knob is read once; use the C ABI directly for the A/B
     _, want = orc.cumulants_upto(x, m, b)
     for k in range(2, m + 1):
         np.testing.assert_allclose(packed(fact[k]), want[k], rtol=1e-9, atol=1e-12)
@@ -610,7 +609,7 @@ def _gloo_gpu_worker(rank, world, port, x, m, b, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("t,n,m,b", [(5001, 9, 6, 3), (3000, 16, 4, 8)])
+@pytest.mark.parametrize("t,n,m,b", [(5001, 9, 6, 3), (3000, 16, 4, 8), (300, 745, 2, 7)])
 def test_two_ranks_on_one_gpu_over_gloo(t, n, m, b, tmp_path, rng):
     """World size 2 through the real CUDA per-rank ops (both ranks on cuda:0,
     host-staged gloo collectives, so no kernel waits on another rank): the
@@ -663,7 +662,8 @@ def test_single_order_cumulant_api_matches_oracle(n, m, b, t, rng):
     np.testing.assert_allclose(packed(got), packed(cs[m]), rtol=1e-9, atol=1e-12)
 
 
-@pytest.mark.parametrize("n,m,b,t", [(800, 2, 4, 300), (1500, 2, 1, 200), (760, 3, 40, 150), (731, 2, 731, 100)])
+@pytest.mark.parametrize("n,m,b,t", [(800, 2, 4, 300), (1500, 2, 1, 200), (760, 3, 40, 150), (731, 2, 731, 100),
+                                     (731, 2, 3, 200), (745, 3, 7, 120)])
 def test_wider_than_one_stage(n, m, b, t, rng):
     """n > 720 variables (one sample chunk of all of them no longer fits the
     kernel's shared-memory stage): the variable-group decomposition against

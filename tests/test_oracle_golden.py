@@ -128,3 +128,21 @@ def test_dense_roundtrip_and_dense_moment(rng):
     for m in (2, 3, 4):
         dense = orc.packed_to_dense(orc.moment(x, m, 2), 5, m, 2)
         np.testing.assert_allclose(dense, orc.dense_moment(x, m), rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("tag", ["cfg5s", "cfg2s"])
+def test_highorder_fixture_inputs_and_low_orders(tag, golden):
+    """tests/golden/highorder.npz (heavy tails to order 6, made by the
+    reference): the recipe regenerates its input bit for bit, and the oracle
+    matches the reference's C1..C4 there (C5/C6 are checked on the GPU,
+    tests/test_gpu_highorder.py)."""
+    g = golden("highorder.npz")
+    spec = {"cfg5s": ("cfg5", 36, 6, 3000), "cfg2s": ("cfg2", 32, 8, 3000)}[tag]
+    name, ncols, b, t = spec
+    x = np.ascontiguousarray(workloads.generate(name, t)[:, :ncols])
+    np.testing.assert_allclose([x.sum(), (x * x).sum(), np.abs(x).max()], g[f"{tag}_xsum"], rtol=1e-13)
+    c1, cs = orc.cumulants_upto(x, 4, b)
+    np.testing.assert_allclose(c1, g[f"{tag}_c1"], rtol=1e-12, atol=1e-15)
+    for k in range(2, 5):
+        idx = g[f"{tag}_c{k}_idx"]
+        np.testing.assert_allclose(cs[k][idx], g[f"{tag}_c{k}_val"], rtol=1e-9, atol=1e-12)
