@@ -233,6 +233,18 @@ int bcg_cumulant_recursion_ex(const bcg_plan *plan, double *mk,
                               const double *const *cmom, int64_t k0,
                               int64_t k1, void *stream);
 
+/* Same, for the ELEMENTS mk[e0, e1) only (everything else untouched): the
+ * element-balanced split of the top orders across GPUs, where each rank holds
+ * the fully reduced M_m on an equal-size span of the packed buffer (an
+ * in-place NCCL reduce-scatter) -- the per-element recursion needs nothing
+ * else.  Blocks inside the span take the bcg_cumulant_recursion_ex kernels;
+ * the at most two blocks the span cuts take the partition kernel with
+ * writes masked to the span. */
+int bcg_cumulant_recursion_span(const bcg_plan *plan, double *mk,
+                                const double *const *lower,
+                                const double *const *cmom, int64_t e0,
+                                int64_t e1, void *stream);
+
 /* Same correction without the moment: out = B_sigma (bc/cumulants.py:53-84,
  * `outer_prod_cum(m, sigma, lower)`), out has S_m elements. */
 int bcg_outer_prod_cum(const bcg_plan *plan, int32_t sigma,

@@ -63,6 +63,7 @@ SIGNATURES = [
     ("bcg_cumulant_recursion", ctypes.c_int, [_vp, _vp, _vp, _vp]),
     ("bcg_cumulant_recursion_range", ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
     ("bcg_cumulant_recursion_ex", ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _vp]),
+    ("bcg_cumulant_recursion_span", ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _vp]),
     ("bcg_outer_prod_cum", ctypes.c_int, [_vp, _i32, _vp, _vp, _vp]),
     ("bcg_axpby", ctypes.c_int, [_i64, _dbl, _vp, _dbl, _vp, _vp, _vp]),
     ("bcg_div", ctypes.c_int, [_i64, _vp, _dbl, _vp, _vp]),

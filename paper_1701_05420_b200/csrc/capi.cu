@@ -532,7 +532,8 @@ int bcg_moment_blocks(const double *xt, int64_t n, int64_t t, const int64_t *col
 }
 
 static int recursion_common(const bcg_plan *plan, double *mk, const double *const *lower, int mode, int sigma_lo,
-                            int sigma_hi, int64_t k0, int64_t k1, cudaStream_t s, const int32_t *klist = nullptr) {
+                            int sigma_hi, int64_t k0, int64_t k1, cudaStream_t s, const int32_t *klist = nullptr,
+                            int64_t e0 = 0, int64_t e1 = INT64_MAX) {
   const bcg::Plan &p = plan->p;
   if (!p.d_offs) return fail(BCG_EINVAL, "host-only plan");
   bcg::RecursionArgs a{};
@@ -563,6 +564,8 @@ static int recursion_common(const bcg_plan *plan, double *mk, const double *cons
   }
   a.mk = mk;
   a.mode = mode;
+  a.e0 = e0;
+  a.e1 = e1;
   a.k0 = std::max<int64_t>(0, k0);
   a.k1 = std::min<int64_t>(a.K, k1);
   a.klist = klist;
@@ -625,6 +628,37 @@ int bcg_cumulant_recursion_ex(const bcg_plan *plan, double *mk, const double *co
                               const double *const *cmom, int64_t k0, int64_t k1, void *stream) {
   if (!plan) return fail(BCG_EINVAL, "plan is NULL");
   return recursion_dispatch(plan, mk, lower, cmom, k0, k1, static_cast<cudaStream_t>(stream));
+}
+
+int bcg_cumulant_recursion_span(const bcg_plan *plan, double *mk, const double *const *lower,
+                                const double *const *cmom, int64_t e0, int64_t e1, void *stream) {
+  if (!plan) return fail(BCG_EINVAL, "plan is NULL");
+  const bcg::Plan &p = plan->p;
+  if (p.m <= 3) return BCG_OK;
+  const auto &offs = p.lay[p.m].offs;
+  const int64_t K = p.lay[p.m].K;
+  e0 = std::max<int64_t>(e0, 0);
+  e1 = std::min<int64_t>(e1, offs[K]);
+  if (e1 <= e0) return BCG_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // blocks entirely inside the span: the regular dispatch (factored kernel)
+  const int64_t ka = std::lower_bound(offs.begin(), offs.end(), e0) - offs.begin();         // offs[ka] >= e0
+  const int64_t kb = std::upper_bound(offs.begin(), offs.end(), e1) - offs.begin() - 1;     // offs[kb] <= e1
+  if (kb > ka) {
+    const int rc = recursion_dispatch(plan, mk, lower, cmom, ka, kb, s);
+    if (rc) return rc;
+  }
+  // the (at most two) blocks cut by the span's ends: partition kernel with
+  // writes masked to [e0, e1)
+  int64_t cut[2] = {-1, -1};
+  if (offs[ka] > e0) cut[0] = ka - 1;                          // block holding e0
+  if (kb < K && offs[kb] < e1 && kb != cut[0]) cut[1] = kb;    // block holding e1 - 1
+  for (int64_t k : cut) {
+    if (k < 0) continue;
+    const int rc = recursion_common(plan, mk, lower, 0, 2, p.m / 2, k, k + 1, s, nullptr, e0, e1);
+    if (rc) return rc;
+  }
+  return BCG_OK;
 }
 
 int bcg_outer_prod_cum(const bcg_plan *plan, int32_t sigma, const double *const *lower, double *out, void *stream) {

@@ -93,6 +93,7 @@ struct RecursionArgs {
   const double *lower[16];  // index = order
   double *mk;               // in/out
   int mode;                 // 0: mk = mk - sum_sigma B_sigma ; 1: mk = B_sigma (single sigma)
+  int64_t e0, e1;           // only elements mk[e0 .. e1) are written (element-span split)
 };
 cudaError_t launch_recursion(const RecursionArgs &args, cudaStream_t stream);
 

@@ -55,13 +55,15 @@ __global__ void __launch_bounds__(256) k_recursion(RecursionArgs a) {
   __syncthreads();
   int64_t E = 1;
   for (int q = 0; q < m; ++q) E *= edges[q];
-  double *blk = a.mk + a.offs[k];
+  double *blk = a.mk + a.offs[k];  // (boff below)
   // first slot of p_begin
   int slot0 = 0;
   for (int p = 0; p < a.p_begin; ++p)
     for (int i = 0; i < 8; ++i) slot0 += a.part_mask[p * 8 + i] != 0;
 
+  const int64_t boff = a.offs[k];
   for (int64_t e = tid; e < E; e += blockDim.x) {
+    if (boff + e < a.e0 || boff + e >= a.e1) continue;  // outside this caller's element span
     int o[16];
     int64_t rem = e;
     for (int q = m - 1; q >= 0; --q) {

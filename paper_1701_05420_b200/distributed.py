@@ -14,15 +14,19 @@ The paper's Alg. 3 and the reference's ``moment_parallel``
      / t_total -> every rank runs the (microsecond-scale) recursion on all
      blocks, so C_k (and the central moment M_k the factored recursion needs)
      is replicated without a second collective;
-   * the two top orders (k >= m-1, k >= 4): reduce-scatter by block range
-     (bc/moments.py:114-131 split) -> / t_total -> recursion on the rank's
-     own blocks -> all-gather: 2x the packed size on the wire instead of the
-     3x of all-reduce + all-gather (cfg5: C6 is 20 GB).
+   * the two top orders (k >= m-1, k >= 4): the packed buffer is padded to
+     world equal element spans; an in-place NCCL reduce-scatter leaves each
+     rank its span fully reduced -> / t_total -> the recursion on that span
+     (per element it reads only its own M_k element and the replicated lower
+     orders; the at most two blocks a span cuts run with masked writes) ->
+     an in-place all-gather: 2x the packed size on the wire instead of the 3x
+     of all-reduce + all-gather, and no staging copy of the packed tensor
+     (cfg5: C6 is 20 GB).
 
 **Block split** (``cumulants_upto_block_split``; ``moment_parallel_blocks``,
 bc/moments.py:99-131, across GPUs).  Every rank holds ALL of X; rank r
-computes blocks [K r/W, K (r+1)/W) of every order (moment + recursion) and an
-all-gather per order rebuilds C_k.  No moment collective, no partial M_k per
+computes blocks [K r/W, K (r+1)/W) of every order (moment + recursion) and one
+in-place broadcast per rank of its block range rebuilds C_k.  No moment collective, no partial M_k per
 GPU (cfg5: 20 GB less per GPU), X read W times in total; results bitwise equal
 to the single-GPU path (every key range of the moment kernel sums in the same
 order).
@@ -91,18 +95,20 @@ class CudaOps:
 
         return _rowstats(*centered)
 
-    def moment_raw(self, centered, k: int, b: int, key_range=None):
+    def moment_raw(self, centered, k: int, b: int, key_range=None, size=None):
         """Packed RAW order-k sums (all blocks, or blocks [k0, k1) only; the
-        rest of the buffer stays zero)."""
+        rest of the buffer stays zero) in a buffer of ``size`` >= S_k
+        elements (zero past S_k: padding for the equal-span collectives)."""
         from . import _native
 
         from .moments import WIDE_N, _moment_raw_wide
 
         xt, t = centered
         n, ldt = xt.shape
-        out = torch.zeros(layout(n, k, b).size, dtype=torch.float64, device=xt.device)
+        S = layout(n, k, b).size
+        out = torch.zeros(max(S, size or 0), dtype=torch.float64, device=xt.device)
         if n > WIDE_N:
-            _moment_raw_wide(xt, t, k, b, out, key_range)
+            _moment_raw_wide(xt, t, k, b, out[:S], key_range)
             return out
         plan = _native.plan(n, k, b)
         wsb = plan.t_ws_bytes(t)  # split-K partials only: xt is already transposed
@@ -122,6 +128,28 @@ class CudaOps:
         from .moments import _divide
 
         _divide(buf, t)
+
+    @staticmethod
+    def _pointer_arrays(lower: dict, central, k: int):
+        import ctypes
+
+        arr = (ctypes.c_void_p * 15)()
+        for j, t in lower.items():
+            arr[j - 2] = t.data_ptr()
+        cm = (ctypes.c_void_p * 15)()
+        for j, t in (central or {}).items():
+            if 4 <= j <= k - 2:
+                cm[j - 2] = t.data_ptr()
+        return arr, cm
+
+    def recursion_span(self, mk, n: int, k: int, b: int, lower: dict, e0: int, e1: int, central=None):
+        """C_k in place on the ELEMENTS mk[e0:e1) (bcg_cumulant_recursion_span)."""
+        from . import _native
+
+        plan = _native.plan(n, k, b)
+        arr, cm = self._pointer_arrays(lower, central, k)
+        _native.check(_native.lib().bcg_cumulant_recursion_span(
+            plan.handle, mk.data_ptr(), arr, cm, int(e0), int(e1), _native.stream_handle()), "recursion")
 
     def recursion_range(self, mk, n: int, k: int, b: int, lower: dict, k0: int, k1: int, central=None):
         """C_k in place on blocks [k0, k1) of the packed M_k.  ``central``
@@ -196,7 +224,12 @@ def cumulants_upto_sharded(x_local, m_max: int, b: int = 2, group=None, ops=None
         # all moment GEMMs only read Xc: issue them up front (lower orders on
         # side streams), so each order's collective overlaps the GEMMs still
         # running -- the top order's in particular
-        early = _issue_moments(ops, Xc, m_max, b) if timer is None else {}
+        # the two top orders (k >= 4) are split by element span: their
+        # buffers are padded to world x span so the collectives run in place
+        S = {k: layout(n, k, b).size for k in range(2, m_max + 1)}
+        split = {k for k in range(4, m_max + 1) if world > 1 and k >= m_max - 1 and k not in keep}
+        size = {k: (_padded(S[k], world) if k in split else S[k]) for k in S}
+        early = _issue_moments(ops, Xc, m_max, b, size) if timer is None else {}
         for k in range(2, m_max + 1):
             top = k == m_max and timer is not None
             if top:
@@ -208,19 +241,20 @@ def cumulants_upto_sharded(x_local, m_max: int, b: int = 2, group=None, ops=None
                 if ev is not None:
                     torch.cuda.current_stream().wait_event(ev)
             else:
-                mk = ops.moment_raw(Xc, k, b)
+                mk = ops.moment_raw(Xc, k, b, size=size[k])
             if top:
                 ev1.record()
                 timer.setdefault("moment_top", []).append((ev0, ev1))
-            lay = layout(n, k, b)
-            if world > 1 and k >= 4 and k >= m_max - 1:
-                # top orders: reduce-scatter -> own blocks -> all-gather
-                k0, k1 = block_bounds(lay.K, world, rank)
-                _reduce_scatter_blocks(mk, lay, world, group)
-                lo, hi = int(lay.offs[k0]), int(lay.offs[k1])
-                ops.divide(mk[lo:hi], t_total)
-                ops.recursion_range(mk, n, k, b, lower, k0, k1, central)
-                _allgather_blocks(mk, lay, world, group)
+            if k in split:
+                # reduce-scatter (in place) -> this rank's element span fully
+                # reduced -> / t -> recursion on the span -> all-gather (in place)
+                c = size[k] // world
+                e0, e1 = rank * c, min((rank + 1) * c, S[k])
+                _reduce_scatter_inplace(mk, c, rank, group)
+                ops.divide(mk[e0:e1], t_total)
+                ops.recursion_span(mk, n, k, b, lower, e0, e1, central)
+                _all_gather_inplace(mk, c, rank, group)
+                mk = mk[:S[k]]
             else:
                 if world > 1:
                     dist.all_reduce(mk, group=group)
@@ -228,7 +262,7 @@ def cumulants_upto_sharded(x_local, m_max: int, b: int = 2, group=None, ops=None
                 if k in keep:
                     central[k] = mk.clone()
                 if k >= 4:
-                    ops.recursion_range(mk, n, k, b, lower, 0, lay.K, central)
+                    ops.recursion_range(mk, n, k, b, lower, 0, layout(n, k, b).K, central)
             lower[k] = mk
             tensors.append(mk)
     return mean, tensors
@@ -280,18 +314,18 @@ def cumulants_upto_block_split(x_full, m_max: int, b: int = 2, group=None, ops=N
                 # the factored recursion of higher orders reads the central
                 # moment of every block: gather it before correcting in place
                 if world > 1:
-                    _allgather_blocks(mk, lay, world, group)
+                    _broadcast_block_ranges(mk, lay, world, group)
                 central[k] = mk.clone()
             if k >= 4:
                 ops.recursion_range(mk, n, k, b, lower, k0, k1, central)
             if world > 1:
-                _allgather_blocks(mk, lay, world, group)
+                _broadcast_block_ranges(mk, lay, world, group)
             lower[k] = mk
             tensors.append(mk)
     return mean, tensors
 
 
-def _issue_moments(ops, centered, m_max: int, b: int) -> dict:
+def _issue_moments(ops, centered, m_max: int, b: int, size: dict) -> dict:
     """Orders 2..m-1 on per-order side streams, the top order on the current
     stream; returns {k: (raw sums, event or None)}.  CUDA ops only (the CPU
     test ops run serially); BCG_SERIAL_ORDERS=1 disables it."""
@@ -311,12 +345,12 @@ def _issue_moments(ops, centered, m_max: int, b: int) -> dict:
         side = _side_streams[key]
         side.wait_event(ready)
         with torch.cuda.stream(side):
-            mk = ops.moment_raw(centered, k, b)
+            mk = ops.moment_raw(centered, k, b, size=size[k])
             ev = torch.cuda.Event()
             ev.record(side)
         mk.record_stream(main)
         out[k] = (mk, ev)
-    out[m_max] = (ops.moment_raw(centered, m_max, b), None)
+    out[m_max] = (ops.moment_raw(centered, m_max, b, size=size[m_max]), None)
     return out
 
 
@@ -325,42 +359,51 @@ def _device_div(v, t, ops):
     return v
 
 
-def _block_spans(lay, world: int):
-    spans = []
+def _padded(S: int, world: int) -> int:
+    """Packed size rounded up to world equal element spans."""
+    return -(-S // world) * world
+
+
+def _nccl(group) -> bool:
+    return dist.get_backend(group) == "nccl"
+
+
+def _reduce_scatter_inplace(buf, c: int, rank: int, group) -> None:
+    """Sum ``buf`` (world x c elements) over ranks into this rank's span
+    buf[rank c : (rank + 1) c].  NCCL runs it in place (receive buffer = send
+    buffer + rank x count): no staging copy of the packed tensor.  (gloo, the
+    CPU tests' backend, gets a staging buffer.)"""
+    own = buf[rank * c:(rank + 1) * c]
+    if _nccl(group):
+        dist.reduce_scatter_tensor(own, buf, group=group)
+    else:
+        tmp = torch.empty_like(own)
+        dist.reduce_scatter_tensor(tmp, buf, group=group)
+        own.copy_(tmp)
+
+
+def _all_gather_inplace(buf, c: int, rank: int, group) -> None:
+    """Every rank's span of ``buf`` to every rank; NCCL in place (send
+    buffer = receive buffer + rank x count)."""
+    own = buf[rank * c:(rank + 1) * c]
+    if _nccl(group):
+        dist.all_gather_into_tensor(buf, own, group=group)
+    else:
+        tmp = torch.empty_like(buf)
+        dist.all_gather_into_tensor(tmp, own.clone(), group=group)
+        buf.copy_(tmp)
+
+
+def _broadcast_block_ranges(mk, lay, world: int, group) -> None:
+    """Rebuild the full packed tensor from each rank's block range: one
+    in-place broadcast per rank of its contiguous range (uneven ranges, no
+    padding, no staging copies)."""
     for r in range(world):
         k0, k1 = block_bounds(lay.K, world, r)
-        spans.append((int(lay.offs[k0]), int(lay.offs[k1])))
-    return spans
-
-
-def _reduce_scatter_blocks(mk, lay, world: int, group) -> None:
-    """Sum ``mk`` over ranks into this rank's block range only (the other
-    ranges are left stale; _allgather_blocks overwrites them)."""
-    spans = _block_spans(lay, world)
-    width = max(hi - lo for lo, hi in spans)
-    rank = dist.get_rank(group)
-    send = torch.zeros(width * world, dtype=mk.dtype, device=mk.device)
-    for r, (a, z) in enumerate(spans):
-        send[r * width: r * width + (z - a)] = mk[a:z]
-    recv = torch.empty(width, dtype=mk.dtype, device=mk.device)
-    dist.reduce_scatter_tensor(recv, send, group=group)
-    lo, hi = spans[rank]
-    mk[lo:hi] = recv[: hi - lo]
-
-
-def _allgather_blocks(mk, lay, world: int, group) -> None:
-    """Rebuild the full packed tensor from each rank's block range."""
-    spans = _block_spans(lay, world)
-    width = max(hi - lo for lo, hi in spans)
-    rank = dist.get_rank(group)
-    lo, hi = spans[rank]
-    send = torch.zeros(width, dtype=mk.dtype, device=mk.device)
-    send[: hi - lo] = mk[lo:hi]
-    recv = torch.empty(width * world, dtype=mk.dtype, device=mk.device)
-    dist.all_gather_into_tensor(recv, send, group=group)
-    for r, (a, z) in enumerate(spans):
-        if r != rank:
-            mk[a:z] = recv[r * width: r * width + (z - a)]
+        lo, hi = int(lay.offs[k0]), int(lay.offs[k1])
+        if hi > lo:
+            src = r if group is None else dist.get_global_rank(group, r)
+            dist.broadcast(mk[lo:hi], src=src, group=group)
 
 
 def to_cumulant_set(mean, tensors, n: int, b: int):

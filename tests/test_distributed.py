@@ -46,18 +46,26 @@ class OracleOps:
         s, q, _ = self.colstats(Xc)
         return s, q
 
-    def moment_raw(self, X, k, b, key_range=None):
+    def moment_raw(self, X, k, b, key_range=None, size=None):
         full = torch.as_tensor(orc.moment_raw_sums(X.numpy(), k, b))
+        out = torch.zeros(max(full.numel(), size or 0), dtype=full.dtype)
         if key_range is None:
-            return full
+            out[:full.numel()] = full
+            return out
         lay = layout(X.shape[1], k, b)
         lo, hi = int(lay.offs[key_range[0]]), int(lay.offs[key_range[1]])
-        out = torch.zeros_like(full)
         out[lo:hi] = full[lo:hi]
         return out
 
     def divide(self, buf, t):
         buf /= t
+
+    def recursion_span(self, mk, n, k, b, lower, e0, e1, central=None):
+        # element-wise: the elements outside [e0, e1) hold unreduced sums on
+        # this rank, but no element of the span reads them
+        S = layout(n, k, b).size
+        full = orc.cumulant_from_moment(mk[:S].numpy().copy(), k, {j: v.numpy() for j, v in lower.items()}, n, b)
+        mk[e0:e1] = torch.as_tensor(full[e0:e1])
 
     def recursion_range(self, mk, n, k, b, lower, k0, k1, central=None):
         full = orc.cumulant_from_moment(mk.numpy().copy(), k, {j: v.numpy() for j, v in lower.items()}, n, b)
@@ -92,7 +100,7 @@ def test_shard_and_block_bounds():
 
 
 @pytest.mark.parametrize("world,mode,m_max,b", [(2, "samples", 6, 2), (3, "samples", 5, 3), (2, "blocks", 6, 2),
-                                                (3, "blocks", 6, 3)])
+                                                (3, "blocks", 6, 3), (4, "samples", 6, 3), (3, "samples", 4, 2)])
 def test_sharded_cumulants_match_oracle(world, mode, m_max, b, tmp_path, rng):
     x = rng.exponential(1.0, size=(403, 5)) + rng.standard_normal((403, 5))
     port = _free_port()

@@ -678,3 +678,42 @@ def test_wider_than_one_stage(n, m, b, t, rng):
     cs = bcg.cumulants_upto(x, m, b=b)
     np.testing.assert_array_equal(packed(cs[m]), packed(bcg.moment(bcg.center(x), m, b)))
     np.testing.assert_array_equal(packed(bcg.moment_parallel_blocks(x, m, b, p=3)), got)
+
+
+@pytest.mark.parametrize("n,m,b,t", [(12, 6, 3, 700), (10, 5, 2, 500), (9, 4, 4, 400), (7, 6, 3, 300)])
+def test_recursion_on_element_spans(n, m, b, t, rng):
+    """bcg_cumulant_recursion_span (the per-rank step of the element-balanced
+    multi-GPU split): spans that cut blocks mid-way, applied to copies of the
+    same M_m, reassemble the full recursion; elements outside a span stay
+    untouched."""
+    import ctypes
+
+    from paper_1701_05420_b200.layout import layout
+
+    x = rng.exponential(1.0, (t, n)) + rng.standard_normal((t, n))
+    cs = bcg.cumulants_upto(x, m - 1, b=b)
+    xc = bcg.center(x)
+    mom = bcg.moment(xc, m, b).data
+    lower = (ctypes.c_void_p * 15)()
+    for k in range(2, m - 1):
+        lower[k - 2] = cs[k].data.data_ptr()
+    cm = (ctypes.c_void_p * 15)()
+    m4 = bcg.moment(xc, 4, b).data if m == 6 else None
+    if m4 is not None:
+        cm[2] = m4.data_ptr()
+    plan = _native.plan(n, m, b)
+    S = layout(n, m, b).size
+    full = mom.clone()
+    _native.check(_native.lib().bcg_cumulant_recursion_span(plan.handle, full.data_ptr(), lower, cm, 0, S,
+                                                            _native.stream_handle()))
+    cuts = [0, S // 3 + 1, S // 3 + 7, (2 * S) // 3 - 5, S]
+    got = torch.empty_like(mom)
+    for e0, e1 in zip(cuts, cuts[1:]):
+        part = mom.clone()
+        _native.check(_native.lib().bcg_cumulant_recursion_span(plan.handle, part.data_ptr(), lower, cm, e0, e1,
+                                                                _native.stream_handle()))
+        assert torch.equal(part[:e0], mom[:e0]) and torch.equal(part[e1:], mom[e1:])
+        got[e0:e1] = part[e0:e1]
+    np.testing.assert_allclose(got.cpu().numpy(), full.cpu().numpy(), rtol=1e-12, atol=1e-15)
+    _, want = orc.cumulants_upto(x, m, b)
+    np.testing.assert_allclose(got.cpu().numpy(), want[m], rtol=1e-9, atol=1e-12)
