@@ -11,14 +11,14 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbcgpu.so")
-SOURCES = ["plan.cu", "moment.cu", "elementwise.cu", "recursion.cu", "recursion_fact.cu", "capi.cu"]
+SOURCES = ["plan.cu", "moment.cu", "elementwise.cu", "recursion.cu", "recursion_fact.cu", "recursion_stream.cu", "capi.cu"]
 # moment.cu is compiled once per part: part 0 = host code + dispatch, parts
 # 1..6 = the kernel instantiations of one CTA tile shape each (parallel nvcc)
 # (recursion_fact.cu likewise: part 0 = dispatch, 1..6 = (m, b) instantiations)
 PARTS = {"moment.cu": ("BCG_MOMENT_PART", 7), "recursion_fact.cu": ("BCG_RF_PART", 7)}
 UNITS = [(s, []) for s in SOURCES if s not in PARTS] + [
     (s, [f"-D{d}={k}"]) for s, (d, n) in PARTS.items() for k in range(n)]
-HEADERS = ["plan.h", "kernels.h", "kr.cuh"]
+HEADERS = ["plan.h", "kernels.h", "kr.cuh", "rf_terms.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

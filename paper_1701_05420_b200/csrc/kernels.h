@@ -104,10 +104,14 @@ struct RecFactArgs {
   const double *cum[16];    // packed C_k, k = 2 .. m-2
   const double *cmom[16];   // packed central moments M_k, k = 4 .. m-2
   double *mk;               // in: M_m, out: C_m
+  const int32_t *order;     // v7 only: position -> work item (null: identity)
 };
 int recursion_fact_terms(int m);
 bool recursion_fact_supported(int m, int b);
 cudaError_t launch_recursion_fact(const RecFactArgs &a, int m, int b, cudaStream_t stream);
+// v7 (recursion_stream.cu): order 6, b = 6, every pointer 16-byte aligned
+bool recursion_stream6_supported(int b);
+cudaError_t launch_recursion_stream6(const RecFactArgs &a, int b, cudaStream_t stream);
 
 extern int64_t g_launches;
 

@@ -466,6 +466,18 @@ static void build_fact_tables(Plan &p) {
       p.term_off[(i * masks.size() + t) * 2 + 1] = (int32_t)p.lay[nc].offs[multiset_rank(c, nc, p.nbar)];
     }
   }
+  p.tail_order.clear();
+  if (m == 6) {
+    p.tail_order.resize(p.full_keys.size());
+    std::iota(p.tail_order.begin(), p.tail_order.end(), 0);
+    auto key_of = [&](int32_t i) { return &LM.keys[(int64_t)p.full_keys[i] * m]; };
+    std::stable_sort(p.tail_order.begin(), p.tail_order.end(), [&](int32_t x, int32_t y) {
+      const int64_t *a = key_of(x), *c = key_of(y);
+      for (int q = 1; q < m; ++q)
+        if (a[q] != c[q]) return a[q] < c[q];
+      return a[0] < c[0];
+    });
+  }
 }
 
 template <typename T>
@@ -501,6 +513,7 @@ std::string upload_plan(Plan &p) {
   UP(d_full_offs, full_offs);
   UP(d_full_keys, full_keys);
   UP(d_partial_keys, partial_keys);
+  UP(d_tail_order, tail_order);
   UP(d_fill_keys, fill_keys);
 #undef UP
   if (e == cudaSuccess) e = up(&p.d_offs, p.lay[p.m].offs);
@@ -521,7 +534,7 @@ void free_plan(Plan &p) {
       if (q) cudaFree(q);
   }
   void *ptrs[] = {p.d_offs, p.d_keys32, p.d_sub_rank, p.d_part_mask, p.d_koff, p.d_term_off,
-                  p.d_full_offs, p.d_full_keys, p.d_partial_keys, p.d_fill_keys};
+                  p.d_full_offs, p.d_full_keys, p.d_partial_keys, p.d_fill_keys, p.d_tail_order};
   for (void *q : ptrs)
     if (q) cudaFree(q);
   for (auto &q : p.d_lower_offs)

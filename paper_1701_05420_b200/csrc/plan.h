@@ -88,6 +88,10 @@ struct Plan {
   std::vector<int32_t> term_off;        // full blocks x terms x 2 factor-block element offsets
   std::vector<int64_t> full_offs;       // M_m element offset of each full block
   std::vector<int32_t> full_keys, partial_keys;  // blocks with all edges == b / the rest
+  // order-6 streamed recursion (recursion_stream.cu): work-list positions
+  // sorted by the key's modes 1..5 (blocks sharing them share every second
+  // factor), then by mode 0
+  std::vector<int32_t> tail_order;
 
   // --- device copies ---
   int64_t *d_offs = nullptr;           // offs of order m
@@ -98,6 +102,7 @@ struct Plan {
   int32_t *d_term_off = nullptr;
   int64_t *d_full_offs = nullptr;
   int32_t *d_full_keys = nullptr, *d_partial_keys = nullptr;
+  int32_t *d_tail_order = nullptr;
   int32_t *d_fill_keys = nullptr;
   int64_t *d_lower_offs[16] = {nullptr};  // offs of orders 2..m-2
 };

@@ -30,6 +30,7 @@
 #include <utility>
 
 #include "kernels.h"
+#include "rf_terms.cuh"
 
 #ifndef BCG_RF_PART
 #error "recursion_fact.cu is compiled once per BCG_RF_PART (0..6), see _build.py"
@@ -37,53 +38,7 @@
 
 namespace bcg {
 
-namespace rf {
-
-__host__ __device__ constexpr int popc(int x) { return x == 0 ? 0 : (x & 1) + popc(x >> 1); }
-__host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
-
-// terms: subsets S of {0..M-1} containing mode 0, 2 <= |S| <= M-2, by mask order
-__host__ __device__ constexpr int term_count(int M) {
-  int c = 0;
-  for (int s = 1; s < (1 << M); s += 2)
-    if (popc(s) >= 2 && popc(s) <= M - 2) ++c;
-  return c;
-}
-__host__ __device__ constexpr int term_mask(int M, int t) {
-  for (int s = 1; s < (1 << M); s += 2)
-    if (popc(s) >= 2 && popc(s) <= M - 2) {
-      if (t == 0) return s;
-      --t;
-    }
-  return 0;
-}
-// row-major stride of mode q inside the factor block over the modes in `mask`
-__host__ __device__ constexpr int stride_in(int mask, int q, int B) {
-  int later = 0;
-  for (int p = q + 1; p < 16; ++p)
-    if (mask & (1 << p)) ++later;
-  return ipow(B, later);
-}
-// compile-time offset contributed by the leading (register row) modes
-// 0..M-CT-1 for row index `row` (row-major)
-__host__ __device__ constexpr int head_offset(int mask, int M, int CT, int B, int row) {
-  int off = 0;
-  for (int q = M - CT - 1; q >= 0; --q) {
-    const int digit = row % B;
-    row /= B;
-    if (mask & (1 << q)) off += digit * stride_in(mask, q, B);
-  }
-  return off;
-}
-
-// the same, forced to a compile-time constant (keeps the unrolled row loops
-// cheap to compile: the offsets are folded by the front end)
-template <int MASK, int M, int CT, int B, int ROW>
-struct HeadOff {
-  static constexpr int value = head_offset(MASK, M, CT, B, ROW);
-};
-
-}  // namespace rf
+// rf:: term tables: rf_terms.cuh
 
 // cp.async (LDGSTS) helpers
 __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
@@ -543,9 +498,19 @@ static cudaError_t go_fact_v2(const RecFactArgs &a_in, cudaStream_t stream) {
 
 template <int M, int B>
 cudaError_t go_fact(const RecFactArgs &a, cudaStream_t stream) {
-  // A/B knob: BCG_RF_VARIANT=2 (v2), 3 (v3 staged), 6 (v6 slab-staged, m = 6)
+  // A/B knob: BCG_RF_VARIANT=2 (v2), 3 (v3 staged), 6 (v6 slab-staged, m = 6), 7 (v7 streamed, m = b = 6)
   static const int variant = getenv("BCG_RF_VARIANT") ? atoi(getenv("BCG_RF_VARIANT")) : 0;
   static const bool no_staged = getenv("BCG_RF_NO_STAGED") != nullptr || variant == 2 || variant == 6;
+  if constexpr (M == 6 && B == 6) {
+    // v7 (recursion_stream.cu): bulk-copy streamed, default where every
+    // factor / block pointer is 16-byte aligned
+    if (variant == 0 || variant == 7) {
+      bool aligned = ((uintptr_t)a.mk & 15) == 0;
+      for (int k = 2; k <= 4; ++k) aligned = aligned && ((uintptr_t)a.cum[k] & 15) == 0;
+      aligned = aligned && ((uintptr_t)a.cmom[4] & 15) == 0;
+      if (aligned) return launch_recursion_stream6(a, B, stream);
+    }
+  }
   if constexpr (M == 6 && Slab6<B>::ok) {
     if (variant == 6) {  // measured equal to v2 at cfg5, slower at cfg4 (profiles/r01_recursion_ncu.txt)
       if (a.nkeys <= 0) return cudaSuccess;

@@ -1,0 +1,431 @@
+// K3 (v7): order-6 cumulant recursion streamed by the bulk-copy engine, for
+// full blocks of even edge b (the cfg5 layout, b = 6).
+//
+// Same arithmetic as v2 (recursion_fact.cu, the factored form of the
+// reference's partition sum bc/cumulants.py:53-136):
+//
+//   C_6 = M_6 - sum_{S containing mode 0, 2 <= |S| <= 4} C_|S|[key|S] * M_{6-|S|}[key|rest]
+//
+// 25 terms, applied per element in the same order with the same fma(-f1, f2, acc)
+// as v2, so both kernels produce bitwise-identical C_6.
+//
+// Why: v2 reads its factors through L1 (50 GB of L2->L1 traffic per 20 GB of
+// M_6 at cfg5, 53% L1 hit, long-scoreboard stalls).  Here:
+//
+//   * persistent CTAs, one per SM, each over a contiguous run of the work
+//     list; the host orders the list by the key's modes 1..5 ("tail"), and
+//     blocks with equal tails share all 25 second factors;
+//   * a block is b slabs (mode-0 index i0), a slab b sub-slabs (mode-1 index
+//     i1) of b^4 elements; a "unit" is 2 sub-slabs (20.7 KB at b = 6), one
+//     contiguous run of M_6;
+//   * warp 0 streams units into an NS-stage shared-memory ring
+//     (cp.async.bulk, mbarrier complete_tx) and prefetches ahead into L2;
+//   * warp 1 streams the factors: per tail the 25 second factors (V: the
+//     sub-blocks not holding mode 0, 72 KB at b = 6), per slab the 25
+//     first-factor slices at i0 (U: 20 KB, NU buffers);
+//   * NGRP consumer groups: a group loads a unit's elements from its ring
+//     stage into registers and releases the stage at once, applies the 25
+//     terms reading every factor from shared memory, and stores C_6 straight
+//     from registers to HBM (streaming stores, in place over M_6).
+//
+// Register tile: a thread owns (b/2)^NRM elements: b/2 digits of each of
+// the NRM trailing modes, interleaved with 2 thread groups per mode
+// (index = 2 d + g), the other modes 2.. at thread level.  Splitting every
+// mode's range between registers and threads makes each term's two factors
+// split the tile (loads per term = 3^|S & tile| + 3^|rest & tile|): 0.33
+// (NRM = 4, 81 elements) / 0.54 (NRM = 3, 27 elements) shared-memory loads per
+// FMA, against v2's 0.64.  Interleaving keeps g5 lanes on adjacent doubles, so
+// a warp's store touches 16-byte runs, and the 16 lanes of a sub-slab hit
+// distinct double-banks on the ring loads.
+//
+// mbarrier phases: consumers release ring stages early and run ahead of each
+// other, so a "full" barrier is indexed such that its previous phase belongs
+// to the same consumer group (which has observed it complete): unit u ->
+// stage u % NS, full barrier u % lcm(NS, NGRP); slab s -> U buffer s % NU,
+// full barrier s % lcm(NU, slab period).  Otherwise a parity wait could pass
+// on a phase two behind.
+//
+// Roofline: HBM, 16 B per element (M_6 in, C_6 out) + every factor value once
+// per tail / slab (from L2).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+#include <utility>
+
+#include "kernels.h"
+#include "kr.cuh"  // BCG_CHECK
+#include "rf_terms.cuh"
+
+namespace bcg {
+
+namespace rs {
+
+using rf::ipow;
+using rf::popc;
+using rf::stride_in;
+using rf::term_count;
+using rf::term_mask;
+
+constexpr int gcd(int x, int y) { return y == 0 ? x : gcd(y, x % y); }
+constexpr int lcm(int x, int y) { return x / gcd(x, y) * y; }
+
+// geometry for order 6, edge B, NRM register modes (the trailing ones),
+// NGRP consumer groups
+template <int B, int RM, int NGRP, int NU_ = 3>
+struct Geo {
+  static constexpr int M = 6;
+  static constexpr int NT = term_count(M);  // 25
+  static constexpr int RG = B / 2;          // register digits per register mode
+  static constexpr int NRM = popc(RM);      // register modes (a subset of 2..5)
+  static constexpr int TPS = ipow(B, 4 - NRM) * ipow(2, NRM);  // threads per sub-slab
+  static constexpr int U1 = 2;                                 // sub-slabs per unit
+  static constexpr int GT = U1 * TPS;                          // threads per group
+  static constexpr int GW = GT / 32;                           // warps per group
+  static constexpr int ROWS = ipow(RG, NRM);                   // elements per thread
+  static constexpr int SUB = ipow(B, 4);                       // elements per sub-slab
+  static constexpr int UNIT = U1 * SUB;                        // elements per unit
+  static constexpr int UPS = B / U1;                           // units per slab
+  static constexpr int UPB = B * UPS;                          // units per block
+  static constexpr int NU = NU_;                               // U buffers
+  static constexpr int NTHREADS = 64 + NGRP * GT;
+  // second factor of term T (modes not holding 0): b^|rest| doubles at ov(T)
+  __host__ __device__ static constexpr int ov(int T) {
+    int o = 0;
+    for (int t = 0; t < T; ++t) o += ipow(B, M - popc(term_mask(M, t)));
+    return o;
+  }
+  // first factor of term T sliced at i0: b^(|S|-1) doubles at ou(T)
+  __host__ __device__ static constexpr int ou(int T) {
+    int o = 0;
+    for (int t = 0; t < T; ++t) o += ipow(B, popc(term_mask(M, t)) - 1);
+    return o;
+  }
+  static constexpr int SEGV = ov(NT), SEGU = ou(NT);
+  // units go round-robin to the groups, so the pattern of slabs a group
+  // visits repeats every NGRP / gcd(NGRP, UPS) slabs; a U full barrier period
+  // that is a multiple of it means a group waiting on slab s has also waited
+  // on slab s - UF, the barrier's previous phase
+  static constexpr int SLAB_PERIOD = NGRP / gcd(NGRP, UPS);
+  static constexpr int NS = (227 * 1024 - 8 * (SEGV + NU * SEGU) - 512) / (8 * UNIT);  // ring stages
+  static constexpr int MF = lcm(NS, NGRP);
+  static constexpr int UF = lcm(NU, SLAB_PERIOD);
+  static constexpr int NBAR = MF + NS + UF + NU + 2;
+  static constexpr size_t SMEM = 8 * (size_t)(SEGV + NU * SEGU + NS * UNIT) + 8 * NBAR;
+  // every bulk copy is a multiple of 16 bytes at a 16-byte aligned offset
+  static constexpr bool ok = B % 2 == 0 && B >= 4 && GT % 32 == 0 && NS >= 2 && SEGU % 2 == 0 &&
+                             UNIT % 2 == 0 && SMEM <= 227 * 1024;
+};
+
+// element offset, inside the factor over the modes of MASK (row-major), of
+// the register digits of tile row ROW (digits of the modes in RM, the last
+// fastest; index = 2 d + g)
+template <int MASK, int B, int RM, int ROW>
+struct RowOff {
+  static constexpr int calc() {
+    int off = 0, r = ROW;
+    for (int q = 5; q >= 2; --q) {
+      if (!(RM & (1 << q))) continue;
+      const int d = r % (B / 2);
+      r /= B / 2;
+      if (MASK & (1 << q)) off += 2 * d * stride_in(MASK, q, B);
+    }
+    return off;
+  }
+  static constexpr int value = calc();
+};
+
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bar_init(uint64_t *b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "RS_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra.uni RS_DONE;\n"
+      "bra.uni RS_WAIT;\n"
+      "RS_DONE:\n"
+      "}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+// global -> shared bulk copy completing on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(b))
+      : "memory");
+}
+// bulk prefetch into L2 (no shared memory)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// ---- factor producer ----
+template <class G, int T>
+__device__ __forceinline__ void load_v(double *sv, const RecFactArgs &a, const int32_t *toff, uint64_t *bar) {
+  constexpr int r = 6 - popc(term_mask(6, T));
+  constexpr int B = 2 * G::RG;
+  const double *src = (r <= 3 ? a.cum[r] : a.cmom[r]) + __ldg(toff + 2 * T + 1);
+  bulk_g2s(sv + G::ov(T), src, 8u * ipow(B, r), bar);
+}
+template <class G, int T>
+__device__ __forceinline__ void load_u(double *su, const RecFactArgs &a, const int32_t *toff, int i0, uint64_t *bar) {
+  constexpr int s = popc(term_mask(6, T));
+  constexpr int L = ipow(2 * G::RG, s - 1);
+  const double *src = a.cum[s] + __ldg(toff + 2 * T) + (int64_t)i0 * L;
+  bulk_g2s(su + G::ou(T), src, 8u * L, bar);
+}
+template <class G, int... Ts>
+__device__ __forceinline__ void load_v_all(double *sv, const RecFactArgs &a, const int32_t *toff, uint64_t *bar,
+                                           std::integer_sequence<int, Ts...>) {
+  (load_v<G, Ts>(sv, a, toff, bar), ...);
+}
+template <class G, int... Ts>
+__device__ __forceinline__ void load_u_all(double *su, const RecFactArgs &a, const int32_t *toff, int i0,
+                                           uint64_t *bar, std::integer_sequence<int, Ts...>) {
+  (load_u<G, Ts>(su, a, toff, i0, bar), ...);
+}
+
+// ---- consumer: one term on the thread's elements.  dig[q] = the thread's
+// index of mode q (modes 1 .. Q0-1) or its group bit (register modes) ----
+template <class G, int B, int RM, int T, int... Rs>
+__device__ __forceinline__ void term(double (&acc)[G::ROWS], const double *su, const double *sv, const int (&dig)[6],
+                                     std::integer_sequence<int, Rs...>) {
+  constexpr int S = term_mask(6, T);
+  constexpr int R = 63 & ~S;
+  int o1 = 0, o2 = 0;
+#pragma unroll
+  for (int q = 1; q < 6; ++q) {
+    if (S & (1 << q)) o1 += dig[q] * stride_in(S, q, B);
+    else o2 += dig[q] * stride_in(R, q, B);
+  }
+  const double *f1 = su + std::integral_constant<int, G::ou(T)>::value + o1;
+  const double *f2 = sv + std::integral_constant<int, G::ov(T)>::value + o2;
+  BCG_CHECK((o1 >= 0 && o1 + RowOff<S, B, RM, G::ROWS - 1>::value < ipow(B, popc(S) - 1)), "u factor", o1);
+  BCG_CHECK((o2 >= 0 && o2 + RowOff<R, B, RM, G::ROWS - 1>::value < ipow(B, 6 - popc(S))), "v factor", o2);
+  ((acc[Rs] = fma(-f1[RowOff<S, B, RM, Rs>::value], f2[RowOff<R, B, RM, Rs>::value], acc[Rs])), ...);
+}
+template <class G, int B, int RM, int... Ts>
+__device__ __forceinline__ void terms(double (&acc)[G::ROWS], const double *su, const double *sv, const int (&dig)[6],
+                                      std::integer_sequence<int, Ts...>) {
+  (term<G, B, RM, Ts>(acc, su, sv, dig, std::make_integer_sequence<int, G::ROWS>{}), ...);
+}
+// modes 2..5 of a sub-slab, row-major
+template <class G, int B, int RM, int... Rs>
+__device__ __forceinline__ void rows_load(double (&acc)[G::ROWS], const double *p, std::integer_sequence<int, Rs...>) {
+  ((acc[Rs] = p[RowOff<0x3c, B, RM, Rs>::value]), ...);
+}
+template <class G, int B, int RM, int... Rs>
+__device__ __forceinline__ void rows_store_global(const double (&acc)[G::ROWS], double *p,
+                                                  std::integer_sequence<int, Rs...>) {
+  (__stcs(p + RowOff<0x3c, B, RM, Rs>::value, acc[Rs]), ...);  // C_6 is written once: streaming stores
+}
+
+}  // namespace rs
+
+#ifndef BCG_RS_PREFETCH
+#define BCG_RS_PREFETCH 6
+#endif
+constexpr int kPrefetchUnits = BCG_RS_PREFETCH;  // M_6 units prefetched into L2 ahead of the ring
+
+template <int B, int RM, int NGRP, int NU>
+__global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU>::NTHREADS, 1) k_recursion_stream6(RecFactArgs a) {
+  using G = rs::Geo<B, RM, NGRP, NU>;
+  constexpr int NT = G::NT, NS = G::NS;
+  extern __shared__ __align__(128) unsigned char rs_smem[];
+  double *sv = reinterpret_cast<double *>(rs_smem);
+  double *su = sv + G::SEGV;          // [NU][SEGU]
+  double *sm = su + G::NU * G::SEGU;  // [NS][UNIT]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sm + NS * G::UNIT);
+  uint64_t *mfull = bars, *mempty = bars + G::MF;
+  uint64_t *ufull = mempty + NS, *uempty = ufull + G::UF;
+  uint64_t *vfull = uempty + G::NU, *vempty = vfull + 1;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < G::MF; ++i) rs::bar_init(&mfull[i], 1);
+    for (int i = 0; i < NS; ++i) rs::bar_init(&mempty[i], G::GW);
+    for (int i = 0; i < G::UF; ++i) rs::bar_init(&ufull[i], 1);
+    for (int i = 0; i < G::NU; ++i) rs::bar_init(&uempty[i], G::UPS * G::GW);
+    rs::bar_init(vfull, 1);
+    rs::bar_init(vempty, NGRP * G::GW);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // this CTA's positions [pbeg, pend) of the work list
+  const int64_t pbeg = a.nkeys * blockIdx.x / gridDim.x, pend = a.nkeys * (blockIdx.x + 1) / gridDim.x;
+  auto item = [&](int64_t pos) -> int64_t { return a.order ? (int64_t)__ldg(a.order + pos) : pos; };
+  // V (the 25 second factors) depends on the key's modes 1..5 only: reload
+  // it only when one of its block offsets changes
+  auto same_v = [&](int64_t it, int64_t prev) -> bool {
+    const int32_t *x = a.term_off + it * 2 * NT + 1, *y = a.term_off + prev * 2 * NT + 1;
+    bool eq = true;
+#pragma unroll
+    for (int T = 0; T < NT; ++T) eq = eq && __ldg(x + 2 * T) == __ldg(y + 2 * T);
+    return eq;
+  };
+  if (warp == 0) {
+    // ---- M_6 producer: units in (position, i0, unit) order into the ring ----
+    if (lane == 0) {
+      int64_t u = 0;
+      static_assert(kPrefetchUnits <= G::UPB, "prefetch at most one block ahead");
+      for (int64_t pos = pbeg; pos < pend; ++pos) {
+        const double *blk = a.mk + __ldg(a.blk_off + item(pos));
+        const double *nblk = pos + 1 < pend ? a.mk + __ldg(a.blk_off + item(pos + 1)) : nullptr;
+        if (pos == pbeg)
+          for (int j = 0; j < kPrefetchUnits; ++j) rs::bulk_prefetch_l2(blk + (int64_t)j * G::UNIT, 8u * G::UNIT);
+        for (int j = 0; j < G::UPB; ++j, ++u) {
+          if (kPrefetchUnits > 0) {  // L2 prefetch kPrefetchUnits ahead of the ring
+            const int jp = j + kPrefetchUnits;
+            if (jp < G::UPB) rs::bulk_prefetch_l2(blk + (int64_t)jp * G::UNIT, 8u * G::UNIT);
+            else if (nblk) rs::bulk_prefetch_l2(nblk + (int64_t)(jp - G::UPB) * G::UNIT, 8u * G::UNIT);
+          }
+          const int st = (int)(u % NS);
+          if (u >= NS) rs::bar_wait(&mempty[st], (uint32_t)((u / NS - 1) & 1));
+          uint64_t *fb = &mfull[u % G::MF];
+          rs::bar_expect(fb, 8u * G::UNIT);
+          rs::bulk_g2s(sm + (int64_t)st * G::UNIT, blk + (int64_t)j * G::UNIT, 8u * G::UNIT, fb);
+        }
+      }
+    }
+    return;
+  }
+  if (warp == 1) {
+    // ---- factor producer: V per run of equal tails, U per slab ----
+    if (lane == 0) {
+      int64_t e = -1, s = 0, prev = -1;
+      for (int64_t pos = pbeg; pos < pend; ++pos) {
+        const int64_t it = item(pos);
+        const int32_t *toff = a.term_off + it * 2 * NT;
+        if (prev < 0 || !same_v(it, prev)) {
+          ++e;
+          if (e > 0) rs::bar_wait(vempty, (uint32_t)((e - 1) & 1));
+          rs::bar_expect(vfull, 8u * G::SEGV);
+          rs::load_v_all<G>(sv, a, toff, vfull, std::make_integer_sequence<int, NT>{});
+        }
+        prev = it;
+        for (int i0 = 0; i0 < B; ++i0, ++s) {
+          const int buf = (int)(s % G::NU);
+          if (s >= G::NU) rs::bar_wait(&uempty[buf], (uint32_t)((s / G::NU - 1) & 1));
+          uint64_t *fb = &ufull[s % G::UF];
+          rs::bar_expect(fb, 8u * G::SEGU);
+          rs::load_u_all<G>(su + buf * G::SEGU, a, toff, i0, fb, std::make_integer_sequence<int, NT>{});
+        }
+      }
+    }
+    return;
+  }
+  // ---- consumers: group grp takes the units u == grp (mod NGRP) ----
+  const int ct = threadIdx.x - 64;
+  const int grp = ct / G::GT, t = ct % G::GT;
+  // lane order (fastest first): the register modes' group bits (last mode
+  // fastest), the thread-level modes, then the sub-slab h (measured faster
+  // than h-before-thread-modes at cfg5)
+  const int h = t / G::TPS, r = t % G::TPS;
+  int dig[6];
+  dig[0] = 0;
+  {
+    int gb = r % (1 << G::NRM), tm = r >> G::NRM;
+#pragma unroll
+    for (int q = 5; q >= 2; --q) {
+      if (RM & (1 << q)) {
+        dig[q] = gb & 1;  // group bit of register mode q (index = 2 d + g)
+        gb >>= 1;
+      } else {
+        dig[q] = tm % B;  // thread-level mode
+        tm /= B;
+      }
+    }
+  }
+  int ebase = 0;  // thread's first element inside its sub-slab (row-major over modes 2..5)
+#pragma unroll
+  for (int q = 2; q < 6; ++q) ebase += dig[q] * rs::ipow(B, 5 - q);
+  int64_t e = -1, s = 0, prev = -1;
+  for (int64_t pos = pbeg; pos < pend; ++pos) {
+    const int64_t it = item(pos);
+    if (prev < 0 || !same_v(it, prev)) {
+      if (e >= 0 && lane == 0) rs::bar_arrive(vempty);  // done with the previous V
+      ++e;
+    }
+    prev = it;
+    rs::bar_wait(vfull, (uint32_t)(e & 1));
+    double *blk = a.mk + __ldg(a.blk_off + it);
+    for (int i0 = 0; i0 < B; ++i0, ++s) {
+      const int ub = (int)(s % G::NU);
+      for (int p = 0; p < G::UPS; ++p) {
+        const int j = i0 * G::UPS + p;
+        const int64_t u = (pos - pbeg) * G::UPB + j;
+        if ((int)(u % NGRP) != grp) continue;
+        const int st = (int)(u % NS);
+        dig[1] = G::U1 * p + h;
+        rs::bar_wait(&mfull[u % G::MF], (uint32_t)((u / G::MF) & 1));
+        double acc[G::ROWS];
+        BCG_CHECK((h * G::SUB + ebase + rs::RowOff<0x3c, B, RM, G::ROWS - 1>::value < G::UNIT), "element", ebase);
+        rs::rows_load<G, B, RM>(acc, sm + (int64_t)st * G::UNIT + h * G::SUB + ebase,
+                                 std::make_integer_sequence<int, G::ROWS>{});
+        __syncwarp();
+        if (lane == 0) rs::bar_arrive(&mempty[st]);  // the elements are in registers: refill the stage
+        rs::bar_wait(&ufull[s % G::UF], (uint32_t)((s / G::UF) & 1));
+        rs::terms<G, B, RM>(acc, su + ub * G::SEGU, sv, dig, std::make_integer_sequence<int, NT>{});
+        __syncwarp();
+        if (lane == 0) rs::bar_arrive(&uempty[ub]);
+        rs::rows_store_global<G, B, RM>(acc, blk + (int64_t)j * G::UNIT + h * G::SUB + ebase,
+                                         std::make_integer_sequence<int, G::ROWS>{});
+      }
+    }
+  }
+  if (e >= 0 && lane == 0) rs::bar_arrive(vempty);
+}
+
+// tile / group / buffer choice (A/B knob BCG_RS_TILE):
+//   0: register modes 3,4,5 (27 elements), mode 2 across threads, 9 consumer warps, 3 U buffers (default)
+//   1: register modes 2,3,4, mode 5 across threads
+//   2: as 0 with 2 U buffers (one more ring stage)
+//   4: register modes 2..5 (81 elements), 6 consumer warps
+template <int B, int RM, int NGRP, int NU>
+static cudaError_t go_stream6(const RecFactArgs &a, int nsm, cudaStream_t stream) {
+  using G = rs::Geo<B, RM, NGRP, NU>;
+  static_assert(G::ok, "stream6 geometry");
+  auto kern = k_recursion_stream6<B, RM, NGRP, NU>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+  if (e != cudaSuccess) return e;
+  const int64_t grid = a.nkeys < nsm ? a.nkeys : nsm;
+  kern<<<(unsigned)grid, G::NTHREADS, G::SMEM, stream>>>(a);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+bool recursion_stream6_supported(int b) { return b == 6; }
+
+cudaError_t launch_recursion_stream6(const RecFactArgs &a, int b, cudaStream_t stream) {
+  if (a.nkeys <= 0) return cudaSuccess;
+  if (b != 6) return cudaErrorInvalidValue;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  static const int tile = getenv("BCG_RS_TILE") ? atoi(getenv("BCG_RS_TILE")) : 0;
+  if (tile == 1) return go_stream6<6, 0x1c, 3, 3>(a, nsm, stream);
+  if (tile == 2) return go_stream6<6, 0x38, 3, 2>(a, nsm, stream);
+  if (tile == 4) return go_stream6<6, 0x3c, 6, 3>(a, nsm, stream);
+  if (tile == 5) return go_stream6<6, 0x38, 4, 3>(a, nsm, stream);
+  if (tile == 6) return go_stream6<6, 0x38, 5, 3>(a, nsm, stream);
+  return go_stream6<6, 0x38, 3, 3>(a, nsm, stream);
+}
+
+}  // namespace bcg

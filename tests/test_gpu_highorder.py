@@ -112,6 +112,36 @@ np.savez({path!r}, **out)
 """
 
 
+def _run_child(cases, env_set, path):
+    """cumulants_upto C_4..C_m of every case in a fresh process (the kernel
+    selection knobs are read once per process) with env_set applied."""
+    code = _PARTITION_CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"), cases=cases, path=path)
+    env = dict(os.environ)
+    for k in ("BCG_RECURSION_PARTITION", "BCG_RF_VARIANT"):
+        env.pop(k, None)
+    env.update(env_set)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return np.load(path)
+
+
+def test_streamed_recursion_is_bitwise_the_register_kernel(tmp_path):
+    """K3 v7 (csrc/recursion_stream.cu: bulk-copy streamed, default for
+    m = b = 6) applies the same 25 terms in the same order with the same fma
+    as v2 (csrc/recursion_fact.cu), so C_6 must be bitwise equal.  Shapes: one
+    block, several blocks per CTA (cfg5s: 462 blocks, 36 columns of the cfg5
+    Student-t recipe), 34 blocks per CTA (n = 60), and partial edges (the
+    partial blocks run the partition kernel in both)."""
+    cases = {"cfg5s": ("tag", "cfg5s")}
+    for i, (n, m, b, t) in enumerate([(6, 6, 6, 500), (16, 6, 6, 300), (60, 6, 6, 200), (30, 6, 6, 257)]):
+        cases[f"b6_{i}"] = ("shape", (n, m, b, t, 2000 + i))
+    v7 = _run_child(cases, {}, str(tmp_path / "v7.npz"))
+    v2 = _run_child(cases, {"BCG_RF_VARIANT": "2"}, str(tmp_path / "v2.npz"))
+    assert sorted(v7.files) == sorted(v2.files)
+    for key in v7.files:
+        assert np.array_equal(v7[key], v2[key]), key
+
+
 def test_factored_recursion_matches_the_partition_sum(tmp_path):
     """K3 factored (production) vs the reference's partition sum (the same
     moments; BCG_RECURSION_PARTITION=1 is read once per process, hence the
@@ -121,18 +151,8 @@ def test_factored_recursion_matches_the_partition_sum(tmp_path):
     for i, (n, m, b, t) in enumerate([(9, 4, 3, 500), (8, 5, 2, 400), (7, 6, 1, 300), (6, 6, 2, 500),
                                       (12, 6, 3, 600), (7, 6, 3, 500), (10, 5, 4, 700)]):
         cases[f"s{i}"] = ("shape", (n, m, b, t, 1000 + i))
-    files = {}
-    for mode in ("factored", "partition"):
-        path = str(tmp_path / f"{mode}.npz")
-        code = _PARTITION_CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"), cases=cases, path=path)
-        env = dict(os.environ)
-        env.pop("BCG_RECURSION_PARTITION", None)
-        if mode == "partition":
-            env["BCG_RECURSION_PARTITION"] = "1"
-        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
-        assert r.returncode == 0, r.stderr[-3000:]
-        files[mode] = np.load(path)
-    fa, pa = files["factored"], files["partition"]
+    fa = _run_child(cases, {}, str(tmp_path / "factored.npz"))
+    pa = _run_child(cases, {"BCG_RECURSION_PARTITION": "1"}, str(tmp_path / "partition.npz"))
     assert sorted(fa.files) == sorted(pa.files)
     for key in fa.files:
         a, p = fa[key], pa[key]
