@@ -123,14 +123,33 @@ static int64_t build_tiles(const Plan &p, const Gemm &g, int tm, int tn, std::ve
     const int64_t r1 = std::min<int64_t>(r0 + tm, g.R);
     for (int64_t c0 = g.row_cstart[r0]; c0 < g.C; c0 += tn) {
       const int64_t c1 = std::min<int64_t>(c0 + tn, g.C);
+      int32_t cache_lo = 0, cache_hi = 0;
       int64_t kmin = INT64_MAX, kmax = -1;
+      // a tile of this band holds row r0 (its columns start at or after
+      // r0's suffix start, the band's smallest); the key range is only
+      // needed for the tile list itself
+      if (!kmin_out && !kmax_out) {
+        ++ntiles;
+        continue;
+      }
       for (int64_t rr = r0; rr < r1; ++rr) {
         int64_t cs = std::max<int64_t>(c0, g.row_cstart[rr]);
         if (cs >= c1) continue;
-        const int64_t klo = g.row_keybase[rr] + g.col_rank[cs];
-        const int64_t khi = g.row_keybase[rr] + g.col_rank[c1 - 1];
-        kmin = std::min<int64_t>(kmin, klo);
-        kmax = std::max<int64_t>(kmax, khi);
+        // column ranks are not monotone in a symmetric plan's column order
+        int32_t rlo = INT32_MAX, rhi = -1;
+        if (rr == r0 || g.row_cstart[rr] != g.row_cstart[rr - 1]) {
+          for (int64_t c = cs; c < c1; ++c) {
+            rlo = std::min(rlo, g.col_rank[c]);
+            rhi = std::max(rhi, g.col_rank[c]);
+          }
+          cache_lo = rlo;
+          cache_hi = rhi;
+        } else {
+          rlo = cache_lo;
+          rhi = cache_hi;
+        }
+        kmin = std::min<int64_t>(kmin, g.row_keybase[rr] + rlo);
+        kmax = std::max<int64_t>(kmax, g.row_keybase[rr] + rhi);
       }
       if (kmax < 0) continue;  // below the staircase
       ++ntiles;
@@ -200,11 +219,23 @@ static void tuple_offsets(const int64_t *T, int k, const std::vector<int64_t> &s
 }
 
 // GEMM tables over the block alphabet 1..N (sym_edge / sym_col0): rows =
-// sorted h-tuples grouped by last entry v <= vmax, cols = sorted (m-h)-tuples,
-// row group v valid from the first column whose tuple starts with >=
-// max(v, tcol).  Each tuple contributes one row / column per produced in-block
-// offset (tuple_offsets); row_olin / col_olin keep the full row-major offset,
-// so the epilogue address of an element is the same for every plan.
+// sorted h-tuples L with one row per produced in-block offset, cols = sorted
+// (m-h)-tuples R likewise; (L, R) is a stored key when R[0] >= v = L[h-1].
+// Each tuple contributes one row / column per produced in-block offset
+// (tuple_offsets); row_olin / col_olin keep the full row-major offset, so the
+// epilogue address of an element is the same for every plan.
+//
+// Full plan: rows grouped by v, columns lexicographic -- row group v is valid
+// from the first column whose tuple starts with >= max(v, tcol).
+//
+// Symmetric plan: a run of equal block indices may straddle the L | R split
+// (L ends with v, R starts with v); the element is canonical (digits
+// non-decreasing within every run of the full key) iff additionally the last
+// digit of L <= the first digit of R.  Columns are ordered by (R[0], first
+// digit) and rows by their valid-column start, so row (v, d) is valid on the
+// suffix {R[0] > v} + {R[0] == v, first digit >= d}: the GEMM produces exactly
+// the canonical elements (C(n+m-1, m) of them when b | n) and k_sym_fill
+// copies every other stored element from its canonical permutation.
 static std::string build_gemm(Plan &p, Gemm &g, const std::vector<int64_t> &sym_edge,
                               const std::vector<int64_t> &sym_col0, int64_t N, int h, int64_t vmax,
                               int64_t tcol) {
@@ -216,82 +247,106 @@ static std::string build_gemm(Plan &p, Gemm &g, const std::vector<int64_t> &sym_
   enum_sorted(N, h, lt);
   enum_sorted(N, r, rt);
   const int64_t NL = (int64_t)lt.size() / h, NR = (int64_t)rt.size() / r;
-  std::vector<int64_t> lorder(NL);
-  std::iota(lorder.begin(), lorder.end(), 0);
-  // (last entry, lexicographic): lex order is already the secondary order
-  std::stable_sort(lorder.begin(), lorder.end(),
-                   [&](int64_t a, int64_t c) { return lt[a * h + h - 1] < lt[c * h + h - 1]; });
-  // right columns, lexicographic
-  std::vector<int64_t> rstart(NR + 1, 0);
+  // ---- columns: (tuple, offset) pairs ----
+  struct Col {
+    int64_t tuple, off, first_digit;
+  };
+  std::vector<Col> cols;
   for (int64_t i = 0; i < NR; ++i) {
-    tuple_offsets(&rt[i * r], r, sym_edge, p.sym, offs);
-    rstart[i + 1] = rstart[i] + (int64_t)offs.size();
+    const int64_t *Rt = &rt[i * r];
+    int64_t tail = 1;  // size of the modes after the first
+    for (int q = 1; q < r; ++q) tail *= sym_edge[Rt[q]];
+    tuple_offsets(Rt, r, sym_edge, p.sym, offs);
+    for (int64_t o : offs) cols.push_back(Col{i, o, o / tail});
   }
-  g.C = rstart[NR];
+  if (p.sym)  // (R[0], first digit), then lexicographic (tuple, offset)
+    std::stable_sort(cols.begin(), cols.end(), [&](const Col &a, const Col &c) {
+      const int64_t fa = rt[a.tuple * r], fc = rt[c.tuple * r];
+      return fa != fc ? fa < fc : a.first_digit < c.first_digit;
+    });
+  g.C = (int64_t)cols.size();
   g.colcols.resize(g.C * r);
   g.col_rank.resize(g.C);
   g.col_olin.resize(g.C);
   g.col_size.resize(g.C);
-  for (int64_t i = 0; i < NR; ++i) {
-    const int64_t *Rt = &rt[i * r];
+  for (int64_t c = 0; c < g.C; ++c) {
+    const int64_t *Rt = &rt[cols[c].tuple * r];
     int64_t e[16], sz = 1;
     for (int q = 0; q < r; ++q) sz *= (e[q] = sym_edge[Rt[q]]);
-    tuple_offsets(Rt, r, sym_edge, p.sym, offs);
-    for (size_t j = 0; j < offs.size(); ++j) {
-      const int64_t c = rstart[i] + (int64_t)j, o = offs[j];
-      int64_t rem = o;
-      for (int q = r - 1; q >= 0; --q) {
-        g.colcols[c * r + q] = (int16_t)(sym_col0[Rt[q]] + rem % e[q]);
-        rem /= e[q];
-      }
-      g.col_rank[c] = (int32_t)i;
-      g.col_olin[c] = (int32_t)o;
-      g.col_size[c] = (int32_t)sz;
+    int64_t rem = cols[c].off;
+    for (int q = r - 1; q >= 0; --q) {
+      g.colcols[c * r + q] = (int16_t)(sym_col0[Rt[q]] + rem % e[q]);
+      rem /= e[q];
     }
+    g.col_rank[c] = (int32_t)cols[c].tuple;
+    g.col_olin[c] = (int32_t)cols[c].off;
+    g.col_size[c] = (int32_t)sz;
   }
-  // first column of the suffix {R : R[0] >= v}; (v, ..., v) is its first tuple
-  std::vector<int64_t> cstart_v(N + 2, g.C), rank_first_v(N + 2, NR);
+  // first column of the suffix valid for a row ending in block v with last
+  // digit d (d = -1: no digit condition, i.e. R[0] >= v)
+  auto cstart = [&](int64_t v, int64_t d) -> int64_t {
+    int64_t lo = 0, hi = g.C;  // first c with (R[0], first digit) >= (v, max(d, 0))
+    const int64_t dd = d < 0 ? 0 : d;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      const int64_t f = rt[cols[mid].tuple * r];
+      const bool before = p.sym ? (f < v || (f == v && cols[mid].first_digit < dd)) : f < v;
+      if (before) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  };
+  std::vector<int64_t> rank_first_v(N + 2, NR);
   for (int64_t v = 1; v <= N; ++v) {
     std::vector<int64_t> vv(r, v);
-    const int64_t rk = multiset_rank(vv.data(), r, N);
-    rank_first_v[v] = rk;
-    cstart_v[v] = rstart[rk];
+    rank_first_v[v] = multiset_rank(vv.data(), r, N);
   }
-  // rows
-  g.R = 0;
+  // full plan: columns lexicographic, so the suffix search above (on R[0]
+  // only) is exact; symmetric plan: rows sorted by their suffix start
+  struct Row {
+    int64_t tuple, off, cs;
+  };
+  std::vector<Row> rows;
   for (int64_t i = 0; i < NL; ++i) {
-    const int64_t *L = &lt[lorder[i] * h];
+    const int64_t *L = &lt[i * h];
     const int64_t v = L[h - 1];
-    if (v > vmax || cstart_v[std::max(v, tcol)] >= g.C) continue;
+    if (v > vmax) continue;
+    const int64_t vc = std::max(v, tcol);
     tuple_offsets(L, h, sym_edge, p.sym, offs);
-    g.R += (int64_t)offs.size();
+    for (int64_t o : offs) {
+      // the digit condition applies only when R may start with v itself
+      const int64_t cs = (p.sym && vc == v) ? cstart(v, o % sym_edge[v]) : cstart(vc, -1);
+      if (cs >= g.C) continue;
+      rows.push_back(Row{i, o, cs});
+    }
   }
+  // (suffix start, last entry, lexicographic): non-decreasing starts, so a
+  // tile's first row has the earliest valid column of its row band
+  std::stable_sort(rows.begin(), rows.end(), [&](const Row &a, const Row &c) {
+    if (a.cs != c.cs) return a.cs < c.cs;
+    return lt[a.tuple * h + h - 1] < lt[c.tuple * h + h - 1];
+  });
+  g.R = (int64_t)rows.size();
   g.rowcols.resize(g.R * h);
   g.row_keybase.resize(g.R);
   g.row_olin.resize(g.R);
   g.row_cstart.resize(g.R);
-  int64_t row = 0;
-  for (int64_t i = 0; i < NL; ++i) {
-    const int64_t *L = &lt[lorder[i] * h];
+  for (int64_t row = 0; row < g.R; ++row) {
+    const int64_t *L = &lt[rows[row].tuple * h];
     const int64_t v = L[h - 1];
-    const int64_t vc = std::max(v, tcol);
-    if (v > vmax || cstart_v[vc] >= g.C) continue;
     int64_t full[16], e[16];
     for (int q = 0; q < h; ++q) full[q] = L[q];
     for (int q = h; q < m; ++q) full[q] = v;
     const int64_t kbase = multiset_rank(full, m, N) - rank_first_v[v];
     for (int q = 0; q < h; ++q) e[q] = sym_edge[L[q]];
-    tuple_offsets(L, h, sym_edge, p.sym, offs);
-    for (size_t j = 0; j < offs.size(); ++j, ++row) {
-      int64_t rem = offs[j];
-      for (int q = h - 1; q >= 0; --q) {
-        g.rowcols[row * h + q] = (int16_t)(sym_col0[L[q]] + rem % e[q]);
-        rem /= e[q];
-      }
-      g.row_keybase[row] = (int32_t)kbase;
-      g.row_olin[row] = (int32_t)offs[j];
-      g.row_cstart[row] = (int32_t)cstart_v[vc];
+    int64_t rem = rows[row].off;
+    for (int q = h - 1; q >= 0; --q) {
+      g.rowcols[row * h + q] = (int16_t)(sym_col0[L[q]] + rem % e[q]);
+      rem /= e[q];
     }
+    g.row_keybase[row] = (int32_t)kbase;
+    g.row_olin[row] = (int32_t)rows[row].off;
+    g.row_cstart[row] = (int32_t)rows[row].cs;
   }
   if (g.R > INT32_MAX || g.C > INT32_MAX) return "GEMM dimension overflow";
   return "";

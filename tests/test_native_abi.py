@@ -79,10 +79,11 @@ def test_gemm_mapping_selfcheck(n, m, b, full):
     assert produced == S if full else produced <= S
 
 
-def _sorted_within_runs_count(n, m, b, h):
-    """Elements a symmetric plan's (h | m-h) GEMM produces: per key, the
-    in-block offsets whose digits are non-decreasing within each run of equal
-    block indices of the left h-tuple and of the right (m-h)-tuple."""
+def _canonical_count(n, m, b):
+    """Elements a symmetric plan's GEMM(s) produce: per key, the in-block
+    offsets whose digits are non-decreasing within each run of equal block
+    indices of the FULL key (runs that straddle the row | column split
+    included) -- one per multiset of m variables, C(n+m-1, m) when b | n."""
     from itertools import combinations_with_replacement, groupby
     from math import comb
 
@@ -96,18 +97,25 @@ def _sorted_within_runs_count(n, m, b, h):
             r *= comb(edge(j) + L - 1, L)
         return r
 
-    return sum(part(k[:h]) * part(k[h:]) for k in combinations_with_replacement(range(1, nb + 1), m))
+    return sum(part(k) for k in combinations_with_replacement(range(1, nb + 1), m))
 
 
-@pytest.mark.parametrize("n,m,b", [(36, 6, 3), (64, 4, 8), (24, 4, 4), (7, 4, 3)])
+@pytest.mark.parametrize("n,m,b", [(36, 6, 3), (64, 4, 8), (24, 4, 4), (7, 4, 3), (48, 5, 4), (13, 6, 4),
+                                   (10, 5, 3), (20, 6, 6)])
 def test_symmetric_plan_produced_count(n, m, b):
-    # even orders run one balanced (m/2 | m/2) GEMM: the produced count is the
-    # closed form (cfg4: 58.5% of S_6, cfg2: 70.3% of S_4)
+    # the GEMMs produce exactly the canonical elements (the multisets of m
+    # variables); k_sym_fill copies the rest (cfg4: 49.8% of S_6, cfg2: 56.7%
+    # of S_4)
+    from math import comb
+
     plan = _native.Plan(n, m, b, host_only=True)
     S, produced = plan.output()
-    assert produced == _sorted_within_runs_count(n, m, b, m // 2)
+    assert produced == _canonical_count(n, m, b)
+    if n % b == 0:
+        assert produced == comb(n + m - 1, m)
     if (n, m, b) == (36, 6, 3):
-        assert abs(produced / S - 0.585) < 1e-3
+        assert abs(produced / S - 0.498) < 1e-3
+    _native.check(_native.lib().bcg_plan_selfcheck(plan.handle))
 
 
 def test_hybrid_odd_order_plan():
