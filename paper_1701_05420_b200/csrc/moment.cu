@@ -92,9 +92,17 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 }
 
 // CTA tile TM x TN, 4 warps in a WGM x WGN grid (warp tile WM x WN of 8x8
-// DMMA sub-tiles).  Factor storage [row][k], 16 doubles per row, sample index
-// XOR-swizzled by ((row & 3) << 2): an m8n8k4 fragment load (rows gid, samples
-// k0 + tig) and a paired STS.128 (samples 2j, 2j+1) are both conflict-free.
+// DMMA sub-tiles).  Factor storage [row][k], 16 doubles per row, the 16-byte
+// sample-pair chunks of row r XOR-swizzled by s(r) = 2 (r & 3) + ((r >> 2) & 1)
+// (kr_swizzle returns 2 s(r), the swizzle of the double index):
+//   * a paired STS.128 of 8 consecutive rows (a quarter warp, one sample pair)
+//     hits 8 distinct chunks;
+//   * an m8n8k4 fragment load (half warp: rows gid = 0..3 or 4..7, samples
+//     k0 + tig) hits 16 distinct doubles, since s(r) >> 1 = r & 3.
+// (The previous (r & 3) << 2 left the stores 2-way conflicted: 17% of the
+// kernel's shared-memory wavefronts at cfg4, profiles/r02_moment_cfg4_ncu.txt.)
+__device__ __forceinline__ int kr_swizzle(int row) { return ((row & 3) << 2) | ((row >> 1) & 2); }
+
 template <int KC, int TM, int TN>
 struct V1Shape {
   static constexpr int WGN = TN >= 4 * TM ? 4 : (TN >= TM ? 2 : 1);
@@ -214,6 +222,7 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
   const int warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int wm = warp % SH::WGM, wn = warp / SH::WGM;
+  // acc[i][j][e] = C[8i + gid][8j + 2 tig + e] (m8n8k4 accumulator fragments)
   double acc[MT][NT][2];
 #pragma unroll
   for (int i = 0; i < MT; ++i)
@@ -235,7 +244,7 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
         sa[q] = colA[q] & 7;
       }
       double *wa = kra + (c & 1) * TM * LDK + ia * LDK;
-      const int swa = (ia & 3) << 2;
+      const int swa = kr_swizzle(ia);
 #pragma unroll
       for (int i = 0; i < SH::NPAIR / SH::PA; ++i) {
         const int j = pa0 + SH::PA * i;
@@ -258,7 +267,7 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
         sb[q] = colB[q] & 7;
       }
       double *wb = krb + (c & 1) * TN * LDK + ib * LDK;
-      const int swb = (ib & 3) << 2;
+      const int swb = kr_swizzle(ib);
 #pragma unroll
       for (int i = 0; i < SH::NPAIR / SH::PB; ++i) {
         const int j = pb0 + SH::PB * i;
@@ -281,15 +290,16 @@ __global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant_
   }
   for (int c = 0; c < nch; ++c) {
     // ---- DMMA over chunk c ----
-    // fragment rows = gid (mod 4 after the 8-row and warp offsets): swizzle (gid & 3) << 2
-    const int swf = (gid & 3) << 2;
-    const double *ka = kra + (c & 1) * TM * LDK + (wm * SH::WM + gid) * LDK + tig;
-    const double *kb = krb + (c & 1) * TN * LDK + (wn * SH::WN + gid) * LDK + tig;
+    // fragment rows = gid (mod 8 after the 8-row and warp offsets), sample
+    // k + tig: double index (k + tig) ^ kr_swizzle(gid)
+    const int swf = kr_swizzle(gid);
+    const double *ka = kra + (c & 1) * TM * LDK + (wm * SH::WM + gid) * LDK;
+    const double *kb = krb + (c & 1) * TN * LDK + (wn * SH::WN + gid) * LDK;
     auto ksteps = [&](int k0, int k1) {
 #pragma unroll
       for (int k = k0; k < k1; k += 4) {
         double fa[MT], fb[NT];
-        const int ks = k ^ swf;
+        const int ks = (k + tig) ^ swf;
 #pragma unroll
         for (int i = 0; i < MT; ++i) fa[i] = ka[8 * i * LDK + ks];
 #pragma unroll
