@@ -261,6 +261,23 @@ int bcg_axpby(int64_t len, double a, const double *x, double c,
 /* out[i] = x[i] / d  (the reference's `out /= t`, bc/_engines.py:99). */
 int bcg_div(int64_t len, const double *x, double d, double *out, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Dense-entry verification (SURVEY §8 f row 4; the reference's dense oracle
+ * bc/oracle.py:89-117 is limited to n^m <= 1e8): for E element tuples
+ * idx[E][m] (0-based column indices, any order, repeats allowed) of the
+ * row-major data x (t rows, row stride ldx >= n, device) with column means
+ * mean[n], out[e][S] = sum_l prod_{q in S} (x[l, idx[e][q]] - mean[idx[e][q]])
+ * for every subset S of {0..m-1} (bit q of S = index q; out[e][0] = t),
+ * 1 <= m <= 8.  Independent of the block layout and of the moment / recursion
+ * kernels; deterministic.  Workspace: bcg_dense_subsets_ws_bytes(E, m, t)
+ * bytes.
+ * ------------------------------------------------------------------------- */
+size_t bcg_dense_subsets_ws_bytes(int64_t E, int32_t m, int64_t t);
+int bcg_dense_subsets(const double *x, int64_t t, int64_t n, int64_t ldx,
+                      const double *mean, int32_t m, const int32_t *idx,
+                      int64_t E, double *out, void *ws, size_t ws_bytes,
+                      void *stream);
+
 #ifdef __cplusplus
 }
 #endif

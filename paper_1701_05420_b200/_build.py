@@ -11,7 +11,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbcgpu.so")
-SOURCES = ["plan.cu", "moment.cu", "elementwise.cu", "recursion.cu", "recursion_fact.cu", "recursion_stream.cu", "capi.cu"]
+SOURCES = ["plan.cu", "moment.cu", "elementwise.cu", "recursion.cu", "recursion_fact.cu", "recursion_stream.cu", "dense.cu", "capi.cu"]
 # moment.cu is compiled once per part: part 0 = host code + dispatch, parts
 # 1..6 = the kernel instantiations of one CTA tile shape each (parallel nvcc)
 # (recursion_fact.cu likewise: part 0 = dispatch, 1..6 = (m, b) instantiations)

@@ -54,6 +54,8 @@ SIGNATURES = [
     ("bcg_moment_raw", ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     ("bcg_moment_raw_t", ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     ("bcg_padded_t", _i64, [_i64]),
+    ("bcg_dense_subsets_ws_bytes", _sz, [_i64, _i32, _i64]),
+    ("bcg_dense_subsets", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _i32, _vp, _i64, _vp, _vp, _sz, _vp]),
     ("bcg_transpose_pad", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp]),
     ("bcg_rowstats", ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     ("bcg_rowstats_ws_bytes", _sz, [_i64, _i64]),

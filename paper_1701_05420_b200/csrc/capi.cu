@@ -683,4 +683,23 @@ int bcg_div(int64_t len, const double *x, double d, double *out, void *stream) {
   return BCG_OK;
 }
 
+size_t bcg_dense_subsets_ws_bytes(int64_t E, int32_t m, int64_t t) {
+  if (E <= 0 || m < 1 || m > 8) return 0;
+  return (size_t)E * (size_t)bcg::dense_subsets_parts(E, t) * ((size_t)1 << m) * sizeof(double);
+}
+
+int bcg_dense_subsets(const double *x, int64_t t, int64_t n, int64_t ldx, const double *mean, int32_t m,
+                      const int32_t *idx, int64_t E, double *out, void *ws, size_t ws_bytes, void *stream) {
+  if (m < 1 || m > 8) return fail(BCG_EINVAL, "dense entries support 1 <= m <= 8");
+  if (t <= 0 || n <= 0 || ldx < n) return fail(BCG_EINVAL, "bad data shape");
+  if (E <= 0) return BCG_OK;
+  if (!x || !mean || !idx || !out) return fail(BCG_EINVAL, "NULL pointer");
+  const size_t need = bcg_dense_subsets_ws_bytes(E, m, t);
+  if (!ws || ws_bytes < need) return fail(BCG_EINVAL, "workspace too small: need " + std::to_string(need) + " bytes");
+  CUDA_TRY(bcg::launch_dense_subsets(x, t, n, ldx, mean, m, idx, E, static_cast<double *>(ws),
+                                     bcg::dense_subsets_parts(E, t), out, static_cast<cudaStream_t>(stream)),
+           "dense subsets");
+  return BCG_OK;
+}
+
 }  // extern "C"

@@ -113,6 +113,12 @@ cudaError_t launch_recursion_fact(const RecFactArgs &a, int m, int b, cudaStream
 bool recursion_stream6_supported(int b);
 cudaError_t launch_recursion_stream6(const RecFactArgs &a, int b, cudaStream_t stream);
 
+// dense-entry verification (dense.cu)
+int dense_subsets_parts(int64_t E, int64_t t);
+cudaError_t launch_dense_subsets(const double *x, int64_t t, int64_t n, int64_t ldx, const double *mean, int m,
+                                 const int32_t *idx, int64_t E, double *part, int P, double *out,
+                                 cudaStream_t stream);
+
 extern int64_t g_launches;
 
 }  // namespace bcg
