@@ -36,8 +36,10 @@ CENTERING_RTOL = 1e-10  # bc/cumulants.py:26
 
 def _check_centered_stats(sums, sumsq, t: int) -> None:
     """|mean| <= 1e-10 * rms per column (bc/cumulants.py:31-39)."""
-    s = sums.cpu().numpy()
-    q = sumsq.cpu().numpy()
+    _check_centered_stats_host(sums.cpu().numpy(), sumsq.cpu().numpy(), t)
+
+
+def _check_centered_stats_host(s, q, t: int) -> None:
     means = np.abs(s / t)
     rms = np.sqrt(q / t)
     bad = means > CENTERING_RTOL * np.maximum(rms, 1e-300)
@@ -197,14 +199,18 @@ def cumulants_device(X, m_max: int, b: int, c1_host: bool = True, timer: dict | 
     """
     t, n = X.shape
     st = _colstats(X, mean=True, bad=True)
-    _raise_if_nonfinite(X, st["bad"])
     tensors: list[BlockSymTensor] = []
     if m_max >= 2:
         xt = _center_transposed(X, st["mean"])
         sums, sq = _rowstats(xt, t)
-        _check_centered_stats(sums, sq, t)
+        # the finite scan, the centering check and C_1 reach the host through
+        # one non-blocking copy; the moment GEMMs are enqueued before the host
+        # waits for it (validation errors are raised as before, and nothing is
+        # returned for invalid data)
+        flags = _stage_to_host(st["bad"], st["mean"], sums, sq)
         if timer is None and m_max >= 3 and not _SERIAL_ORDERS:
-            return (st["mean"].cpu().numpy() if c1_host else st["mean"]), _orders_concurrent(xt, t, m_max, b)
+            tensors = _orders_concurrent(xt, t, m_max, b)
+            return _validated_c1(X, flags, t, c1_host, st["mean"]), tensors
         central: dict = {}  # central moment M_4 kept for the factored order-6 recursion
         keep = _central_kept(m_max, b)
         for k in range(2, m_max + 1):
@@ -220,8 +226,36 @@ def cumulants_device(X, m_max: int, b: int, c1_host: bool = True, timer: dict | 
             if k >= 4:
                 _recursion_inplace(Mk, tensors, central)
             tensors.append(Mk)
+        return _validated_c1(X, flags, t, c1_host, st["mean"]), tensors
+    _raise_if_nonfinite(X, st["bad"])
     c1 = st["mean"].cpu().numpy() if c1_host else st["mean"]
     return c1, tensors
+
+
+def _stage_to_host(bad, mean, sums, sumsq):
+    """[bad index, mean (n), row sums (n), row sums of squares (n)] copied to
+    pinned host memory behind the current stream's work; returns (buffer, event)."""
+    torch = _native.torch_cuda()
+    dev = torch.cat([bad.to(torch.float64), mean, sums, sumsq])
+    host = torch.empty(dev.shape, dtype=torch.float64, pin_memory=True)
+    host.copy_(dev, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    return host, ev
+
+
+def _validated_c1(X, flags, t: int, c1_host: bool, mean_dev):
+    """Wait for the staged flags only (not for the work enqueued after them),
+    raise the reference's validation errors, return C_1."""
+    host, ev = flags
+    ev.synchronize()
+    v = host.numpy()
+    n = X.shape[1]
+    idx = int(v[0])
+    if idx >= 0:
+        raise ValidationError(f"non-finite value at row {idx // n + 1}, column {idx % n + 1}")
+    _check_centered_stats_host(v[1 + n:1 + 2 * n], v[1 + 2 * n:1 + 3 * n], t)
+    return v[1:1 + n].copy() if c1_host else mean_dev
 
 
 # BCG_SERIAL_ORDERS=1: one order after the other on the current stream (A/B knob)
