@@ -472,7 +472,7 @@ def main():
     if os.path.exists(tpath):
         with open(tpath) as f:
             tr = json.load(f)
-        if tr.get("plan") == "symmetric":  # captured on the current plan
+        if tr.get("plan") == "canonical":  # captured on the current (canonical symmetric) plan
             traffic = tr.get("dram_bytes_per_launch")
 
     cpu = None

@@ -23,7 +23,7 @@
 //   * warp 1 streams the factors: per tail the 25 second factors (V: the
 //     sub-blocks not holding mode 0, 72 KB at b = 6), per slab the 25
 //     first-factor slices at i0 (U: 20 KB, NU buffers);
-//   * NGRP consumer groups: a group loads a unit's elements from its ring
+//   * NGRP (4) consumer groups of 3 warps: a group loads a unit's elements from its ring
 //     stage into registers and releases the stage at once, applies the 25
 //     terms reading every factor from shared memory, and stores C_6 straight
 //     from registers to HBM (streaming stores, in place over M_6).
@@ -72,7 +72,7 @@ constexpr int lcm(int x, int y) { return x / gcd(x, y) * y; }
 
 // geometry for order 6, edge B, NRM register modes (the trailing ones),
 // NGRP consumer groups
-template <int B, int RM, int NGRP, int NU_ = 3>
+template <int B, int RM, int NGRP, int NU_ = 3, int XB = 1>
 struct Geo {
   static constexpr int M = 6;
   static constexpr int NT = term_count(M);  // 25
@@ -108,8 +108,8 @@ struct Geo {
   // on slab s - UF, the barrier's previous phase
   static constexpr int SLAB_PERIOD = NGRP / gcd(NGRP, UPS);
   static constexpr int NS = (227 * 1024 - 8 * (SEGV + NU * SEGU) - 512) / (8 * UNIT);  // ring stages
-  static constexpr int MF = lcm(NS, NGRP);
-  static constexpr int UF = lcm(NU, SLAB_PERIOD);
+  static constexpr int MF = lcm(NS, NGRP) * XB;
+  static constexpr int UF = lcm(NU, SLAB_PERIOD) * XB;
   static constexpr int NBAR = MF + NS + UF + NU + 2;
   static constexpr size_t SMEM = 8 * (size_t)(SEGV + NU * SEGU + NS * UNIT) + 8 * NBAR;
   // every bulk copy is a multiple of 16 bytes at a 16-byte aligned offset
@@ -234,14 +234,17 @@ __device__ __forceinline__ void rows_store_global(const double (&acc)[G::ROWS], 
 
 }  // namespace rs
 
+#ifndef BCG_RS_OPAQUE
+#define BCG_RS_OPAQUE 1
+#endif
 #ifndef BCG_RS_PREFETCH
 #define BCG_RS_PREFETCH 6
 #endif
 constexpr int kPrefetchUnits = BCG_RS_PREFETCH;  // M_6 units prefetched into L2 ahead of the ring
 
-template <int B, int RM, int NGRP, int NU>
-__global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU>::NTHREADS, 1) k_recursion_stream6(RecFactArgs a) {
-  using G = rs::Geo<B, RM, NGRP, NU>;
+template <int B, int RM, int NGRP, int NU, int XB>
+__global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB>::NTHREADS, 1) k_recursion_stream6(RecFactArgs a) {
+  using G = rs::Geo<B, RM, NGRP, NU, XB>;
   constexpr int NT = G::NT, NS = G::NS;
   extern __shared__ __align__(128) unsigned char rs_smem[];
   double *sv = reinterpret_cast<double *>(rs_smem);
@@ -375,9 +378,22 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU>::NTHREADS, 1) k_recur
         BCG_CHECK((h * G::SUB + ebase + rs::RowOff<0x3c, B, RM, G::ROWS - 1>::value < G::UNIT), "element", ebase);
         rs::rows_load<G, B, RM>(acc, sm + (int64_t)st * G::UNIT + h * G::SUB + ebase,
                                  std::make_integer_sequence<int, G::ROWS>{});
+        // the LDS above are only issued, not necessarily performed: order them
+        // before the bulk-copy engine's refill of this stage (async proxy)
+        // that the arrive below allows -- without this fence the refill can
+        // land first (seen as 76-224 corrupted elements of one block per
+        // launch when the producer already waits on this very stage)
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncwarp();
-        if (lane == 0) rs::bar_arrive(&mempty[st]);  // the elements are in registers: refill the stage
+        if (lane == 0) rs::bar_arrive(&mempty[st]);  // refill the stage
         rs::bar_wait(&ufull[s % G::UF], (uint32_t)((s / G::UF) & 1));
+#if BCG_RS_OPAQUE
+        // keep the 50 per-term factor offsets out of registers: without this
+        // the compiler hoists them out of the unit loop (loop-invariant),
+        // which costs ~50 registers per thread and with them a consumer group
+#pragma unroll
+        for (int q = 1; q < 6; ++q) asm volatile("" : "+r"(dig[q]));
+#endif
         rs::terms<G, B, RM>(acc, su + ub * G::SEGU, sv, dig, std::make_integer_sequence<int, NT>{});
         __syncwarp();
         if (lane == 0) rs::bar_arrive(&uempty[ub]);
@@ -389,16 +405,19 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU>::NTHREADS, 1) k_recur
   if (e >= 0 && lane == 0) rs::bar_arrive(vempty);
 }
 
-// tile / group / buffer choice (A/B knob BCG_RS_TILE):
-//   0: register modes 3,4,5 (27 elements), mode 2 across threads, 9 consumer warps, 3 U buffers (default)
-//   1: register modes 2,3,4, mode 5 across threads
-//   2: as 0 with 2 U buffers (one more ring stage)
-//   4: register modes 2..5 (81 elements), 6 consumer warps
-template <int B, int RM, int NGRP, int NU>
+// tile / group / buffer choice (A/B knob BCG_RS_TILE), cfg5 layout, L2 flushed
+// (profiles/r02_recursion_stream.txt):
+//   0: register modes 3,4,5 (27 elements), mode 2 across threads, 4 consumer
+//      groups (12 warps, 128 registers), 3 U buffers -- default, 11.2 ms
+//   1: 3 consumer groups (165 registers)                        12.0 ms
+//   2: 4 groups, 2 U buffers (one more ring stage)
+//   3: register modes 2,3,4 (mode 5 across threads), 4 groups
+//   4: register modes 2..5 (81 elements), 6 consumer warps      13.6 ms
+template <int B, int RM, int NGRP, int NU, int XB = 1>
 static cudaError_t go_stream6(const RecFactArgs &a, int nsm, cudaStream_t stream) {
-  using G = rs::Geo<B, RM, NGRP, NU>;
+  using G = rs::Geo<B, RM, NGRP, NU, XB>;
   static_assert(G::ok, "stream6 geometry");
-  auto kern = k_recursion_stream6<B, RM, NGRP, NU>;
+  auto kern = k_recursion_stream6<B, RM, NGRP, NU, XB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
   if (e != cudaSuccess) return e;
   const int64_t grid = a.nkeys < nsm ? a.nkeys : nsm;
@@ -420,12 +439,11 @@ cudaError_t launch_recursion_stream6(const RecFactArgs &a, int b, cudaStream_t s
     if (nsm <= 0) nsm = 148;
   }
   static const int tile = getenv("BCG_RS_TILE") ? atoi(getenv("BCG_RS_TILE")) : 0;
-  if (tile == 1) return go_stream6<6, 0x1c, 3, 3>(a, nsm, stream);
-  if (tile == 2) return go_stream6<6, 0x38, 3, 2>(a, nsm, stream);
+  if (tile == 1) return go_stream6<6, 0x38, 3, 3>(a, nsm, stream);
+  if (tile == 2) return go_stream6<6, 0x38, 4, 2>(a, nsm, stream);
+  if (tile == 3) return go_stream6<6, 0x1c, 4, 3>(a, nsm, stream);
   if (tile == 4) return go_stream6<6, 0x3c, 6, 3>(a, nsm, stream);
-  if (tile == 5) return go_stream6<6, 0x38, 4, 3>(a, nsm, stream);
-  if (tile == 6) return go_stream6<6, 0x38, 5, 3>(a, nsm, stream);
-  return go_stream6<6, 0x38, 3, 3>(a, nsm, stream);
+  return go_stream6<6, 0x38, 4, 3>(a, nsm, stream);
 }
 
 }  // namespace bcg

@@ -142,6 +142,25 @@ def test_streamed_recursion_is_bitwise_the_register_kernel(tmp_path):
         assert np.array_equal(v7[key], v2[key]), key
 
 
+def test_streamed_recursion_is_deterministic_under_load():
+    """v7 releases its ring stages as soon as a unit is loaded and its
+    consumer groups run ahead of each other; repeated launches on a layout
+    with ~34 blocks per CTA must agree bit for bit (a stage refilled before
+    its loads were performed showed up here as a few corrupted elements)."""
+    from paper_1701_05420_b200.cumulants import cumulants_device
+
+    rng = np.random.default_rng(77)
+    x = torch.from_numpy(rng.exponential(1.0, size=(200, 60)) + rng.standard_normal((200, 60))).cuda()
+    first = None
+    for _ in range(4):
+        _, ts = cumulants_device(x, 6, 6, c1_host=False)
+        c6 = ts[-1].data.clone()
+        if first is None:
+            first = c6
+        else:
+            assert torch.equal(first, c6)
+
+
 def test_factored_recursion_matches_the_partition_sum(tmp_path):
     """K3 factored (production) vs the reference's partition sum (the same
     moments; BCG_RECURSION_PARTITION=1 is read once per process, hence the
