@@ -109,6 +109,10 @@ int bcg_plan_gemm(const bcg_plan *plan, int32_t i, int32_t *ngemm, int32_t *spli
  * elements its GEMMs compute (S_m for a full plan, fewer for a symmetric one:
  * 2 * t * produced is the FP64 work the DMMA kernel executes). */
 int bcg_plan_output(const bcg_plan *plan, int64_t *S_out, int64_t *produced);
+/* Elements the moment GEMMs' CTA tiles cover (tiled area incl. masked
+ * staircase and edge positions; produced / tiled is the tile efficiency) and
+ * the number of narrow band-edge tiles among them. */
+int bcg_plan_tiled(const bcg_plan *plan, int64_t *tiled, int64_t *edge_tiles);
 /* Host-only plan (tables built, nothing uploaded): layout queries work
  * without a GPU; compute calls on it fail with BCG_EINVAL. */
 int bcg_plan_create_host(int64_t n, int32_t m, int32_t b, bcg_plan **plan);

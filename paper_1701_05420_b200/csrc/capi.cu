@@ -64,7 +64,7 @@ Slicing choose_slicing(const bcg::Plan &p, int64_t t) {
   // to fill the GPU by itself (>= 8 waves) runs one slice per launch and
   // accumulates straight into `out` (no workspace, no reduce pass).
   int64_t ntiles = 0;
-  for (const bcg::Gemm &g : p.gemm) ntiles += (int64_t)g.tiles.size();
+  for (const bcg::Gemm &g : p.gemm) ntiles += (int64_t)(g.tiles.size() + g.etiles.size());
   ntiles = std::max<int64_t>(1, ntiles);
   const int64_t S = p.S_out;
   int64_t cap = kWsCap / std::max<int64_t>(1, S * 8);
@@ -118,7 +118,7 @@ int run_moment(const bcg::Plan &p, const double *xt, int64_t t, int64_t ldt, dou
     // every GEMM of the plan writes a disjoint set of keys of the same slice
     // partials, so one reduce pass follows them all
     for (const bcg::Gemm &g : p.gemm) {
-      if (g.tiles.empty()) continue;
+      if (g.tiles.empty() && g.etiles.empty()) continue;
       a.h = g.h;
       a.r = g.r;
       a.rowcols = g.d_rowcols;
@@ -129,16 +129,22 @@ int run_moment(const bcg::Plan &p, const double *xt, int64_t t, int64_t ldt, dou
       a.col_rank = g.d_col_rank;
       a.col_olin = g.d_col_olin;
       a.col_size = g.d_col_size;
-      a.tiles = g.d_tiles;
-      a.tile_kmin = g.d_tile_kmin;
-      a.tile_kmax = g.d_tile_kmax;
-      a.ntiles = (int)g.tiles.size();
       a.R = g.R;
       a.C = g.C;
-      const int64_t grid = (int64_t)a.ntiles * a.nslices;
-      if (grid > INT32_MAX) return fail(BCG_EINVAL, "moment grid too large");
-      CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream, g.tm, g.tn), "moment kernel");
-      bcg::g_launches++;
+      // the full-width tiles, then the band-edge tiles (tm x etn): disjoint
+      // elements of the same partials, each summed in the same sample order
+      for (int pass = 0; pass < 2; ++pass) {
+        const auto &tl = pass == 0 ? g.tiles : g.etiles;
+        if (tl.empty()) continue;
+        a.tiles = pass == 0 ? g.d_tiles : g.d_etiles;
+        a.tile_kmin = pass == 0 ? g.d_tile_kmin : g.d_etile_kmin;
+        a.tile_kmax = pass == 0 ? g.d_tile_kmax : g.d_etile_kmax;
+        a.ntiles = (int)tl.size();
+        const int64_t grid = (int64_t)a.ntiles * a.nslices;
+        if (grid > INT32_MAX) return fail(BCG_EINVAL, "moment grid too large");
+        CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream, g.tm, pass == 0 ? g.tn : g.etn), "moment kernel");
+        bcg::g_launches++;
+      }
     }
     if (a.nslices > 1) {
       CUDA_TRY(bcg::launch_reduce_slices(a.ws, a.nslices, a.S, lo, hi, out, stream),
@@ -242,6 +248,18 @@ int bcg_plan_output(const bcg_plan *plan, int64_t *S_out, int64_t *produced) {
   return BCG_OK;
 }
 
+int bcg_plan_tiled(const bcg_plan *plan, int64_t *tiled, int64_t *edge_tiles) {
+  if (!plan) return fail(BCG_EINVAL, "plan is NULL");
+  int64_t area = 0, ne = 0;
+  for (const bcg::Gemm &g : plan->p.gemm) {
+    area += (int64_t)g.tiles.size() * g.tm * g.tn + (int64_t)g.etiles.size() * g.tm * g.etn;
+    ne += (int64_t)g.etiles.size();
+  }
+  if (tiled) *tiled = area;
+  if (edge_tiles) *edge_tiles = ne;
+  return BCG_OK;
+}
+
 int bcg_plan_selfcheck(const bcg_plan *plan) {
   if (!plan) return fail(BCG_EINVAL, "plan is NULL");
   const bcg::Plan &p = plan->p;
@@ -252,9 +270,11 @@ int bcg_plan_selfcheck(const bcg_plan *plan) {
   std::vector<uint8_t> seen(S, 0);
   int64_t count = 0;
   for (const bcg::Gemm &g : p.gemm)
-  for (const bcg::Tile &tl : g.tiles) {
+  for (int pass = 0; pass < 2; ++pass)
+  for (const bcg::Tile &tl : pass == 0 ? g.tiles : g.etiles) {
+    const int tw = pass == 0 ? g.tn : g.etn;
     for (int64_t r = tl.row0; r < std::min<int64_t>(tl.row0 + g.tm, g.R); ++r) {
-      for (int64_t c = tl.col0; c < std::min<int64_t>(tl.col0 + g.tn, g.C); ++c) {
+      for (int64_t c = tl.col0; c < std::min<int64_t>(tl.col0 + tw, g.C); ++c) {
         if (c < g.row_cstart[r]) continue;
         const int64_t kg = g.row_keybase[r] + g.col_rank[c];
         if (kg < 0 || kg >= (int64_t)p.koff.size()) return fail(BCG_EINVAL, "selfcheck: key index out of range");

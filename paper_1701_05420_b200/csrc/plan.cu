@@ -113,23 +113,33 @@ int default_variant() {  // only the v1 kernel family (variant 0) remains
 
 // Staircase tile list of GEMM g for a tm x tn CTA tile.  Returns the number
 // of tiles.
+// etn > 0: a band's last tile is a tm x etn "edge" tile when at most etn
+// columns remain (listed in etiles / ekmin / ekmax; *nedge counts them)
 static int64_t build_tiles(const Plan &p, const Gemm &g, int tm, int tn, std::vector<Tile> *tiles,
-                           std::vector<int32_t> *kmin_out, std::vector<int32_t> *kmax_out) {
+                           std::vector<int32_t> *kmin_out, std::vector<int32_t> *kmax_out, int etn = 0,
+                           std::vector<Tile> *etiles = nullptr, std::vector<int32_t> *ekmin = nullptr,
+                           std::vector<int32_t> *ekmax = nullptr, int64_t *nedge = nullptr) {
   if (tiles) tiles->clear();
   if (kmin_out) kmin_out->clear();
   if (kmax_out) kmax_out->clear();
+  if (etiles) etiles->clear();
+  if (ekmin) ekmin->clear();
+  if (ekmax) ekmax->clear();
+  if (nedge) *nedge = 0;
   int64_t ntiles = 0;
   for (int64_t r0 = 0; r0 < g.R; r0 += tm) {
     const int64_t r1 = std::min<int64_t>(r0 + tm, g.R);
     for (int64_t c0 = g.row_cstart[r0]; c0 < g.C; c0 += tn) {
-      const int64_t c1 = std::min<int64_t>(c0 + tn, g.C);
+      const bool edge = etn > 0 && g.C - c0 <= etn;
+      const int64_t c1 = std::min<int64_t>(c0 + (edge ? etn : tn), g.C);
       int32_t cache_lo = 0, cache_hi = 0;
       int64_t kmin = INT64_MAX, kmax = -1;
       // a tile of this band holds row r0 (its columns start at or after
       // r0's suffix start, the band's smallest); the key range is only
       // needed for the tile list itself
       if (!kmin_out && !kmax_out) {
-        ++ntiles;
+        if (edge && nedge) ++*nedge;
+        else ++ntiles;
         continue;
       }
       for (int64_t rr = r0; rr < r1; ++rr) {
@@ -152,6 +162,13 @@ static int64_t build_tiles(const Plan &p, const Gemm &g, int tm, int tn, std::ve
         kmax = std::max<int64_t>(kmax, g.row_keybase[rr] + rhi);
       }
       if (kmax < 0) continue;  // below the staircase
+      if (edge) {
+        if (nedge) ++*nedge;
+        if (etiles) etiles->push_back(Tile{(int32_t)r0, (int32_t)c0});
+        if (ekmin) ekmin->push_back((int32_t)kmin);
+        if (ekmax) ekmax->push_back((int32_t)kmax);
+        continue;
+      }
       ++ntiles;
       if (tiles) tiles->push_back(Tile{(int32_t)r0, (int32_t)c0});
       if (kmin_out) kmin_out->push_back((int32_t)kmin);
@@ -422,7 +439,14 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant, bool sym) 
   p.produced = 0;
   for (Gemm &g : p.gemm) {
     choose_shape(p, g);
-    build_tiles(p, g, g.tm, g.tn, &g.tiles, &g.tile_kmin, &g.tile_kmax);
+    // narrow edge tiles where the band's overhang would leave half a tile
+    // masked (tm x tn/2 must be a compiled shape)
+    g.etn = 0;
+    const int half = g.tn / 2;
+    if (!std::getenv("BCG_NO_EDGE_TILES") && half >= 8 && v1_shape_supported(pick_kc((int)p.n), m, g.tm, half))
+      g.etn = half;
+    build_tiles(p, g, g.tm, g.tn, &g.tiles, &g.tile_kmin, &g.tile_kmax, g.etn, &g.etiles, &g.etile_kmin,
+                &g.etile_kmax);
     p.produced += gemm_produced(g);
   }
   // symmetric plan: blocks with a repeated block index of edge > 1 hold
@@ -558,6 +582,9 @@ std::string upload_plan(Plan &p) {
     UPG(d_tiles, tiles);
     UPG(d_tile_kmin, tile_kmin);
     UPG(d_tile_kmax, tile_kmax);
+    UPG(d_etiles, etiles);
+    UPG(d_etile_kmin, etile_kmin);
+    UPG(d_etile_kmax, etile_kmax);
 #undef UPG
   }
 #define UP(d, s) if (e == cudaSuccess) e = up(&p.d, p.s)
@@ -584,7 +611,8 @@ std::string upload_plan(Plan &p) {
 void free_plan(Plan &p) {
   for (Gemm &g : p.gemm) {
     void *gp[] = {g.d_rowcols, g.d_colcols, g.d_row_keybase, g.d_row_olin, g.d_row_cstart,
-                  g.d_col_rank, g.d_col_olin, g.d_col_size, g.d_tiles, g.d_tile_kmin, g.d_tile_kmax};
+                  g.d_col_rank, g.d_col_olin, g.d_col_size, g.d_tiles, g.d_tile_kmin, g.d_tile_kmax,
+                  g.d_etiles, g.d_etile_kmin, g.d_etile_kmax};
     for (void *q : gp)
       if (q) cudaFree(q);
   }

@@ -41,12 +41,19 @@ struct Gemm {
   std::vector<int32_t> col_size;        // |R| = prod edges(R)
   std::vector<Tile> tiles;
   std::vector<int32_t> tile_kmin, tile_kmax;  // key range a tile touches
+  // edge tiles: a band's last tile when at most etn columns remain, run with
+  // a tm x etn CTA tile (etn = tn / 2; 0 = none) -- the staircase overhang
+  int etn = 0;
+  std::vector<Tile> etiles;
+  std::vector<int32_t> etile_kmin, etile_kmax;
   // device copies
   int16_t *d_rowcols = nullptr, *d_colcols = nullptr;
   int32_t *d_row_keybase = nullptr, *d_row_olin = nullptr, *d_row_cstart = nullptr;
   int32_t *d_col_rank = nullptr, *d_col_olin = nullptr, *d_col_size = nullptr;
   Tile *d_tiles = nullptr;
   int32_t *d_tile_kmin = nullptr, *d_tile_kmax = nullptr;
+  Tile *d_etiles = nullptr;
+  int32_t *d_etile_kmin = nullptr, *d_etile_kmax = nullptr;
 };
 
 struct Plan {

@@ -169,3 +169,18 @@ def test_no_cpu_fallback_without_a_device():
     out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "CUDA_VISIBLE_DEVICES": ""},
                          capture_output=True, text=True, timeout=300)
     assert "raised:" in out.stdout, out.stdout + out.stderr
+
+
+def test_edge_tiles_cover_the_staircase_overhang():
+    # band-edge tiles (tm x tn/2) where at most half a tile of columns remains:
+    # cfg4's order-6 plan covers its 4.50M canonical elements with >= 0.90 of
+    # the tiled area (0.88 without them), and every element exactly once
+    import ctypes
+
+    lib = _native.lib()
+    plan = _native.Plan(36, 6, 3, host_only=True)
+    tiled, edges = ctypes.c_int64(), ctypes.c_int64()
+    _native.check(lib.bcg_plan_tiled(plan.handle, ctypes.byref(tiled), ctypes.byref(edges)))
+    _, produced = plan.output()
+    assert edges.value > 0 and produced / tiled.value >= 0.90
+    _native.check(lib.bcg_plan_selfcheck(plan.handle))
