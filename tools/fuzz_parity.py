@@ -1,6 +1,8 @@
 """Randomized parity sweep: random (n, m, b, t, distribution) through the
 GPU path (moment, cumulants_upto, moment_parallel_blocks, outer_prod_cum)
 against the CPU oracle.  Prints one line per failure and a summary.
+Moments: rtol 1e-12; cumulants: |got - want| <= 1e-9 |want| + 1e-11 x the
+magnitude of the terms the recursion subtracts (cancellation-aware).
 
     python tools/fuzz_parity.py --cases 300 --seed 1
 """
@@ -56,14 +58,29 @@ def main():
             cs = bcg.cumulants_upto(x, m, b=b)
             c1, want = orc.cumulants_upto(x, m, b)
             np.testing.assert_allclose(cs[1], c1, rtol=1e-12, atol=1e-12)
+            # an element's rounding error scales with the magnitudes its
+            # computation cancels: the sample sum's absolute moment
+            # (1/t) sum_l prod |x_c| plus, from order 4, the reference's
+            # partition sums of |lower cumulants| (bc/cumulants.py:53-136) --
+            # not with |C_k| itself
+            xc = x - x.mean(axis=0)
             for k in range(2, m + 1):
                 w = want[k]
-                scale = float(np.max(np.abs(w))) if w.size else 1.0
-                np.testing.assert_allclose(cs[k].packed_host(), w, rtol=1e-9, atol=1e-11 * max(scale, 1e-300),
-                                           err_msg=f"C{k}")
+                term = orc.moment(np.abs(xc), k, b)
+                if k >= 4:
+                    absl = {j: np.abs(want[j]) for j in range(2, k - 1)}
+                    for sigma in range(2, k // 2 + 1):
+                        term = term + orc.outer_prod_cum(k, sigma, absl, n, b)
+                err = np.abs(cs[k].packed_host() - w)
+                bad = err > 1e-9 * np.abs(w) + 1e-11 * term + 1e-300
+                if bad.any():
+                    i = int(np.argmax(bad))
+                    raise AssertionError(f"C{k}: {int(bad.sum())} elements, e.g. [{i}] got-want {err[i]:.3e} "
+                                         f"|want| {abs(w[i]):.3e} term scale {term[i]:.3e}")
         except Exception as exc:  # report and continue
             fails += 1
-            print(f"FAIL {what}: {str(exc).splitlines()[0][:200]}", flush=True)
+            msg = " | ".join(line.strip() for line in str(exc).splitlines() if line.strip())
+            print(f"FAIL {what}: {type(exc).__name__}: {msg[:600]}", flush=True)
     print(f"{a.cases} cases, {fails} failures, {time.time() - t0:.1f} s", flush=True)
 
 
