@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--weak", action="store_true", help="N > 1: t rows per GPU (own seed) instead of a t-row split")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the multi-GPU (NCCL sample-split) code path even with one rank (validation)")
     ap.add_argument("--dry-run", action="store_true",
                     help="launch / rendezvous / shard bookkeeping only (gloo, no GPU): one JSON line")
     ap.add_argument("--t", type=int, default=0,
@@ -84,14 +86,15 @@ def relaunch_if_needed(args) -> bool:
     return True
 
 
-def config_dict(cfg, t_total, world, weak, overridden):
+def config_dict(cfg, t_total, world, weak, overridden, sharded=False):
     note = f"; t overridden, BASELINE t={cfg.t}" if overridden else ""
     split = (f"weak: {t_total // world} rows per GPU, own seed per rank" if weak
              else f"strong: rows [t r/N, t (r+1)/N) of the canonical matrix")
     return {
         "workload": f"{cfg.name}: cumulants_upto C1..C{cfg.m}, t={t_total} x n={cfg.n}, b={cfg.b} ({cfg.desc}){note}",
         "t": t_total, "n": cfg.n, "b": cfg.b, "m_max": cfg.m,
-        "parallelism": f"t-shard x{world} ({split}), NCCL reduce-scatter/all-gather" if world > 1 else "single GPU",
+        "parallelism": (f"t-shard x{world} ({split}), NCCL reduce-scatter/all-gather" if world > 1 or sharded
+                        else "single GPU"),
         "l2": "inputs larger than L2 (X = %.0f MB per GPU vs 126 MB L2)" % (t_total / world * cfg.n * 8 / 1e6),
     }
 
@@ -373,8 +376,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # the NCCL sample-split path: every N > 1 run, and --sharded at N = 1
+    dist_mode = world > 1 or args.sharded
+    if dist_mode:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
 
     if args.weak:
         t_local = args.t or cfg.t
@@ -385,7 +392,7 @@ def main():
         t_total = args.t or cfg.t
         lo, hi = shard_bounds(t_total, world, rank)
         t_local = hi - lo
-        if world == 1:
+        if not dist_mode:
             x_host = workloads.generate(cfg.name, t_total)
             X = torch.from_numpy(x_host).cuda()
         else:
@@ -405,16 +412,16 @@ def main():
     exec_top_local = 2.0 * t_local * produced_top
 
     def barrier():
-        if world > 1:
+        if dist_mode:
             dist.barrier()
 
     def step_device(timer=None):
-        if world > 1:
+        if dist_mode:
             return cumulants_upto_sharded(X, cfg.m, cfg.b, timer=timer)
         return cumulants_device(X, cfg.m, cfg.b, c1_host=False, timer=timer)
 
     def step_e2e():
-        if world > 1:
+        if dist_mode:
             mean, ts = cumulants_upto_sharded(x_pinned, cfg.m, cfg.b)
             return [mean.cpu()] + [t.cpu() for t in ts]
         cs = bcg.cumulants_upto(x_pinned, cfg.m, b=cfg.b)
@@ -432,7 +439,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         ms = e0.elapsed_time(e1) / steps
-        if world > 1:
+        if dist_mode:
             v = torch.tensor([ms], dtype=torch.float64, device="cuda")
             dist.all_reduce(v, op=dist.ReduceOp.MAX)
             ms = float(v.item())
@@ -465,7 +472,7 @@ def main():
         e2e = {"value": flops_total / (ms_e2e / 1e3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": int(x_host.nbytes), "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                "api": ("paper_1701_05420_b200.cumulants_upto(pinned host tensor) + packed_host() per order"
-                       if world == 1 else "distributed.cumulants_upto_sharded(pinned host shard) + .cpu()")}
+                       if not dist_mode else "distributed.cumulants_upto_sharded(pinned host shard) + .cpu()")}
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}.json")
@@ -493,7 +500,7 @@ def main():
             "vs_baseline": None,
             "dtype": "f64",
             "data": f"synthetic ({cfg.name} recipe, workloads.py; seeded PCG64), resident in HBM",
-            "config": config_dict(cfg, t_total, world, args.weak, bool(args.t)),
+            "config": config_dict(cfg, t_total, world, args.weak, bool(args.t), dist_mode),
             "value_def": ("reference-equivalent rate: sum_k 2 t S_k (every stored element, as the reference "
                           "computes) / step time; the symmetric plans execute fewer FLOPs (roofline)"),
             "roofline": {
@@ -510,7 +517,7 @@ def main():
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_mode:
         dist.destroy_process_group()
 
 
