@@ -32,8 +32,12 @@ struct MomentArgs {
 };
 
 // fixed split-K slice length (samples): the summation order of every element
-// depends on t only (see moment.cu)
-constexpr int64_t kSliceLen = 16384;
+// depends on t only (see moment.cu).  Longer slices cut the partials' DRAM
+// traffic but cost wave balance (profiles/r02_moment_experiments.log (7)).
+#ifndef BCG_SLICE_LEN
+#define BCG_SLICE_LEN 16384
+#endif
+constexpr int64_t kSliceLen = BCG_SLICE_LEN;
 size_t moment_smem_bytes(int KC, int n, int tm = 64, int tn = 64);
 int pick_kc(int n);
 bool v1_shape_supported(int KC, int m, int tm, int tn);
