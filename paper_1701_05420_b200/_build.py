@@ -15,7 +15,7 @@ SOURCES = ["plan.cu", "moment.cu", "elementwise.cu", "recursion.cu", "recursion_
 # moment.cu is compiled once per part: part 0 = host code + dispatch, parts
 # 1..6 = the kernel instantiations of one CTA tile shape each (parallel nvcc)
 # (recursion_fact.cu likewise: part 0 = dispatch, 1..6 = (m, b) instantiations)
-PARTS = {"moment.cu": ("BCG_MOMENT_PART", 7), "recursion_fact.cu": ("BCG_RF_PART", 7)}
+PARTS = {"moment.cu": ("BCG_MOMENT_PART", 9), "recursion_fact.cu": ("BCG_RF_PART", 7)}
 UNITS = [(s, []) for s in SOURCES if s not in PARTS] + [
     (s, [f"-D{d}={k}"]) for s, (d, n) in PARTS.items() for k in range(n)]
 HEADERS = ["plan.h", "kernels.h", "kr.cuh", "rf_terms.cuh"]

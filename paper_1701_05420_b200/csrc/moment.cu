@@ -43,12 +43,16 @@
 #include "plan.h"
 
 #ifndef BCG_MOMENT_PART
-#error "moment.cu is compiled once per BCG_MOMENT_PART (0..6), see _build.py"
+#error "moment.cu is compiled once per BCG_MOMENT_PART (0..8), see _build.py"
 #endif
 
 namespace bcg {
 
 constexpr int kThreads = 128;
+// CTA threads of a tile shape: 4 warps, or 8 for the 8192-element tiles
+// (128 x 64, 64 x 128: a 32 x 32 warp tile each, half the Khatri-Rao build
+// per FMA of one dimension)
+__host__ __device__ constexpr int moment_threads(int tm, int tn) { return tm * tn >= 8192 ? 256 : 128; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -105,16 +109,19 @@ __device__ __forceinline__ int kr_swizzle(int row) { return ((row & 3) << 2) | (
 
 template <int KC, int TM, int TN>
 struct V1Shape {
-  static constexpr int WGN = TN >= 4 * TM ? 4 : (TN >= TM ? 2 : 1);
-  static constexpr int WGM = 4 / WGN;
+  static constexpr int NTH = moment_threads(TM, TN);
+  static constexpr int NW = NTH / 32;
+  static constexpr int WGN = NW == 8 ? TN / 32 : (TN >= 4 * TM ? 4 : (TN >= TM ? 2 : 1));
+  static constexpr int WGM = NW / WGN;
   static constexpr int WM = TM / WGM, WN = TN / WGN;
   static constexpr int MT = WM / 8, NT = WN / 8;
   static constexpr int LDK = KC;       // factor row stride (doubles), swizzled
   static_assert(KC == 16, "the TMA box is one 128-byte swizzle span of samples");
-  static constexpr int PA = kThreads / TM, PB = kThreads / TN;  // threads per factor row
-  static constexpr int NPAIR = KC / 2;                          // sample pairs per chunk
+  static constexpr int PA = NTH / TM, PB = NTH / TN;  // threads per factor row
+  static constexpr int NPAIR = KC / 2;                // sample pairs per chunk
+  static_assert(WGM * WGN == NW, "warp grid");
   static_assert(WM % 8 == 0 && WN % 8 == 0, "warp tile must be a multiple of 8");
-  static_assert(kThreads % TM == 0 && kThreads % TN == 0, "TM, TN must divide 128");
+  static_assert(NTH % TM == 0 && NTH % TN == 0, "TM, TN must divide the CTA threads");
   static_assert(NPAIR % PA == 0 && NPAIR % PB == 0, "sample pairs must split evenly");
 };
 
@@ -154,7 +161,8 @@ __device__ __forceinline__ double2 kr_pair(const double *const (&row)[8], const 
 
 // H, R: compile-time row / column mode counts (0: the runtime a.h / a.r)
 template <int KC, int H, int R, int TM, int TN>
-__global__ void __launch_bounds__(kThreads) k_moment_dmma(const __grid_constant__ CUtensorMap tmap, MomentArgs a) {
+__global__ void __launch_bounds__(moment_threads(TM, TN)) k_moment_dmma(const __grid_constant__ CUtensorMap tmap,
+                                                                        MomentArgs a) {
   using SH = V1Shape<KC, TM, TN>;
   constexpr int LDX = KC;                  // staged row: 16 doubles = one 128-byte swizzle span
   constexpr int LDK = SH::LDK, MT = SH::MT, NT = SH::NT;
@@ -388,7 +396,7 @@ bool v1_shape_supported(int KC, int m, int tm, int tn) {
   if (tm == 64 && tn == 64) return true;
   if (m < 2 || m > 8) return false;
   return (tm == 16 && tn == 128) || (tm == 128 && tn == 16) || (tm == 32 && tn == 64) ||
-         (tm == 64 && tn == 32) || (tm == 32 && tn == 32);
+         (tm == 64 && tn == 32) || (tm == 32 && tn == 32) || (tm == 128 && tn == 64) || (tm == 64 && tn == 128);
 }
 
 #define BCG_SHAPE_DECL(TMV, TNV) \
@@ -399,6 +407,8 @@ BCG_SHAPE_DECL(128, 16)
 BCG_SHAPE_DECL(32, 64)
 BCG_SHAPE_DECL(64, 32)
 BCG_SHAPE_DECL(32, 32)
+BCG_SHAPE_DECL(128, 64)
+BCG_SHAPE_DECL(64, 128)
 #undef BCG_SHAPE_DECL
 
 cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t stream, int tm, int tn) {
@@ -408,7 +418,7 @@ cudaError_t launch_moment(const MomentArgs &args, int KC, int grid, cudaStream_t
   if (!v1_shape_supported(KC, h + r, tm, tn)) return cudaErrorInvalidValue;
 #define GO(TMV, TNV) \
   if (tm == TMV && tn == TNV) return launch_moment_##TMV##x##TNV(args, grid, stream, generic);
-  GO(64, 64) GO(16, 128) GO(128, 16) GO(32, 64) GO(64, 32) GO(32, 32)
+  GO(64, 64) GO(16, 128) GO(128, 16) GO(32, 64) GO(64, 32) GO(32, 32) GO(128, 64) GO(64, 128)
 #undef GO
   return cudaErrorInvalidValue;
 }
@@ -463,7 +473,7 @@ static cudaError_t go_v1(const MomentArgs &args, int grid, cudaStream_t stream) 
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kThreads, smem, stream>>>(map, args);
+  kern<<<grid, moment_threads(TM, TN), smem, stream>>>(map, args);
   return cudaGetLastError();
 }
 
@@ -503,6 +513,12 @@ static cudaError_t go_v1(const MomentArgs &args, int grid, cudaStream_t stream) 
 #elif BCG_MOMENT_PART == 6
 #define TMV_ 32
 #define TNV_ 32
+#elif BCG_MOMENT_PART == 7
+#define TMV_ 128
+#define TNV_ 64
+#elif BCG_MOMENT_PART == 8
+#define TMV_ 64
+#define TNV_ 128
 #endif
 #define BCG_DEF_EXPAND(A, B) BCG_SHAPE_DEF(A, B)
 BCG_DEF_EXPAND(TMV_, TNV_)

@@ -200,9 +200,18 @@ static void choose_shape(const Plan &p, Gemm &g) {
     return;
   }
   if (pick_kc((int)p.n) != 16 || m < 2 || m > 8) return;
-  static const int shapes[][2] = {{64, 64}, {16, 128}, {128, 16}, {32, 64}, {64, 32}, {32, 32}};
+  // 64 x 128 before 128 x 64 (equal modeled cost; measured 1% faster at the
+  // cfg5 order-6 staircase, profiles/r02_moment_experiments.log (8))
+  static const int shapes[][2] = {{64, 64}, {16, 128}, {128, 16}, {32, 64}, {64, 32}, {32, 32}, {64, 128}, {128, 64}};
   double best = gemm_cost(p, g, 64, 64);
+  // 8-warp shapes (64 x 128, 128 x 64) halve one dimension's Khatri-Rao build
+  // per FMA: a win where the build is expensive (three-mode factors on both
+  // sides: cfg5 order 6 -7.3%), a loss for two-mode factors (cfg3 order 5's
+  // (2|3) GEMM: +2%); BCG_NO_WIDE_TILES=1 disables them (A/B knob)
+  static const bool no_wide = std::getenv("BCG_NO_WIDE_TILES") != nullptr;
+  const bool wide_ok = !no_wide && g.h >= 3 && g.r >= 3;
   for (const auto &sh : shapes) {
+    if (!wide_ok && sh[0] * sh[1] >= 8192) continue;
     const double c = gemm_cost(p, g, sh[0], sh[1]);
     if (c < best * 0.97) {  // switch only for a clear modeled gain
       best = c;

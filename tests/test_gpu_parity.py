@@ -382,7 +382,7 @@ def test_factored_recursion_matches_oracle(n, m, b, t, rng):
         np.testing.assert_allclose(packed(fact[k]), want[k], rtol=1e-9, atol=1e-12)
 
 
-@pytest.mark.parametrize("tile", ["64x64", "16x128", "128x16", "32x64", "64x32", "32x32"])
+@pytest.mark.parametrize("tile", ["64x64", "16x128", "128x16", "32x64", "64x32", "32x32", "128x64", "64x128"])
 def test_v1_tile_shapes_match_oracle_and_each_other(tile, monkeypatch, rng):
     """Every v1 CTA tile shape (BCG_TILE override of the plan's model choice)
     gives the oracle's moments and bitwise-identical results."""
