@@ -64,7 +64,7 @@ Slicing choose_slicing(const bcg::Plan &p, int64_t t) {
   // to fill the GPU by itself (>= 8 waves) runs one slice per launch and
   // accumulates straight into `out` (no workspace, no reduce pass).
   int64_t ntiles = 0;
-  for (const bcg::Gemm &g : p.gemm) ntiles += (int64_t)(g.tiles.size() + g.etiles.size());
+  for (const bcg::Gemm &g : p.gemm) ntiles += (int64_t)(g.tiles.size() + g.et[0].size() + g.et[1].size());
   ntiles = std::max<int64_t>(1, ntiles);
   const int64_t S = p.S_out;
   int64_t cap = kWsCap / std::max<int64_t>(1, S * 8);
@@ -118,7 +118,7 @@ int run_moment(const bcg::Plan &p, const double *xt, int64_t t, int64_t ldt, dou
     // every GEMM of the plan writes a disjoint set of keys of the same slice
     // partials, so one reduce pass follows them all
     for (const bcg::Gemm &g : p.gemm) {
-      if (g.tiles.empty() && g.etiles.empty()) continue;
+      if (g.tiles.empty() && g.et[0].empty() && g.et[1].empty()) continue;
       a.h = g.h;
       a.r = g.r;
       a.rowcols = g.d_rowcols;
@@ -131,18 +131,20 @@ int run_moment(const bcg::Plan &p, const double *xt, int64_t t, int64_t ldt, dou
       a.col_size = g.d_col_size;
       a.R = g.R;
       a.C = g.C;
-      // the full-width tiles, then the band-edge tiles (tm x etn): disjoint
-      // elements of the same partials, each summed in the same sample order
-      for (int pass = 0; pass < 2; ++pass) {
-        const auto &tl = pass == 0 ? g.tiles : g.etiles;
+      // the full-width tiles, then the band-edge tiles (tm x ew[0], tm x
+      // ew[1]): disjoint elements of the same partials, each summed in the
+      // same sample order
+      for (int pass = 0; pass < 3; ++pass) {
+        const auto &tl = pass == 0 ? g.tiles : g.et[pass - 1];
         if (tl.empty()) continue;
-        a.tiles = pass == 0 ? g.d_tiles : g.d_etiles;
-        a.tile_kmin = pass == 0 ? g.d_tile_kmin : g.d_etile_kmin;
-        a.tile_kmax = pass == 0 ? g.d_tile_kmax : g.d_etile_kmax;
+        a.tiles = pass == 0 ? g.d_tiles : g.d_et[pass - 1];
+        a.tile_kmin = pass == 0 ? g.d_tile_kmin : g.d_ekmin[pass - 1];
+        a.tile_kmax = pass == 0 ? g.d_tile_kmax : g.d_ekmax[pass - 1];
         a.ntiles = (int)tl.size();
         const int64_t grid = (int64_t)a.ntiles * a.nslices;
         if (grid > INT32_MAX) return fail(BCG_EINVAL, "moment grid too large");
-        CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream, g.tm, pass == 0 ? g.tn : g.etn), "moment kernel");
+        CUDA_TRY(bcg::launch_moment(a, sl.KC, (int)grid, stream, g.tm, pass == 0 ? g.tn : g.ew[pass - 1]),
+                 "moment kernel");
         bcg::g_launches++;
       }
     }
@@ -252,8 +254,11 @@ int bcg_plan_tiled(const bcg_plan *plan, int64_t *tiled, int64_t *edge_tiles) {
   if (!plan) return fail(BCG_EINVAL, "plan is NULL");
   int64_t area = 0, ne = 0;
   for (const bcg::Gemm &g : plan->p.gemm) {
-    area += (int64_t)g.tiles.size() * g.tm * g.tn + (int64_t)g.etiles.size() * g.tm * g.etn;
-    ne += (int64_t)g.etiles.size();
+    area += (int64_t)g.tiles.size() * g.tm * g.tn;
+    for (int i = 0; i < 2; ++i) {
+      area += (int64_t)g.et[i].size() * g.tm * g.ew[i];
+      ne += (int64_t)g.et[i].size();
+    }
   }
   if (tiled) *tiled = area;
   if (edge_tiles) *edge_tiles = ne;
@@ -270,9 +275,9 @@ int bcg_plan_selfcheck(const bcg_plan *plan) {
   std::vector<uint8_t> seen(S, 0);
   int64_t count = 0;
   for (const bcg::Gemm &g : p.gemm)
-  for (int pass = 0; pass < 2; ++pass)
-  for (const bcg::Tile &tl : pass == 0 ? g.tiles : g.etiles) {
-    const int tw = pass == 0 ? g.tn : g.etn;
+  for (int pass = 0; pass < 3; ++pass)
+  for (const bcg::Tile &tl : pass == 0 ? g.tiles : g.et[pass - 1]) {
+    const int tw = pass == 0 ? g.tn : g.ew[pass - 1];
     for (int64_t r = tl.row0; r < std::min<int64_t>(tl.row0 + g.tm, g.R); ++r) {
       for (int64_t c = tl.col0; c < std::min<int64_t>(tl.col0 + tw, g.C); ++c) {
         if (c < g.row_cstart[r]) continue;

@@ -111,81 +111,81 @@ int default_variant() {  // only the v1 kernel family (variant 0) remains
   return 0;
 }
 
-// Staircase tile list of GEMM g for a tm x tn CTA tile.  Returns the number
-// of tiles.
-// etn > 0: a band's last tile is a tm x etn "edge" tile when at most etn
-// columns remain (listed in etiles / ekmin / ekmax; *nedge counts them)
-static int64_t build_tiles(const Plan &p, const Gemm &g, int tm, int tn, std::vector<Tile> *tiles,
-                           std::vector<int32_t> *kmin_out, std::vector<int32_t> *kmax_out, int etn = 0,
-                           std::vector<Tile> *etiles = nullptr, std::vector<int32_t> *ekmin = nullptr,
-                           std::vector<int32_t> *ekmax = nullptr, int64_t *nedge = nullptr) {
-  if (tiles) tiles->clear();
-  if (kmin_out) kmin_out->clear();
-  if (kmax_out) kmax_out->clear();
-  if (etiles) etiles->clear();
-  if (ekmin) ekmin->clear();
-  if (ekmax) ekmax->clear();
-  if (nedge) *nedge = 0;
-  int64_t ntiles = 0;
+// Staircase tile lists of GEMM g for a tm x tn CTA tile.  Every band of tm
+// rows is covered from its first row's suffix start by tiles of width
+// w[0] = tn; its tail by the narrower widths w[1] = tn/2, w[2] = tn/4 where
+// those are compiled shapes (0 = not available): a tail of R < tn columns
+// takes one tn tile if R > w[1] + w[2], else w[1] (then w[2]) or w[2] alone
+// -- at most w[2] - 1 (or w[1] - 1) masked columns instead of up to tn - 1.
+// out (3 classes, or null) receives each class's tiles and key ranges;
+// returns the modeled cost: sum over tiles of tm x w x (1 + 10 (1/w + 1/tm))
+// (a Khatri-Rao product ~ 10 FMA-equivalents: its X loads, DMULs on the
+// shared FP64 pipe, the smem store; fitted to profiles/r01_tile_shapes.log).
+struct TileLists {
+  std::vector<Tile> t;
+  std::vector<int32_t> kmin, kmax;
+};
+static double build_tiles(const Plan &p, const Gemm &g, int tm, const int (&w)[3], TileLists *out) {
+  (void)p;
+  if (out)
+    for (int i = 0; i < 3; ++i) out[i] = TileLists();
+  double cost = 0.0;
   for (int64_t r0 = 0; r0 < g.R; r0 += tm) {
     const int64_t r1 = std::min<int64_t>(r0 + tm, g.R);
-    for (int64_t c0 = g.row_cstart[r0]; c0 < g.C; c0 += tn) {
-      const bool edge = etn > 0 && g.C - c0 <= etn;
-      const int64_t c1 = std::min<int64_t>(c0 + (edge ? etn : tn), g.C);
-      int32_t cache_lo = 0, cache_hi = 0;
-      int64_t kmin = INT64_MAX, kmax = -1;
-      // a tile of this band holds row r0 (its columns start at or after
-      // r0's suffix start, the band's smallest); the key range is only
-      // needed for the tile list itself
-      if (!kmin_out && !kmax_out) {
-        if (edge && nedge) ++*nedge;
-        else ++ntiles;
-        continue;
+    int64_t c0 = g.row_cstart[r0];
+    while (c0 < g.C) {
+      const int64_t rem = g.C - c0;
+      int cls = 0;
+      if (rem < w[0]) {
+        if (w[1] && rem <= w[1]) cls = (w[2] && rem <= w[2]) ? 2 : 1;
+        else if (w[1] && w[2] && rem <= w[1] + w[2]) cls = 1;
       }
-      for (int64_t rr = r0; rr < r1; ++rr) {
-        int64_t cs = std::max<int64_t>(c0, g.row_cstart[rr]);
-        if (cs >= c1) continue;
-        // column ranks are not monotone in a symmetric plan's column order
-        int32_t rlo = INT32_MAX, rhi = -1;
-        if (rr == r0 || g.row_cstart[rr] != g.row_cstart[rr - 1]) {
-          for (int64_t c = cs; c < c1; ++c) {
-            rlo = std::min(rlo, g.col_rank[c]);
-            rhi = std::max(rhi, g.col_rank[c]);
+      const int tw = w[cls];
+      const int64_t c1 = std::min<int64_t>(c0 + tw, g.C);
+      cost += (double)tm * tw * (1.0 + 10.0 * (1.0 / tw + 1.0 / tm));
+      if (out) {
+        // key range of the tile (column ranks are not monotone in a
+        // symmetric plan's column order); rows of equal start share it
+        int64_t kmin = INT64_MAX, kmax = -1;
+        int32_t rlo = 0, rhi = -1;
+        for (int64_t rr = r0; rr < r1; ++rr) {
+          const int64_t cs = std::max<int64_t>(c0, g.row_cstart[rr]);
+          if (cs >= c1) continue;
+          if (rr == r0 || g.row_cstart[rr] != g.row_cstart[rr - 1]) {
+            rlo = INT32_MAX;
+            rhi = -1;
+            for (int64_t c = cs; c < c1; ++c) {
+              rlo = std::min(rlo, g.col_rank[c]);
+              rhi = std::max(rhi, g.col_rank[c]);
+            }
           }
-          cache_lo = rlo;
-          cache_hi = rhi;
-        } else {
-          rlo = cache_lo;
-          rhi = cache_hi;
+          kmin = std::min<int64_t>(kmin, g.row_keybase[rr] + rlo);
+          kmax = std::max<int64_t>(kmax, g.row_keybase[rr] + rhi);
         }
-        kmin = std::min<int64_t>(kmin, g.row_keybase[rr] + rlo);
-        kmax = std::max<int64_t>(kmax, g.row_keybase[rr] + rhi);
+        if (kmax >= 0) {
+          out[cls].t.push_back(Tile{(int32_t)r0, (int32_t)c0});
+          out[cls].kmin.push_back((int32_t)kmin);
+          out[cls].kmax.push_back((int32_t)kmax);
+        }
       }
-      if (kmax < 0) continue;  // below the staircase
-      if (edge) {
-        if (nedge) ++*nedge;
-        if (etiles) etiles->push_back(Tile{(int32_t)r0, (int32_t)c0});
-        if (ekmin) ekmin->push_back((int32_t)kmin);
-        if (ekmax) ekmax->push_back((int32_t)kmax);
-        continue;
-      }
-      ++ntiles;
-      if (tiles) tiles->push_back(Tile{(int32_t)r0, (int32_t)c0});
-      if (kmin_out) kmin_out->push_back((int32_t)kmin);
-      if (kmax_out) kmax_out->push_back((int32_t)kmax);
+      c0 += tw;
     }
   }
-  return ntiles;
+  return cost;
 }
 
-// Modeled cost (in useful-FMA units) of running GEMM g with a tm x tn tile:
-// tiled area x (1 + 10 * Khatri-Rao products per FMA).  The weight of a KR
-// product (~10 FMA-equivalents: its X loads, DMULs on the shared FP64 pipe,
-// the smem store) and the negligible effect of fragment-load pressure are
-// fitted to the shape sweep in profiles/r01_tile_shapes.log.
+// tile widths of a tm x tn plan: tn and the compiled narrower edge shapes
+static void tile_widths(const Plan &p, int m, int tm, int tn, int (&w)[3]) {
+  const int kc = pick_kc((int)p.n);
+  w[0] = tn;
+  w[1] = (!std::getenv("BCG_NO_EDGE_TILES") && tn / 2 >= 8 && v1_shape_supported(kc, m, tm, tn / 2)) ? tn / 2 : 0;
+  w[2] = (w[1] && tn / 4 >= 8 && v1_shape_supported(kc, m, tm, tn / 4)) ? tn / 4 : 0;
+}
+
 static double gemm_cost(const Plan &p, const Gemm &g, int tm, int tn) {
-  const int64_t ntiles = build_tiles(p, g, tm, tn, nullptr, nullptr, nullptr);
-  return (double)ntiles * tm * tn * (1.0 + 10.0 * (1.0 / tn + 1.0 / tm));
+  int w[3];
+  tile_widths(p, g.h + g.r, tm, tn, w);
+  return build_tiles(p, g, tm, w, nullptr);
 }
 
 static void choose_shape(const Plan &p, Gemm &g) {
@@ -448,14 +448,19 @@ std::string build_plan(int64_t n, int m, int b, Plan &p, int variant, bool sym) 
   p.produced = 0;
   for (Gemm &g : p.gemm) {
     choose_shape(p, g);
-    // narrow edge tiles where the band's overhang would leave half a tile
-    // masked (tm x tn/2 must be a compiled shape)
-    g.etn = 0;
-    const int half = g.tn / 2;
-    if (!std::getenv("BCG_NO_EDGE_TILES") && half >= 8 && v1_shape_supported(pick_kc((int)p.n), m, g.tm, half))
-      g.etn = half;
-    build_tiles(p, g, g.tm, g.tn, &g.tiles, &g.tile_kmin, &g.tile_kmax, g.etn, &g.etiles, &g.etile_kmin,
-                &g.etile_kmax);
+    int w[3];
+    tile_widths(p, m, g.tm, g.tn, w);
+    TileLists tl[3];
+    build_tiles(p, g, g.tm, w, tl);
+    g.tiles = std::move(tl[0].t);
+    g.tile_kmin = std::move(tl[0].kmin);
+    g.tile_kmax = std::move(tl[0].kmax);
+    for (int i = 0; i < 2; ++i) {
+      g.ew[i] = w[i + 1];
+      g.et[i] = std::move(tl[i + 1].t);
+      g.ekmin[i] = std::move(tl[i + 1].kmin);
+      g.ekmax[i] = std::move(tl[i + 1].kmax);
+    }
     p.produced += gemm_produced(g);
   }
   // symmetric plan: blocks with a repeated block index of edge > 1 hold
@@ -591,9 +596,11 @@ std::string upload_plan(Plan &p) {
     UPG(d_tiles, tiles);
     UPG(d_tile_kmin, tile_kmin);
     UPG(d_tile_kmax, tile_kmax);
-    UPG(d_etiles, etiles);
-    UPG(d_etile_kmin, etile_kmin);
-    UPG(d_etile_kmax, etile_kmax);
+    for (int i = 0; i < 2; ++i) {
+      UPG(d_et[i], et[i]);
+      UPG(d_ekmin[i], ekmin[i]);
+      UPG(d_ekmax[i], ekmax[i]);
+    }
 #undef UPG
   }
 #define UP(d, s) if (e == cudaSuccess) e = up(&p.d, p.s)
@@ -621,7 +628,7 @@ void free_plan(Plan &p) {
   for (Gemm &g : p.gemm) {
     void *gp[] = {g.d_rowcols, g.d_colcols, g.d_row_keybase, g.d_row_olin, g.d_row_cstart,
                   g.d_col_rank, g.d_col_olin, g.d_col_size, g.d_tiles, g.d_tile_kmin, g.d_tile_kmax,
-                  g.d_etiles, g.d_etile_kmin, g.d_etile_kmax};
+                  g.d_et[0], g.d_ekmin[0], g.d_ekmax[0], g.d_et[1], g.d_ekmin[1], g.d_ekmax[1]};
     for (void *q : gp)
       if (q) cudaFree(q);
   }

@@ -41,19 +41,20 @@ struct Gemm {
   std::vector<int32_t> col_size;        // |R| = prod edges(R)
   std::vector<Tile> tiles;
   std::vector<int32_t> tile_kmin, tile_kmax;  // key range a tile touches
-  // edge tiles: a band's last tile when at most etn columns remain, run with
-  // a tm x etn CTA tile (etn = tn / 2; 0 = none) -- the staircase overhang
-  int etn = 0;
-  std::vector<Tile> etiles;
-  std::vector<int32_t> etile_kmin, etile_kmax;
+  // band-edge tiles: a band's tail is covered by narrower tiles of width
+  // ew[0] = tn/2 and ew[1] = tn/4 (0 = not a compiled shape) -- the staircase
+  // overhang; et[i] / ekmin[i] / ekmax[i] as tiles / tile_kmin / tile_kmax
+  int ew[2] = {0, 0};
+  std::vector<Tile> et[2];
+  std::vector<int32_t> ekmin[2], ekmax[2];
   // device copies
   int16_t *d_rowcols = nullptr, *d_colcols = nullptr;
   int32_t *d_row_keybase = nullptr, *d_row_olin = nullptr, *d_row_cstart = nullptr;
   int32_t *d_col_rank = nullptr, *d_col_olin = nullptr, *d_col_size = nullptr;
   Tile *d_tiles = nullptr;
   int32_t *d_tile_kmin = nullptr, *d_tile_kmax = nullptr;
-  Tile *d_etiles = nullptr;
-  int32_t *d_etile_kmin = nullptr, *d_etile_kmax = nullptr;
+  Tile *d_et[2] = {nullptr, nullptr};
+  int32_t *d_ekmin[2] = {nullptr, nullptr}, *d_ekmax[2] = {nullptr, nullptr};
 };
 
 struct Plan {
