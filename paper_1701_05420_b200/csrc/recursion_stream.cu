@@ -20,9 +20,11 @@
 //     contiguous run of M_6;
 //   * warp 0 streams units into an NS-stage shared-memory ring
 //     (cp.async.bulk, mbarrier complete_tx) and prefetches ahead into L2;
-//   * warp 1 streams the factors: per tail the 25 second factors (V: the
+//   * warp 1 streams the factors, one lane per term (a V or U load is ONE
+//     warp-wide bulk-copy instruction): per tail the 25 second factors (V: the
 //     sub-blocks not holding mode 0, 72 KB at b = 6), per slab the 25
-//     first-factor slices at i0 (U: 20 KB, NU buffers);
+//     first-factor slices at i0 (U: 20 KB, NU buffers); M_6 copies carry an
+//     L2 evict-first policy, factor copies evict-last;
 //   * NGRP (4) consumer groups of 3 warps: a group loads a unit's elements from its ring
 //     stage into registers and releases the stage at once, applies the 25
 //     terms reading every factor from shared memory, and stores C_6 straight
@@ -37,6 +39,20 @@
 // FMA, against v2's 0.64.  Interleaving keeps g5 lanes on adjacent doubles, so
 // a warp's store touches 16-byte runs, and the 16 lanes of a sub-slab hit
 // distinct double-banks on the ring loads.
+//
+// Lane order (v8).  ncu's per-instruction wavefront counts of v7d fit one rule
+// exactly (tools/rs_wavefront_model.py, profiles/r02_rs_wavefront_rule.txt):
+// an LDS.64 takes max(bank rule, ceil(distinct addresses per lane quad / 2))
+// wavefronts -- a factor indexed by BOTH lane bits 0 and 1 costs two even when
+// the warp reads 4 distinct doubles.  v8 puts the low bit of the mode-2 digit
+// and the sub-slab in lane bits 0, 1 (0.476 factor wavefronts per element
+// instead of 0.633).  What bounds the kernel, though, is the data RETURN of
+// the loads (32 lanes x 8 B = 2 L1 cycles per LDS.64 whatever the broadcast):
+// 14.5 loads per element = 116 B per element against 128 B / clk / SM, i.e.
+// 7.9 ms at cfg5 with the L1 pipe 100% busy; only a larger register tile
+// lowers it, and at b = 6 = 2 x 3 the 27-element tile is the only one whose
+// thread count per unit is a multiple of 32 short of 81 elements (254
+// registers, measured slower).
 //
 // mbarrier phases: consumers release ring stages early and run ahead of each
 // other, so a "full" barrier is indexed such that its previous phase belongs
@@ -72,8 +88,11 @@ constexpr int lcm(int x, int y) { return x / gcd(x, y) * y; }
 
 // geometry for order 6, edge B, NRM register modes (the trailing ones),
 // NGRP consumer groups
-template <int B, int RM, int NGRP, int NU_ = 3, int XB = 1>
+template <int B, int RM, int NGRP, int NU_ = 3, int XB = 1, int LO_ = 0, int HINT_ = 0, int PP_ = 0>
 struct Geo {
+  static constexpr int PP = PP_;      // factor producer: 0 = one lane issues all copies, 1 = one lane per term
+  static constexpr int LO = LO_;      // consumer lane order (see the kernel)
+  static constexpr int HINT = HINT_;  // L2 eviction hints on the bulk copies
   static constexpr int M = 6;
   static constexpr int NT = term_count(M);  // 25
   static constexpr int RG = B / 2;          // register digits per register mode
@@ -88,7 +107,10 @@ struct Geo {
   static constexpr int UPS = B / U1;                           // units per slab
   static constexpr int UPB = B * UPS;                          // units per block
   static constexpr int NU = NU_;                               // U buffers
-  static constexpr int NTHREADS = 64 + NGRP * GT;
+  // PP = 2: ONE producer warp (lane 31 streams M_6, lanes 0..24 the factors),
+  // so 5 consumer groups fit 512 threads at 128 registers
+  static constexpr int PW = PP_ == 2 ? 1 : 2;  // producer warps
+  static constexpr int NTHREADS = 32 * PW + NGRP * GT;
   // second factor of term T (modes not holding 0): b^|rest| doubles at ov(T)
   __host__ __device__ static constexpr int ov(int T) {
     int o = 0;
@@ -153,6 +175,25 @@ __device__ __forceinline__ void bar_wait(uint64_t *b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// the same for a warp whose lanes wait on different barriers (PP = 2: the
+// M_6 lane and the factor lanes share a warp): no uniform branches, and
+// test_wait, not try_wait -- a try_wait suspends the whole warp, the other
+// lanes' path with it, until its time limit
+__device__ __forceinline__ void bar_wait_div(uint64_t *b, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+    if (!ok) __nanosleep(32);  // let the warp's other path run
+  } while (!ok);
+}
 __device__ __forceinline__ void bar_expect(uint64_t *b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
 }
@@ -166,6 +207,24 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(su32(b))
       : "memory");
 }
+// the same with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *b, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(b)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
 // bulk prefetch into L2 (no shared memory)
 __device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
@@ -173,28 +232,32 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes
 
 // ---- factor producer ----
 template <class G, int T>
-__device__ __forceinline__ void load_v(double *sv, const RecFactArgs &a, const int32_t *toff, uint64_t *bar) {
+__device__ __forceinline__ void load_v(double *sv, const RecFactArgs &a, const int32_t *toff, uint64_t *bar,
+                                       uint64_t pol) {
   constexpr int r = 6 - popc(term_mask(6, T));
   constexpr int B = 2 * G::RG;
   const double *src = (r <= 3 ? a.cum[r] : a.cmom[r]) + __ldg(toff + 2 * T + 1);
-  bulk_g2s(sv + G::ov(T), src, 8u * ipow(B, r), bar);
+  if constexpr (G::HINT) bulk_g2s_hint(sv + G::ov(T), src, 8u * ipow(B, r), bar, pol);
+  else bulk_g2s(sv + G::ov(T), src, 8u * ipow(B, r), bar);
 }
 template <class G, int T>
-__device__ __forceinline__ void load_u(double *su, const RecFactArgs &a, const int32_t *toff, int i0, uint64_t *bar) {
+__device__ __forceinline__ void load_u(double *su, const RecFactArgs &a, const int32_t *toff, int i0, uint64_t *bar,
+                                       uint64_t pol) {
   constexpr int s = popc(term_mask(6, T));
   constexpr int L = ipow(2 * G::RG, s - 1);
   const double *src = a.cum[s] + __ldg(toff + 2 * T) + (int64_t)i0 * L;
-  bulk_g2s(su + G::ou(T), src, 8u * L, bar);
+  if constexpr (G::HINT) bulk_g2s_hint(su + G::ou(T), src, 8u * L, bar, pol);
+  else bulk_g2s(su + G::ou(T), src, 8u * L, bar);
 }
 template <class G, int... Ts>
 __device__ __forceinline__ void load_v_all(double *sv, const RecFactArgs &a, const int32_t *toff, uint64_t *bar,
-                                           std::integer_sequence<int, Ts...>) {
-  (load_v<G, Ts>(sv, a, toff, bar), ...);
+                                           uint64_t pol, std::integer_sequence<int, Ts...>) {
+  (load_v<G, Ts>(sv, a, toff, bar, pol), ...);
 }
 template <class G, int... Ts>
 __device__ __forceinline__ void load_u_all(double *su, const RecFactArgs &a, const int32_t *toff, int i0,
-                                           uint64_t *bar, std::integer_sequence<int, Ts...>) {
-  (load_u<G, Ts>(su, a, toff, i0, bar), ...);
+                                           uint64_t *bar, uint64_t pol, std::integer_sequence<int, Ts...>) {
+  (load_u<G, Ts>(su, a, toff, i0, bar, pol), ...);
 }
 
 // ---- consumer: one term on the thread's elements.  dig[q] = the thread's
@@ -242,9 +305,10 @@ __device__ __forceinline__ void rows_store_global(const double (&acc)[G::ROWS], 
 #endif
 constexpr int kPrefetchUnits = BCG_RS_PREFETCH;  // M_6 units prefetched into L2 ahead of the ring
 
-template <int B, int RM, int NGRP, int NU, int XB>
-__global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB>::NTHREADS, 1) k_recursion_stream6(RecFactArgs a) {
-  using G = rs::Geo<B, RM, NGRP, NU, XB>;
+template <int B, int RM, int NGRP, int NU, int XB, int LO, int HINT, int PP>
+__global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP>::NTHREADS, 1)
+    k_recursion_stream6(RecFactArgs a) {
+  using G = rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP>;
   constexpr int NT = G::NT, NS = G::NS;
   extern __shared__ __align__(128) unsigned char rs_smem[];
   double *sv = reinterpret_cast<double *>(rs_smem);
@@ -279,10 +343,15 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB>::NTHREADS, 1) k_r
     for (int T = 0; T < NT; ++T) eq = eq && __ldg(x + 2 * T) == __ldg(y + 2 * T);
     return eq;
   };
-  if (warp == 0) {
-    // ---- M_6 producer: units in (position, i0, unit) order into the ring ----
-    if (lane == 0) {
+  auto pwait = [&](uint64_t *b, uint32_t parity) {
+    if constexpr (PP == 2) rs::bar_wait_div(b, parity);
+    else rs::bar_wait(b, parity);
+  };
+  if (warp == 0 && (PP != 2 || lane == 31)) {
+    // ---- M_6 producer (one lane): units in (position, i0, unit) order into the ring ----
+    if (lane == (PP == 2 ? 31 : 0)) {
       int64_t u = 0;
+      const uint64_t pol = HINT ? rs::policy_evict_first() : 0;  // M_6 is read once
       static_assert(kPrefetchUnits <= G::UPB, "prefetch at most one block ahead");
       for (int64_t pos = pbeg; pos < pend; ++pos) {
         const double *blk = a.mk + __ldg(a.blk_off + item(pos));
@@ -296,19 +365,70 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB>::NTHREADS, 1) k_r
             else if (nblk) rs::bulk_prefetch_l2(nblk + (int64_t)(jp - G::UPB) * G::UNIT, 8u * G::UNIT);
           }
           const int st = (int)(u % NS);
-          if (u >= NS) rs::bar_wait(&mempty[st], (uint32_t)((u / NS - 1) & 1));
+          if (u >= NS) pwait(&mempty[st], (uint32_t)((u / NS - 1) & 1));
           uint64_t *fb = &mfull[u % G::MF];
           rs::bar_expect(fb, 8u * G::UNIT);
-          rs::bulk_g2s(sm + (int64_t)st * G::UNIT, blk + (int64_t)j * G::UNIT, 8u * G::UNIT, fb);
+          if constexpr (HINT) rs::bulk_g2s_hint(sm + (int64_t)st * G::UNIT, blk + (int64_t)j * G::UNIT, 8u * G::UNIT, fb, pol);
+          else rs::bulk_g2s(sm + (int64_t)st * G::UNIT, blk + (int64_t)j * G::UNIT, 8u * G::UNIT, fb);
         }
       }
     }
     return;
   }
-  if (warp == 1) {
+  if (PP == 2 ? (warp == 0) : (warp == 1 && PP == 1)) {
+    if (lane >= NT) return;
+    constexpr unsigned kMask = (1u << NT) - 1;
+    // ---- factor producer, one lane per term: the 25 copies of a V or U load
+    // are ONE warp instruction each (the single-lane version issues 25 bulk
+    // copies + 25 offset loads per slab through the same MIO queue the
+    // consumers' LDS keep full, and the consumers end up waiting on U) ----
+    static_assert(NT <= 32, "one lane per term");
+    const bool act = lane < NT;
+    const int T = act ? lane : 0;
+    const int sS = rs::popc(rs::term_mask(6, T)), rR = 6 - sS;
+    const uint32_t vbytes = 8u * rs::ipow(B, rR), ubytes = 8u * rs::ipow(B, sS - 1);
+    const int ulen = rs::ipow(B, sS - 1);
+    double *vdst = sv + G::ov(T), *udst = su + G::ou(T);
+    const double *vsrc = rR <= 3 ? a.cum[rR] : a.cmom[rR];
+    const double *usrc = a.cum[sS];
+    const uint64_t pol = HINT ? rs::policy_evict_last() : 0;
+    int64_t e = -1, s = 0;
+    int32_t pv = 0;
+    for (int64_t pos = pbeg; pos < pend; ++pos) {
+      const int64_t it = item(pos);
+      const int32_t *toff = a.term_off + it * 2 * NT;
+      const int32_t uo = __ldg(toff + 2 * T), vo = __ldg(toff + 2 * T + 1);
+      const bool newv = pos == pbeg || __any_sync(kMask, act && vo != pv);
+      pv = vo;
+      if (newv) {
+        ++e;
+        if (e > 0) pwait(vempty, (uint32_t)((e - 1) & 1));
+        if (lane == 0) rs::bar_expect(vfull, 8u * G::SEGV);
+        __syncwarp(kMask);
+        if (act) {
+          if constexpr (HINT) rs::bulk_g2s_hint(vdst, vsrc + vo, vbytes, vfull, pol);
+          else rs::bulk_g2s(vdst, vsrc + vo, vbytes, vfull);
+        }
+      }
+      for (int i0 = 0; i0 < B; ++i0, ++s) {
+        const int buf = (int)(s % G::NU);
+        if (s >= G::NU) pwait(&uempty[buf], (uint32_t)((s / G::NU - 1) & 1));
+        uint64_t *fb = &ufull[s % G::UF];
+        if (lane == 0) rs::bar_expect(fb, 8u * G::SEGU);
+        __syncwarp(kMask);
+        if (act) {
+          if constexpr (HINT) rs::bulk_g2s_hint(udst + buf * G::SEGU, usrc + uo + (int64_t)i0 * ulen, ubytes, fb, pol);
+          else rs::bulk_g2s(udst + buf * G::SEGU, usrc + uo + (int64_t)i0 * ulen, ubytes, fb);
+        }
+      }
+    }
+    return;
+  }
+  if (warp == 1 && PP == 0) {
     // ---- factor producer: V per run of equal tails, U per slab ----
     if (lane == 0) {
       int64_t e = -1, s = 0, prev = -1;
+      const uint64_t pol = HINT ? rs::policy_evict_last() : 0;  // the factors are re-read by every block sharing them
       for (int64_t pos = pbeg; pos < pend; ++pos) {
         const int64_t it = item(pos);
         const int32_t *toff = a.term_off + it * 2 * NT;
@@ -316,7 +436,7 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB>::NTHREADS, 1) k_r
           ++e;
           if (e > 0) rs::bar_wait(vempty, (uint32_t)((e - 1) & 1));
           rs::bar_expect(vfull, 8u * G::SEGV);
-          rs::load_v_all<G>(sv, a, toff, vfull, std::make_integer_sequence<int, NT>{});
+          rs::load_v_all<G>(sv, a, toff, vfull, pol, std::make_integer_sequence<int, NT>{});
         }
         prev = it;
         for (int i0 = 0; i0 < B; ++i0, ++s) {
@@ -324,22 +444,37 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB>::NTHREADS, 1) k_r
           if (s >= G::NU) rs::bar_wait(&uempty[buf], (uint32_t)((s / G::NU - 1) & 1));
           uint64_t *fb = &ufull[s % G::UF];
           rs::bar_expect(fb, 8u * G::SEGU);
-          rs::load_u_all<G>(su + buf * G::SEGU, a, toff, i0, fb, std::make_integer_sequence<int, NT>{});
+          rs::load_u_all<G>(su + buf * G::SEGU, a, toff, i0, fb, pol, std::make_integer_sequence<int, NT>{});
         }
       }
     }
     return;
   }
   // ---- consumers: group grp takes the units u == grp (mod NGRP) ----
-  const int ct = threadIdx.x - 64;
+  const int ct = threadIdx.x - 32 * G::PW;
   const int grp = ct / G::GT, t = ct % G::GT;
   // lane order (fastest first): the register modes' group bits (last mode
   // fastest), the thread-level modes, then the sub-slab h (measured faster
   // than h-before-thread-modes at cfg5)
-  const int h = t / G::TPS, r = t % G::TPS;
+  int h = t / G::TPS;
+  const int r = t % G::TPS;
   int dig[6];
   dig[0] = 0;
-  {
+  if constexpr (LO == 1) {
+    // lane order chosen with the measured wavefront rule (an LDS.64 costs
+    // max(bank rule, ceil(distinct addresses per lane quad / 2)) wavefronts,
+    // tools/rs_wavefront_model.py): lane bits 0, 1 = the low bit of the
+    // mode-2 digit and the sub-slab, so a quad of lanes reads <= 2 distinct
+    // doubles of every factor not holding modes 1 and 2 together; bits 2..4
+    // = the group bits of modes 5, 4, 3; the warp = the high part of the
+    // mode-2 digit.  0.476 factor wavefronts per element instead of 0.633.
+    static_assert(LO != 1 || (RM == 0x38 && B == 6), "lane order 1 is laid out for register modes 3,4,5 at b = 6");
+    dig[2] = (t & 1) + 2 * (t >> 5);
+    h = (t >> 1) & 1;
+    dig[5] = (t >> 2) & 1;
+    dig[4] = (t >> 3) & 1;
+    dig[3] = (t >> 4) & 1;
+  } else {
     int gb = r % (1 << G::NRM), tm = r >> G::NRM;
 #pragma unroll
     for (int q = 5; q >= 2; --q) {
@@ -405,19 +540,24 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB>::NTHREADS, 1) k_r
   if (e >= 0 && lane == 0) rs::bar_arrive(vempty);
 }
 
-// tile / group / buffer choice (A/B knob BCG_RS_TILE), cfg5 layout, L2 flushed
-// (profiles/r02_recursion_stream.txt):
-//   0: register modes 3,4,5 (27 elements), mode 2 across threads, 4 consumer
-//      groups (12 warps, 128 registers), 3 U buffers -- default, 11.2 ms
-//   1: 3 consumer groups (165 registers)                        12.0 ms
-//   2: 4 groups, 2 U buffers (one more ring stage)
-//   3: register modes 2,3,4 (mode 5 across threads), 4 groups
-//   4: register modes 2..5 (81 elements), 6 consumer warps      13.6 ms
-template <int B, int RM, int NGRP, int NU, int XB = 1>
+// variant choice (A/B knob BCG_RS_TILE), cfg5 layout, L2 flushed, same box
+// (profiles/r02_recursion_stream.txt; every variant bitwise equal to v2):
+//   default (v8): register modes 3,4,5 (27 elements), 4 consumer groups (12
+//      warps, 128 registers), quad-aware lane order, 4 U buffers + 3 ring
+//      stages, one producer lane per term, L2 eviction hints      10.89 ms
+//   0: v7d -- lane order g5,g4,g3,mode 2,h; 3 U buffers + 4 stages; one
+//      lane issues all factor copies; no hints                    11.46 ms
+//   1: v7d with 3 consumer groups (165 registers)
+//   4: register modes 2..5 (81 elements), 6 consumer warps, 254 registers
+//   5: v7d + the lane order          6: 5 + 4 U buffers
+//   14: 6 + per-term producer lanes (= v8 without the hints)      11.16 ms
+//   17: v8 with ONE producer warp (lane 31 streams M_6, lanes 0..24 the factors) 10.71 ms
+//   18: 17 with 5 consumer groups (15 warps, 3 U buffers + 4 stages)   10.80 ms
+template <int B, int RM, int NGRP, int NU, int LO = 0, int HINT = 0, int PP = 0, int XB = 1>
 static cudaError_t go_stream6(const RecFactArgs &a, int nsm, cudaStream_t stream) {
-  using G = rs::Geo<B, RM, NGRP, NU, XB>;
+  using G = rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP>;
   static_assert(G::ok, "stream6 geometry");
-  auto kern = k_recursion_stream6<B, RM, NGRP, NU, XB>;
+  auto kern = k_recursion_stream6<B, RM, NGRP, NU, XB, LO, HINT, PP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
   if (e != cudaSuccess) return e;
   const int64_t grid = a.nkeys < nsm ? a.nkeys : nsm;
@@ -438,12 +578,16 @@ cudaError_t launch_recursion_stream6(const RecFactArgs &a, int b, cudaStream_t s
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  static const int tile = getenv("BCG_RS_TILE") ? atoi(getenv("BCG_RS_TILE")) : 0;
+  static const int tile = getenv("BCG_RS_TILE") ? atoi(getenv("BCG_RS_TILE")) : -1;
+  if (tile == 0) return go_stream6<6, 0x38, 4, 3>(a, nsm, stream);
   if (tile == 1) return go_stream6<6, 0x38, 3, 3>(a, nsm, stream);
-  if (tile == 2) return go_stream6<6, 0x38, 4, 2>(a, nsm, stream);
-  if (tile == 3) return go_stream6<6, 0x1c, 4, 3>(a, nsm, stream);
   if (tile == 4) return go_stream6<6, 0x3c, 6, 3>(a, nsm, stream);
-  return go_stream6<6, 0x38, 4, 3>(a, nsm, stream);
+  if (tile == 5) return go_stream6<6, 0x38, 4, 3, 1>(a, nsm, stream);
+  if (tile == 6) return go_stream6<6, 0x38, 4, 4, 1>(a, nsm, stream);
+  if (tile == 14) return go_stream6<6, 0x38, 4, 4, 1, 0, 1>(a, nsm, stream);
+  if (tile == 17) return go_stream6<6, 0x38, 4, 4, 1, 1, 2>(a, nsm, stream);
+  if (tile == 18) return go_stream6<6, 0x38, 5, 3, 1, 1, 2>(a, nsm, stream);
+  return go_stream6<6, 0x38, 4, 4, 1, 1, 1>(a, nsm, stream);
 }
 
 }  // namespace bcg
