@@ -88,8 +88,9 @@ constexpr int lcm(int x, int y) { return x / gcd(x, y) * y; }
 
 // geometry for order 6, edge B, NRM register modes (the trailing ones),
 // NGRP consumer groups
-template <int B, int RM, int NGRP, int NU_ = 3, int XB = 1, int LO_ = 0, int HINT_ = 0, int PP_ = 0>
+template <int B, int RM, int NGRP, int NU_ = 3, int XB = 1, int LO_ = 0, int HINT_ = 0, int PP_ = 0, int TM_ = 0>
 struct Geo {
+  static constexpr int TM = TM_;      // 1: tail-constant second factors cached per lane in tensor memory
   static constexpr int PP = PP_;      // factor producer: 0 = one lane issues all copies, 1 = one lane per term
   static constexpr int LO = LO_;      // consumer lane order (see the kernel)
   static constexpr int HINT = HINT_;  // L2 eviction hints on the bulk copies
@@ -132,7 +133,7 @@ struct Geo {
   static constexpr int NS = (227 * 1024 - 8 * (SEGV + NU * SEGU) - 512) / (8 * UNIT);  // ring stages
   static constexpr int MF = lcm(NS, NGRP) * XB;
   static constexpr int UF = lcm(NU, SLAB_PERIOD) * XB;
-  static constexpr int NBAR = MF + NS + UF + NU + 2;
+  static constexpr int NBAR = MF + NS + UF + NU + 2 + 2;  // + done barrier, TMEM base slot
   static constexpr size_t SMEM = 8 * (size_t)(SEGV + NU * SEGU + NS * UNIT) + 8 * NBAR;
   // every bulk copy is a multiple of 16 bytes at a 16-byte aligned offset
   static constexpr bool ok = B % 2 == 0 && B >= 4 && GT % 32 == 0 && NS >= 2 && SEGU % 2 == 0 &&
@@ -260,13 +261,139 @@ __device__ __forceinline__ void load_u_all(double *su, const RecFactArgs &a, con
   (load_u<G, Ts>(su, a, toff, i0, bar, pol), ...);
 }
 
+// ---- tensor memory as a per-lane operand cache (TM = 1) ----
+// What bounds the consumers is the L1 return path (8 B x 32 lanes per
+// LDS.64).  Five terms' second factors hold no mode 1, so a thread reads the
+// same 81 doubles of V in every unit of a tail: they are copied once per tail
+// into the warp's tensor-memory lanes (tcgen05.st, 162 columns of a lane per
+// warp; 3 consumer warps share a 32-lane quadrant, 486 of 512 columns) and
+// read back with tcgen05.ld -- a datapath of its own -- instead of 81 of the
+// unit's 391 shared-memory loads.
+__host__ __device__ constexpr bool tm_term(int T) { return T == 0 || T == 2 || T == 4 || T == 6 || T == 8; }
+template <int RM>
+__host__ __device__ constexpr int tm_vcount(int T) {
+  return ipow(3, popc((63 & ~term_mask(6, T)) & RM));
+}
+template <int RM>
+__host__ __device__ constexpr int tm_col(int T) {  // first column (32-bit) of term T's values
+  int c = 0;
+  for (int t = 0; t < T; ++t)
+    if (tm_term(t)) c += 2 * tm_vcount<RM>(t);
+  return c;
+}
+template <int RM>
+__host__ __device__ constexpr int tm_cols() { return tm_col<RM>(25); }
+// factor offset of the J-th distinct register-digit combination of the modes
+// in R (mode 5 fastest), and the combination a tile row uses
+template <int R, int B, int RM, int J>
+struct VOffJ {
+  static constexpr int calc() {
+    int off = 0, j = J;
+    for (int q = 5; q >= 2; --q) {
+      if (!(RM & (1 << q)) || !(R & (1 << q))) continue;
+      const int d = j % (B / 2);
+      j /= B / 2;
+      off += 2 * d * stride_in(R, q, B);
+    }
+    return off;
+  }
+  static constexpr int value = calc();
+};
+template <int R, int B, int RM, int ROW>
+struct VJ {
+  static constexpr int calc() {
+    int j = 0, mul = 1, r = ROW;
+    for (int q = 5; q >= 2; --q) {
+      if (!(RM & (1 << q))) continue;
+      const int d = r % (B / 2);
+      r /= B / 2;
+      if (R & (1 << q)) {
+        j += d * mul;
+        mul *= B / 2;
+      }
+    }
+    return j;
+  }
+  static constexpr int value = calc();
+};
+__device__ __forceinline__ void tm_st1(uint32_t taddr, double v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(taddr), "r"(__double2loint(v)),
+               "r"(__double2hiint(v))
+               : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+// 9 doubles (18 columns) of the lane; the wait is part of the statement so no
+// use of the registers can be scheduled before it
+__device__ __forceinline__ void tm_ld9(uint32_t taddr, double (&v)[9]) {
+  uint32_t r[18];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%18];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x2.b32 {%16, %17}, [%19];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17])
+      : "r"(taddr), "r"(taddr + 16)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 9; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+}
+// copy term T's values of this thread (o2 = its offset in the factor) into its lane
+template <class G, int B, int RM, int T, int... Js>
+__device__ __forceinline__ void tm_fill_term(uint32_t tbase, const double *sv, const int (&dig)[6],
+                                             std::integer_sequence<int, Js...>) {
+  constexpr int R = 63 & ~term_mask(6, T);
+  int o2 = 0;
+#pragma unroll
+  for (int q = 2; q < 6; ++q)
+    if (R & (1 << q)) o2 += dig[q] * stride_in(R, q, B);
+  const double *f2 = sv + std::integral_constant<int, G::ov(T)>::value + o2;
+  (tm_st1(tbase + tm_col<RM>(T) + 2 * Js, f2[VOffJ<R, B, RM, Js>::value]), ...);
+}
+template <class G, int B, int RM, int... Ts>
+__device__ __forceinline__ void tm_fill(uint32_t tbase, const double *sv, const int (&dig)[6],
+                                        std::integer_sequence<int, Ts...>) {
+  ((tm_term(Ts) ? tm_fill_term<G, B, RM, Ts>(tbase, sv, dig, std::make_integer_sequence<int, tm_vcount<RM>(Ts)>{})
+                : (void)0),
+   ...);
+  tm_wait_st();
+}
+// rows [9 C, 9 C + 9) of a term whose 27 values are the tile rows themselves
+template <class G, int B, int RM, int S, int C, int... Is>
+__device__ __forceinline__ void tm_rows27(double (&acc)[G::ROWS], const double *f1, uint32_t tcol,
+                                          std::integer_sequence<int, Is...>) {
+  double v[9];
+  tm_ld9(tcol + 18 * C, v);
+  ((acc[9 * C + Is] = fma(-f1[RowOff<S, B, RM, 9 * C + Is>::value], v[Is], acc[9 * C + Is])), ...);
+}
+
 // ---- consumer: one term on the thread's elements.  dig[q] = the thread's
 // index of mode q (modes 1 .. Q0-1) or its group bit (register modes) ----
 template <class G, int B, int RM, int T, int... Rs>
 __device__ __forceinline__ void term(double (&acc)[G::ROWS], const double *su, const double *sv, const int (&dig)[6],
-                                     std::integer_sequence<int, Rs...>) {
+                                     uint32_t tbase, std::integer_sequence<int, Rs...>) {
   constexpr int S = term_mask(6, T);
   constexpr int R = 63 & ~S;
+  if constexpr (G::TM && tm_term(T)) {
+    // second factor from the lane's tensor-memory copy
+    int o1 = 0;
+#pragma unroll
+    for (int q = 1; q < 6; ++q)
+      if (S & (1 << q)) o1 += dig[q] * stride_in(S, q, B);
+    const double *f1 = su + std::integral_constant<int, G::ou(T)>::value + o1;
+    const uint32_t tcol = tbase + tm_col<RM>(T);
+    if constexpr (tm_vcount<RM>(T) == 9) {
+      double v[9];
+      tm_ld9(tcol, v);
+      ((acc[Rs] = fma(-f1[RowOff<S, B, RM, Rs>::value], v[VJ<R, B, RM, Rs>::value], acc[Rs])), ...);
+    } else {
+      static_assert(tm_vcount<RM>(T) == 27 && G::ROWS == 27, "27-value terms index the tile rows");
+      tm_rows27<G, B, RM, S, 0>(acc, f1, tcol, std::make_integer_sequence<int, 9>{});
+      tm_rows27<G, B, RM, S, 1>(acc, f1, tcol, std::make_integer_sequence<int, 9>{});
+      tm_rows27<G, B, RM, S, 2>(acc, f1, tcol, std::make_integer_sequence<int, 9>{});
+    }
+    return;
+  }
   int o1 = 0, o2 = 0;
 #pragma unroll
   for (int q = 1; q < 6; ++q) {
@@ -281,8 +408,8 @@ __device__ __forceinline__ void term(double (&acc)[G::ROWS], const double *su, c
 }
 template <class G, int B, int RM, int... Ts>
 __device__ __forceinline__ void terms(double (&acc)[G::ROWS], const double *su, const double *sv, const int (&dig)[6],
-                                      std::integer_sequence<int, Ts...>) {
-  (term<G, B, RM, Ts>(acc, su, sv, dig, std::make_integer_sequence<int, G::ROWS>{}), ...);
+                                      uint32_t tbase, std::integer_sequence<int, Ts...>) {
+  (term<G, B, RM, Ts>(acc, su, sv, dig, tbase, std::make_integer_sequence<int, G::ROWS>{}), ...);
 }
 // modes 2..5 of a sub-slab, row-major
 template <class G, int B, int RM, int... Rs>
@@ -305,10 +432,10 @@ __device__ __forceinline__ void rows_store_global(const double (&acc)[G::ROWS], 
 #endif
 constexpr int kPrefetchUnits = BCG_RS_PREFETCH;  // M_6 units prefetched into L2 ahead of the ring
 
-template <int B, int RM, int NGRP, int NU, int XB, int LO, int HINT, int PP>
-__global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP>::NTHREADS, 1)
+template <int B, int RM, int NGRP, int NU, int XB, int LO, int HINT, int PP, int TM>
+__global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP, TM>::NTHREADS, 1)
     k_recursion_stream6(RecFactArgs a) {
-  using G = rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP>;
+  using G = rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP, TM>;
   constexpr int NT = G::NT, NS = G::NS;
   extern __shared__ __align__(128) unsigned char rs_smem[];
   double *sv = reinterpret_cast<double *>(rs_smem);
@@ -318,6 +445,8 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP>::NT
   uint64_t *mfull = bars, *mempty = bars + G::MF;
   uint64_t *ufull = mempty + NS, *uempty = ufull + G::UF;
   uint64_t *vfull = uempty + G::NU, *vempty = vfull + 1;
+  uint64_t *done = vempty + 1;                                  // TM: consumers finished (before the dealloc)
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(done + 1);     // TM: allocated tensor-memory base
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -327,9 +456,26 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP>::NT
     for (int i = 0; i < G::NU; ++i) rs::bar_init(&uempty[i], G::UPS * G::GW);
     rs::bar_init(vfull, 1);
     rs::bar_init(vempty, NGRP * G::GW);
+    rs::bar_init(done, NGRP * G::GW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  if constexpr (TM) {
+    static_assert(!TM || (PP == 1 && rs::tm_cols<RM>() * ((NGRP * G::GW + 3) / 4) <= 512), "tensor-memory columns");
+    if (warp == 0) {  // the whole SM's 512 columns (one CTA per SM)
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(rs::su32(tslot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  }
   __syncthreads();
+  uint32_t tbase = 0;
+  if constexpr (TM) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    // this warp's lanes (quadrant warp % 4) and its column range among the
+    // consumer warps sharing the quadrant
+    tbase = *tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(rs::tm_cols<RM>() * ((warp - G::PW) >> 2));
+  }
 
   // this CTA's positions [pbeg, pend) of the work list
   const int64_t pbeg = a.nkeys * blockIdx.x / gridDim.x, pend = a.nkeys * (blockIdx.x + 1) / gridDim.x;
@@ -372,6 +518,12 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP>::NT
           else rs::bulk_g2s(sm + (int64_t)st * G::UNIT, blk + (int64_t)j * G::UNIT, 8u * G::UNIT, fb);
         }
       }
+    }
+    if constexpr (TM) {  // free the tensor memory once every consumer warp is done with it
+      __syncwarp();
+      rs::bar_wait(done, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(*tslot) : "memory");
     }
     return;
   }
@@ -490,7 +642,7 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP>::NT
   int ebase = 0;  // thread's first element inside its sub-slab (row-major over modes 2..5)
 #pragma unroll
   for (int q = 2; q < 6; ++q) ebase += dig[q] * rs::ipow(B, 5 - q);
-  int64_t e = -1, s = 0, prev = -1;
+  int64_t e = -1, s = 0, prev = -1, efill = -1;
   for (int64_t pos = pbeg; pos < pend; ++pos) {
     const int64_t it = item(pos);
     if (prev < 0 || !same_v(it, prev)) {
@@ -499,6 +651,12 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP>::NT
     }
     prev = it;
     rs::bar_wait(vfull, (uint32_t)(e & 1));
+    if constexpr (TM) {
+      if (e != efill) {  // new tail: this thread's tail-constant second factors -> its tensor-memory lane
+        rs::tm_fill<G, B, RM>(tbase, sv, dig, std::make_integer_sequence<int, NT>{});
+        efill = e;
+      }
+    }
     double *blk = a.mk + __ldg(a.blk_off + it);
     for (int i0 = 0; i0 < B; ++i0, ++s) {
       const int ub = (int)(s % G::NU);
@@ -529,7 +687,7 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP>::NT
 #pragma unroll
         for (int q = 1; q < 6; ++q) asm volatile("" : "+r"(dig[q]));
 #endif
-        rs::terms<G, B, RM>(acc, su + ub * G::SEGU, sv, dig, std::make_integer_sequence<int, NT>{});
+        rs::terms<G, B, RM>(acc, su + ub * G::SEGU, sv, dig, tbase, std::make_integer_sequence<int, NT>{});
         __syncwarp();
         if (lane == 0) rs::bar_arrive(&uempty[ub]);
         rs::rows_store_global<G, B, RM>(acc, blk + (int64_t)j * G::UNIT + h * G::SUB + ebase,
@@ -538,11 +696,19 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP>::NT
     }
   }
   if (e >= 0 && lane == 0) rs::bar_arrive(vempty);
+  if constexpr (TM) {
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) rs::bar_arrive(done);
+  }
 }
 
 // variant choice (A/B knob BCG_RS_TILE), cfg5 layout, L2 flushed, same box
 // (profiles/r02_recursion_stream.txt; every variant bitwise equal to v2):
-//   default (v8): register modes 3,4,5 (27 elements), 4 consumer groups (12
+//   default (v9): v8 + the 81 tail-constant second-factor values of a thread
+//      cached in its tensor-memory lane (tcgen05.st per tail, tcgen05.ld per
+//      unit instead of 81 of 391 shared-memory loads)              10.68 ms (v8 on that box: 11.21)
+//   16 (v8): register modes 3,4,5 (27 elements), 4 consumer groups (12
 //      warps, 128 registers), quad-aware lane order, 4 U buffers + 3 ring
 //      stages, one producer lane per term, L2 eviction hints      10.89 ms
 //   0: v7d -- lane order g5,g4,g3,mode 2,h; 3 U buffers + 4 stages; one
@@ -553,11 +719,11 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP>::NT
 //   14: 6 + per-term producer lanes (= v8 without the hints)      11.16 ms
 //   17: v8 with ONE producer warp (lane 31 streams M_6, lanes 0..24 the factors) 10.71 ms
 //   18: 17 with 5 consumer groups (15 warps, 3 U buffers + 4 stages)   10.80 ms
-template <int B, int RM, int NGRP, int NU, int LO = 0, int HINT = 0, int PP = 0, int XB = 1>
+template <int B, int RM, int NGRP, int NU, int LO = 0, int HINT = 0, int PP = 0, int TM = 0, int XB = 1>
 static cudaError_t go_stream6(const RecFactArgs &a, int nsm, cudaStream_t stream) {
-  using G = rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP>;
+  using G = rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP, TM>;
   static_assert(G::ok, "stream6 geometry");
-  auto kern = k_recursion_stream6<B, RM, NGRP, NU, XB, LO, HINT, PP>;
+  auto kern = k_recursion_stream6<B, RM, NGRP, NU, XB, LO, HINT, PP, TM>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
   if (e != cudaSuccess) return e;
   const int64_t grid = a.nkeys < nsm ? a.nkeys : nsm;
@@ -585,9 +751,10 @@ cudaError_t launch_recursion_stream6(const RecFactArgs &a, int b, cudaStream_t s
   if (tile == 5) return go_stream6<6, 0x38, 4, 3, 1>(a, nsm, stream);
   if (tile == 6) return go_stream6<6, 0x38, 4, 4, 1>(a, nsm, stream);
   if (tile == 14) return go_stream6<6, 0x38, 4, 4, 1, 0, 1>(a, nsm, stream);
+  if (tile == 16) return go_stream6<6, 0x38, 4, 4, 1, 1, 1>(a, nsm, stream);
   if (tile == 17) return go_stream6<6, 0x38, 4, 4, 1, 1, 2>(a, nsm, stream);
   if (tile == 18) return go_stream6<6, 0x38, 5, 3, 1, 1, 2>(a, nsm, stream);
-  return go_stream6<6, 0x38, 4, 4, 1, 1, 1>(a, nsm, stream);
+  return go_stream6<6, 0x38, 4, 4, 1, 1, 1, 1>(a, nsm, stream);
 }
 
 }  // namespace bcg

@@ -1,6 +1,6 @@
 """Shared-memory wavefront model of the streamed order-6 recursion (K3 v7/v8),
 calibrated on ncu's per-instruction "L1 Wavefronts Shared" of the v7d kernel
-(profiles/r02_rs_v7d_ncu.txt): an LDS.64 warp instruction takes
+(profiles/r02_rs_v7d_v8_v9_ncu.txt, profiles/r02_rs_wavefront_rule.txt): an LDS.64 warp instruction takes
 
     max( bank rule: most distinct 4-byte words mapped to one of the 32 banks,
          quad rule: over the 8 lane quads, ceil(distinct addresses in the quad / 2) )
@@ -133,9 +133,10 @@ def store_sectors(reg, coords):
 
 V7D = dict(reg={3: (3, 2), 4: (3, 2), 5: (3, 2)},
            coords=[(5, 2, 1), (4, 2, 1), (3, 2, 1), (2, 6, 1), (1, 2, 1)])
-# v8: lane bits 0, 1 = the group bits of modes 5 and 3 ... chosen by --search
+# v8 / v9 (chosen by --search): lane bits 0, 1 = low bit of the mode-2 digit, sub-slab;
+# bits 2..4 = group bits of modes 5, 4, 3; warp = high part of the mode-2 digit
 V8 = dict(reg={3: (3, 2), 4: (3, 2), 5: (3, 2)},
-          coords=[(5, 2, 1), (1, 2, 1), (4, 2, 1), (3, 2, 1), (2, 6, 1)])
+          coords=[(2, 2, 1), (1, 2, 1), (5, 2, 1), (4, 2, 1), (3, 2, 1), (2, 3, 2)])
 
 if __name__ == "__main__":
     for name, cfg in (("v7d", V7D), ("v8", V8)):
