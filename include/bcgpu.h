@@ -113,6 +113,10 @@ int bcg_plan_output(const bcg_plan *plan, int64_t *S_out, int64_t *produced);
  * staircase and edge positions; produced / tiled is the tile efficiency) and
  * the number of narrow band-edge tiles among them. */
 int bcg_plan_tiled(const bcg_plan *plan, int64_t *tiled, int64_t *edge_tiles);
+/* Waste breakdown of the staircase cover (introspection, tools/tile_waste.py):
+ * out[0] tiled area, out[1] valid pairs, out[2] area of empty 8 x 8 sub-tiles,
+ * out[3] area of empty 32 x 32 warp tiles, out[4] overhang past R / C. */
+int bcg_plan_waste(const bcg_plan *plan, int64_t *out);
 /* Host-only plan (tables built, nothing uploaded): layout queries work
  * without a GPU; compute calls on it fail with BCG_EINVAL. */
 int bcg_plan_create_host(int64_t n, int32_t m, int32_t b, bcg_plan **plan);

@@ -38,6 +38,7 @@ SIGNATURES = [
     ("bcg_plan_create_flags", ctypes.c_int, [_i64, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
     ("bcg_plan_output", ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     ("bcg_plan_tiled", ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    ("bcg_plan_waste", ctypes.c_int, [_vp, ctypes.POINTER(_i64)]),
     ("bcg_plan_kernel", ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                                        ctypes.POINTER(_i64)]),
     ("bcg_plan_gemm", ctypes.c_int, [_vp, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32), _vp,

@@ -265,6 +265,42 @@ int bcg_plan_tiled(const bcg_plan *plan, int64_t *tiled, int64_t *edge_tiles) {
   return BCG_OK;
 }
 
+// waste breakdown of the staircase cover (debug / tools/tile_waste.py):
+// out[0] = tiled area, out[1] = valid (row, col) pairs inside the tiles (col >=
+// the row's first valid column), out[2] = area of the 8 x 8 DMMA sub-tiles
+// with no valid pair, out[3] = area of the 32 x 32 warp tiles with no valid
+// pair, out[4] = area right of C or below R (overhang)
+int bcg_plan_waste(const bcg_plan *plan, int64_t *out) {
+  if (!plan || !out) return fail(BCG_EINVAL, "plan / out is NULL");
+  for (int i = 0; i < 5; ++i) out[i] = 0;
+  for (const bcg::Gemm &g : plan->p.gemm)
+    for (int pass = 0; pass < 3; ++pass)
+      for (const bcg::Tile &tl : pass == 0 ? g.tiles : g.et[pass - 1]) {
+        const int tw = pass == 0 ? g.tn : g.ew[pass - 1];
+        out[0] += (int64_t)g.tm * tw;
+        auto valid = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+          int64_t v = 0;
+          for (int64_t r = r0; r < std::min<int64_t>(r1, g.R); ++r) {
+            const int64_t lo = std::max<int64_t>(c0, g.row_cstart[r]), hi = std::min<int64_t>(c1, g.C);
+            if (hi > lo) v += hi - lo;
+          }
+          return v;
+        };
+        out[1] += valid(tl.row0, tl.row0 + g.tm, tl.col0, tl.col0 + tw);
+        for (int i = 0; i < g.tm; i += 8)
+          for (int j = 0; j < tw; j += 8)
+            if (!valid(tl.row0 + i, tl.row0 + i + 8, tl.col0 + j, tl.col0 + j + 8)) out[2] += 64;
+        for (int i = 0; i < g.tm; i += 32)
+          for (int j = 0; j < tw; j += 32)
+            if (!valid(tl.row0 + i, tl.row0 + i + 32, tl.col0 + j, tl.col0 + j + std::min(32, tw - j)))
+              out[3] += 32 * std::min(32, tw - j);
+        for (int64_t r = tl.row0; r < tl.row0 + g.tm; ++r)
+          for (int64_t c = tl.col0; c < tl.col0 + tw; ++c)
+            if (r >= g.R || c >= g.C) out[4]++;
+      }
+  return BCG_OK;
+}
+
 int bcg_plan_selfcheck(const bcg_plan *plan) {
   if (!plan) return fail(BCG_EINVAL, "plan is NULL");
   const bcg::Plan &p = plan->p;
