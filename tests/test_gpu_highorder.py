@@ -142,6 +142,24 @@ def test_streamed_recursion_is_bitwise_the_register_kernel(tmp_path):
         assert np.array_equal(v7[key], v2[key]), key
 
 
+def test_streamed_recursion_variants_are_bitwise_equal(tmp_path):
+    """The streamed recursion's A/B variants (BCG_RS_TILE, csrc/recursion_stream.cu)
+    differ in lane order, buffering, producer layout and -- the default, v9 --
+    in reading 81 second-factor values per thread from tensor memory
+    (tcgen05.st / tcgen05.ld) instead of shared memory; none changes a term,
+    its order or its fma.  Default vs v7d (0) vs v8 (16), several tails per
+    CTA so the tensor-memory copy is refilled."""
+    cases = {"cfg5s": ("tag", "cfg5s"), "n60": ("shape", (60, 6, 6, 200, 2002)), "n18": ("shape", (18, 6, 6, 300, 2003))}
+    for k in ("BCG_RS_TILE",):
+        os.environ.pop(k, None)
+    v9 = _run_child(cases, {}, str(tmp_path / "v9.npz"))
+    for tile in ("0", "16"):
+        other = _run_child(cases, {"BCG_RS_TILE": tile}, str(tmp_path / f"t{tile}.npz"))
+        assert sorted(v9.files) == sorted(other.files)
+        for key in v9.files:
+            assert np.array_equal(v9[key], other[key]), (tile, key)
+
+
 def test_streamed_recursion_is_deterministic_under_load():
     """v7 releases its ring stages as soon as a unit is loaded and its
     consumer groups run ahead of each other; repeated launches on a layout
