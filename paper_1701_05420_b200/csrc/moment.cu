@@ -363,187 +363,6 @@ __global__ void __launch_bounds__(moment_threads(TM, TN)) k_moment_dmma(const __
   }
 }
 
-// ---- register-private Khatri-Rao variant (BCG_MOMENT_PRIV=1, A/B) ----
-// Every lane builds the m8n8k4 fragments it feeds to its own DMMAs straight
-// from the staged samples: fa[i] = prod_q X[s, rowcols[8 i + gid][q]] at the
-// sample of its k slot.  No factor matrices in shared memory, no fragment
-// loads, and no CTA barrier in the sample loop: warps only share the TMA ring
-// of sample chunks (full / empty mbarriers, NSTG stages), so a warp's DMMAs
-// never wait for another warp's build.  Cost: each factor value is built by
-// every warp that uses it (2x the DMULs of the shared build at 64 x 64).
-// Same products, same k order: bitwise the shared-build kernel.
-constexpr int kPrivStages = 4;
-
-__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, P1;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-
-template <int KC, int H, int R, int TM, int TN>
-__global__ void __launch_bounds__(moment_threads(TM, TN), 512 / moment_threads(TM, TN))
-    k_moment_priv(const __grid_constant__ CUtensorMap tmap, MomentArgs a) {
-  using SH = V1Shape<KC, TM, TN>;
-  constexpr int LDX = KC, MT = SH::MT, NT = SH::NT, NSTG = kPrivStages;
-  static_assert(H >= 1 && R >= 1, "compile-time mode counts");
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  const int n = a.n;
-  const int xstaged = xstaged_rows(n);
-  const int xrows = (xstaged + 7) / 8 * 8;
-  double *xs = reinterpret_cast<double *>(smem_raw);  // [NSTG][xrows][16], 128-byte swizzle
-  uint64_t *full = reinterpret_cast<uint64_t *>(xs + NSTG * xrows * LDX);
-  uint64_t *empty = full + NSTG;
-
-  const int tid = threadIdx.x;
-  const int unit = blockIdx.x;
-  const int sl_local = unit / a.ntiles;
-  const int tile_id = unit - sl_local * a.ntiles;
-  const int slice = a.slice0 + sl_local;
-  if (a.kmin_sel > 0 || a.kmax_sel < INT32_MAX) {
-    if (a.tile_kmax[tile_id] < a.kmin_sel || a.tile_kmin[tile_id] > a.kmax_sel) return;
-  }
-  const Tile tile = a.tiles[tile_id];
-  const int64_t sbeg = (int64_t)slice * a.slice_len;
-  const int64_t send = min(a.t, sbeg + a.slice_len);
-  const int nch = (int)((send - sbeg + KC - 1) / KC);
-
-  const int warp = tid >> 5, lane = tid & 31;
-  const int gid = lane >> 2, tig = lane & 3;
-  const int wm = warp % SH::WGM, wn = warp / SH::WGM;
-
-  // per-lane operand offsets: sample k = 4 s + tig of staged variable c sits
-  // at c * 16 + 2 (((k >> 1) ^ (c & 7))) + (k & 1) (128-byte swizzle); with the
-  // lane's bits folded in that is  P ^ (4 s),  P = c * 16 + ((c & 6) << 1) +
-  // 2 ((tig >> 1) ^ (c & 1)) + (tig & 1)  (bits 2, 3 of P come from c & 6 only)
-  uint32_t pa[MT][H], pb[NT][R];
-  {
-    const int t1 = tig >> 1, t0 = tig & 1;
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-      const int64_t grow = (int64_t)tile.row0 + wm * SH::WM + 8 * i + gid;
-#pragma unroll
-      for (int q = 0; q < H; ++q) {
-        const int c = grow < a.R ? a.rowcols[grow * H + q] : 0;
-        pa[i][q] = (uint32_t)(c * LDX + ((c & 6) << 1) + 2 * (t1 ^ (c & 1)) + t0);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      const int64_t gcol = (int64_t)tile.col0 + wn * SH::WN + 8 * j + gid;
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const int c = gcol < a.C ? a.colcols[gcol * R + q] : 0;
-        pb[j][q] = (uint32_t)(c * LDX + ((c & 6) << 1) + 2 * (t1 ^ (c & 1)) + t0);
-      }
-    }
-  }
-
-  if (tid == 0) {
-    for (int i = 0; i < NSTG; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], SH::NW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-
-  auto issue = [&](int c) {  // thread 0: stage chunk c
-    const int st = c % NSTG;
-    mbar_expect(&full[st], (uint32_t)(xstaged * KC * sizeof(double)));
-    double *dst = xs + st * xrows * LDX;
-    const int s0 = (int)(sbeg + (int64_t)c * KC);
-    const int bh = xbox_rows(n);
-    for (int v0 = 0; v0 < xstaged; v0 += bh) tma_load_2d(dst + v0 * LDX, &tmap, s0, v0, &full[st]);
-  };
-  int next_issue = 0;
-  if (tid == 0)
-    for (; next_issue < nch && next_issue < NSTG; ++next_issue) issue(next_issue);
-
-  double acc[MT][NT][2];
-#pragma unroll
-  for (int i = 0; i < MT; ++i)
-#pragma unroll
-    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  for (int c = 0; c < nch; ++c) {
-    const int st = c % NSTG;
-    if (tid == 0) {
-      // refill every stage all warps have released (chunk next_issue - NSTG
-      // done): a poll, except for the chunk this iteration itself needs
-      while (next_issue < nch) {
-        uint64_t *eb = &empty[next_issue % NSTG];
-        const uint32_t par = (uint32_t)((next_issue / NSTG - 1) & 1);
-        if (next_issue <= c) mbar_wait(eb, par);
-        else if (!mbar_test(eb, par)) break;
-        issue(next_issue);
-        ++next_issue;
-      }
-    }
-    mbar_wait(&full[st], (uint32_t)((c / NSTG) & 1));
-    const double *xst = xs + st * xrows * LDX;
-#pragma unroll
-    for (int s = 0; s < KC / 4; ++s) {
-      double fa[MT], fb[NT];
-#pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        double v = xst[pa[i][0] ^ (4u * s)];
-#pragma unroll
-        for (int q = 1; q < H; ++q) v *= xst[pa[i][q] ^ (4u * s)];
-        fa[i] = v;
-      }
-#pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        double v = xst[pb[j][0] ^ (4u * s)];
-#pragma unroll
-        for (int q = 1; q < R; ++q) v *= xst[pb[j][q] ^ (4u * s)];
-        fb[j] = v;
-      }
-#pragma unroll
-      for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int j = 0; j < NT; ++j) dmma884(acc[i][j], fa[i], fb[j]);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
-  }
-  // ---- epilogue: scatter to packed addresses (as k_moment_dmma) ----
-  double *dst = a.nslices == 1 ? a.out : a.ws + (int64_t)sl_local * a.S;
-  const bool accumulate = a.nslices == 1;
-#pragma unroll
-  for (int i = 0; i < MT; ++i) {
-    const int64_t row = (int64_t)tile.row0 + wm * SH::WM + 8 * i + gid;
-    if (row >= a.R) continue;
-    const int32_t kb0 = a.row_keybase[row], ro = a.row_olin[row], cs = a.row_cstart[row];
-#pragma unroll
-    for (int j = 0; j < NT; ++j) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int64_t col = (int64_t)tile.col0 + wn * SH::WN + 8 * j + 2 * tig + e;
-        if (col >= a.C || col < cs) continue;
-        const int32_t key = kb0 + a.col_rank[col];
-        if (key < a.kmin_sel || key > a.kmax_sel) continue;
-        const int64_t base = a.offs[key];
-        const int64_t addr = base + (int64_t)ro * a.col_size[col] + a.col_olin[col];
-        if (accumulate)
-          dst[addr] += acc[i][j][e];
-        else
-          dst[addr] = acc[i][j][e];
-      }
-    }
-  }
-}
-
 #if BCG_MOMENT_PART == 0
 // ---- part 0: shape-independent host code, the split-K reduce, dispatch ----
 // out[i] = ((out[i] + ws[0][i]) + ws[1][i]) + ...  for i in [lo, hi): the
@@ -647,23 +466,11 @@ static cudaError_t make_xt_map(const MomentArgs &a, CUtensorMap *map) {
 
 template <int KC, int H, int R, int TM, int TN>
 static cudaError_t go_v1(const MomentArgs &args, int grid, cudaStream_t stream) {
+  const size_t smem = moment_smem_bytes(KC, args.n, TM, TN);
+  auto kern = k_moment_dmma<KC, H, R, TM, TN>;
   CUtensorMap map;
   cudaError_t e = make_xt_map(args, &map);
   if (e != cudaSuccess) return e;
-  if constexpr (H > 0 && R > 0) {
-    static const bool priv = getenv("BCG_MOMENT_PRIV") != nullptr;  // A/B: register-private Khatri-Rao build
-    if (priv) {
-      const size_t xrows = (size_t)(xstaged_rows(args.n) + 7) / 8 * 8;
-      const size_t psmem = sizeof(double) * kPrivStages * xrows * KC + 2 * kPrivStages * sizeof(uint64_t) + 1024;
-      auto pk = k_moment_priv<KC, H, R, TM, TN>;
-      e = cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-      if (e != cudaSuccess) return e;
-      pk<<<grid, moment_threads(TM, TN), psmem, stream>>>(map, args);
-      return cudaGetLastError();
-    }
-  }
-  const size_t smem = moment_smem_bytes(KC, args.n, TM, TN);
-  auto kern = k_moment_dmma<KC, H, R, TM, TN>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, moment_threads(TM, TN), smem, stream>>>(map, args);
