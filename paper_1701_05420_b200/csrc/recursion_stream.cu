@@ -475,6 +475,8 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP, TM>
     // this warp's lanes (quadrant warp % 4) and its column range among the
     // consumer warps sharing the quadrant
     tbase = *tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(rs::tm_cols<RM>() * ((warp - G::PW) >> 2));
+    BCG_CHECK((warp < G::PW || ((tbase & 0xffffu) - (*tslot & 0xffffu)) + rs::tm_cols<RM>() <= 512u), "tensor-memory columns",
+              tbase & 0xffffu);
   }
 
   // this CTA's positions [pbeg, pend) of the work list
