@@ -30,6 +30,7 @@ def test_v7d_matches_the_ncu_histogram():
     # ncu, v7d: 157 loads x 1, 36 x 4/3, 171 x 2 wavefronts = 547 per warp and unit
     assert dict(hist) == {1.0: 157, 1.33: 36, 2.0: 171}
     assert abs(total - 547.0) < 1e-9
+    assert model.ring_wavefronts(model.V7D["reg"], model.V7D["coords"]) == 2.0   # ncu: 27 ring loads x 2
 
 
 def test_v8_lane_order_matches_ncu():
@@ -37,6 +38,7 @@ def test_v8_lane_order_matches_ncu():
     # ncu, v8: 317 loads x 1 + 47 x 2 = 411
     assert dict(hist) == {1.0: 317, 2.0: 47}
     assert abs(total - 411.0) < 1e-9
+    assert model.ring_wavefronts(model.V8["reg"], model.V8["coords"]) == 4.0    # ncu: 27 ring loads x 4
 
 
 def test_quad_rule_on_known_patterns():

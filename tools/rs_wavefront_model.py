@@ -1,15 +1,20 @@
-"""Shared-memory wavefront model of the streamed order-6 recursion (K3 v7/v8),
-calibrated on ncu's per-instruction "L1 Wavefronts Shared" of the v7d kernel
-(profiles/r02_rs_v7d_v8_v9_ncu.txt, profiles/r02_rs_wavefront_rule.txt): an LDS.64 warp instruction takes
+"""Shared-memory wavefront model of the streamed order-6 recursion (K3 v7/v8/v9),
+calibrated on ncu's per-instruction "L1 Wavefronts Shared" of the v7d and v8
+kernels (profiles/r02_rs_v7d_v8_v9_ncu.txt, profiles/r02_rs_wavefront_rule.txt).
+An LDS.64 warp instruction takes
 
-    max( bank rule: most distinct 4-byte words mapped to one of the 32 banks,
-         quad rule: over the 8 lane quads, ceil(distinct addresses in the quad / 2) )
+    bank rule over all 32 lanes                     if every lane quad reads <= 2 distinct addresses,
+    bank rule(lanes 0-15) + bank rule(lanes 16-31)  otherwise
 
-wavefronts.  The quad rule is what the measurement adds: a factor whose
+wavefronts (bank rule: the most distinct 4-byte words mapped to one of the 32
+banks).  The quad condition is what the measurement adds: a factor whose
 address depends on BOTH lane bits 0 and 1 costs 2 wavefronts even when the
-whole warp reads only 4 distinct doubles.  With it the model reproduces the
-measured histogram of the 364 factor loads exactly (157 x 1, 36 x 4/3,
-171 x 2 wavefronts; 547 per warp and unit).
+whole warp reads only 4 distinct doubles, and the two half-warps are then
+served separately, each with its own bank conflicts.  The rule reproduces,
+exactly: v7d's 364 factor loads (157 x 1, 36 x 4/3, 171 x 2 = 547 wavefronts
+per warp and unit) and its ring loads (2 each); v8's factor loads (317 x 1,
+47 x 2 = 411) and its ring loads (4 each: the sub-slab and the mode-2 low bit
+share a quad and the sub-slab stride is 0 mod 16 banks).
 
 A configuration is a register tile (digits per mode a thread holds, their
 digit stride) and a list of thread-level coordinates (mode, radix, digit
@@ -60,8 +65,29 @@ def bank_rule(addrs, width=8):
 
 
 def lds_wavefronts(addrs, width=8):
-    quad = max((len(set(addrs[i:i + 4])) + 1) // 2 for i in range(0, len(addrs), 4))
-    return max(bank_rule(addrs, width), quad)
+    quad = max(len(set(addrs[i:i + 4])) for i in range(0, len(addrs), 4))
+    if quad <= 2:
+        return bank_rule(addrs, width)
+    return bank_rule(addrs[:16], width) + (bank_rule(addrs[16:], width) if len(addrs) > 16 else 0)
+
+
+def ring_wavefronts(reg, coords):
+    """Wavefronts per ring load (a thread's M_6 elements of one unit, row-major over modes 1..5)."""
+    thr = threads_of(coords)
+    nwarps = (len(thr) + 31) // 32
+    regq = sorted(reg)
+    tot, n = 0, 0
+    for cmb in itertools.product(*[range(reg[q][0]) for q in regq]):
+        for w in range(nwarps):
+            addrs = []
+            for t in thr[32 * w: 32 * w + 32]:
+                off = 0
+                for q in range(1, 6):
+                    off += (t[q] + (reg[q][1] * cmb[regq.index(q)] if q in reg else 0)) * B ** (5 - q)
+                addrs.append(8 * off)
+            tot += lds_wavefronts(addrs)
+            n += 1
+    return tot / n
 
 
 def threads_of(coords):
@@ -142,6 +168,7 @@ if __name__ == "__main__":
     for name, cfg in (("v7d", V7D), ("v8", V8)):
         r = evaluate(cfg["reg"], cfg["coords"])
         print(f"{name}: loads/FMA {r[0]:.3f}  factor wavefronts/element {r[1]:.4f}  threads {r[2]}  tile {r[3]}"
+              f"  ring-load wavefronts {ring_wavefronts(cfg['reg'], cfg['coords']):.1f}"
               f"  store sectors/instr {store_sectors(cfg['reg'], cfg['coords']):.1f}")
     if "--search" in sys.argv:
         reg = V7D["reg"]
@@ -155,7 +182,8 @@ if __name__ == "__main__":
         for vn, cs in variants.items():
             for perm in itertools.permutations(cs):
                 r = evaluate(reg, list(perm))
-                best.append((r[1], store_sectors(reg, list(perm)), vn, perm))
+                # factor loads + the 27 ring loads, per element
+                best.append((r[1] + ring_wavefronts(reg, list(perm)) / 32.0, store_sectors(reg, list(perm)), vn, perm))
         best.sort(key=lambda x: (x[0], x[1]))
         for b in best[:25]:
             print(f"{b[0]:.4f} sectors {b[1]:.1f} {b[2]} {b[3]}")
