@@ -184,3 +184,21 @@ def test_edge_tiles_cover_the_staircase_overhang():
     _, produced = plan.output()
     assert edges.value > 0 and produced / tiled.value >= 0.90
     _native.check(lib.bcg_plan_selfcheck(plan.handle))
+
+
+def test_plan_waste_breakdown():
+    """bcg_plan_waste (tools/tile_waste.py): the valid (row, column) pairs
+    inside the tiles are exactly the produced elements, and most of the cover's
+    waste at cfg4's order 6 is whole empty 8 x 8 DMMA sub-tiles."""
+    import ctypes
+
+    lib = _native.lib()
+    plan = _native.Plan(36, 6, 3, host_only=True)
+    out = (ctypes.c_int64 * 5)()
+    _native.check(lib.bcg_plan_waste(plan.handle, out))
+    tiled, edges = ctypes.c_int64(), ctypes.c_int64()
+    _native.check(lib.bcg_plan_tiled(plan.handle, ctypes.byref(tiled), ctypes.byref(edges)))
+    _, produced = plan.output()
+    assert out[0] == tiled.value and out[1] == produced
+    assert out[3] <= out[2] <= out[0] - out[1]          # empty warp tiles within empty sub-tiles within the waste
+    assert 0.05 < out[2] / out[0] < 0.10 and out[4] <= out[0] - out[1]
