@@ -1,5 +1,5 @@
-// K3 (v7): order-6 cumulant recursion streamed by the bulk-copy engine, for
-// full blocks of even edge b (the cfg5 layout, b = 6).
+// K3 (v7 .. v9): order-6 cumulant recursion streamed by the bulk-copy engine,
+// for full blocks of edge b = 6 (the cfg5 layout).
 //
 // Same arithmetic as v2 (recursion_fact.cu, the factored form of the
 // reference's partition sum bc/cumulants.py:53-136):
@@ -27,8 +27,10 @@
 //     L2 evict-first policy, factor copies evict-last;
 //   * NGRP (4) consumer groups of 3 warps: a group loads a unit's elements from its ring
 //     stage into registers and releases the stage at once, applies the 25
-//     terms reading every factor from shared memory, and stores C_6 straight
-//     from registers to HBM (streaming stores, in place over M_6).
+//     terms reading the factors from shared memory (v9: 81 of a thread's 364
+//     factor values per unit from its tensor-memory lane instead, see "tensor
+//     memory" below), and stores C_6 straight from registers to HBM
+//     (streaming stores, in place over M_6).
 //
 // Register tile: a thread owns (b/2)^NRM elements: b/2 digits of each of
 // the NRM trailing modes, interleaved with 2 thread groups per mode
@@ -42,17 +44,20 @@
 //
 // Lane order (v8).  ncu's per-instruction wavefront counts of v7d fit one rule
 // exactly (tools/rs_wavefront_model.py, profiles/r02_rs_wavefront_rule.txt):
-// an LDS.64 takes max(bank rule, ceil(distinct addresses per lane quad / 2))
-// wavefronts -- a factor indexed by BOTH lane bits 0 and 1 costs two even when
-// the warp reads 4 distinct doubles.  v8 puts the low bit of the mode-2 digit
-// and the sub-slab in lane bits 0, 1 (0.476 factor wavefronts per element
-// instead of 0.633).  What bounds the kernel, though, is the data RETURN of
-// the loads (32 lanes x 8 B = 2 L1 cycles per LDS.64 whatever the broadcast):
-// 14.5 loads per element = 116 B per element against 128 B / clk / SM, i.e.
-// 7.9 ms at cfg5 with the L1 pipe 100% busy; only a larger register tile
-// lowers it, and at b = 6 = 2 x 3 the 27-element tile is the only one whose
-// thread count per unit is a multiple of 32 short of 81 elements (254
-// registers, measured slower).
+// an LDS.64 whose lane quads each read <= 2 distinct addresses takes the bank
+// rule over the warp, any other the sum of its two half-warps' bank rules -- a
+// factor indexed by BOTH lane bits 0 and 1 costs two wavefronts even when the
+// warp reads 4 distinct doubles.  v8 puts the low bit of the mode-2 digit and
+// the sub-slab in lane bits 0, 1 (0.476 factor wavefronts per element instead
+// of 0.633, as ncu then measured).  That changed the time by 0.3%: the
+// wavefront count is not what bounds the consumers.  What the A/Bs are
+// consistent with is the NUMBER of loads -- 14.5 per element, each returning
+// 32 x 8 B to the register file: 116 B per element against the 128 B / clk /
+// SM of the L1 return path would be 7.9 ms at cfg5 -- since moving 21% of them
+// to tensor memory (v9) is what did shorten the kernel.  Fewer loads per FMA
+// needs a larger register tile, and at b = 6 = 2 x 3 the 27-element tile is
+// the only one whose thread count per unit is a multiple of 32 short of 81
+// elements (254 registers, measured slower).
 //
 // mbarrier phases: consumers release ring stages early and run ahead of each
 // other, so a "full" barrier is indexed such that its previous phase belongs
