@@ -49,15 +49,15 @@
 // factor indexed by BOTH lane bits 0 and 1 costs two wavefronts even when the
 // warp reads 4 distinct doubles.  v8 puts the low bit of the mode-2 digit and
 // the sub-slab in lane bits 0, 1 (0.476 factor wavefronts per element instead
-// of 0.633, as ncu then measured).  That changed the time by 0.3%: the
-// wavefront count is not what bounds the consumers.  What the A/Bs are
-// consistent with is the NUMBER of loads -- 14.5 per element, each returning
-// 32 x 8 B to the register file: 116 B per element against the 128 B / clk /
-// SM of the L1 return path would be 7.9 ms at cfg5 -- since moving 21% of them
-// to tensor memory (v9) is what did shorten the kernel.  Fewer loads per FMA
-// needs a larger register tile, and at b = 6 = 2 x 3 the 27-element tile is
-// the only one whose thread count per unit is a multiple of 32 short of 81
-// elements (254 registers, measured slower).
+// of 0.633, as ncu then measured; tools/lds_rate.cu confirms on the hardware
+// that an LDS.64 costs its wavefronts, 1 cycle per SM each).  That changed the
+// time by 0.3%: shared-memory bandwidth is not what bounds the consumers (L1
+// data pipe 65% busy, FP64 pipe 37%, issue slots 40% in ncu) -- they run
+// dependent LDS -> DFMA chains at 3 warps per scheduler and 128 registers.
+// A larger register tile (fewer loads per FMA) does not fit: at b = 6 = 2 x 3
+// the 27-element tile is the only one whose thread count per unit is a
+// multiple of 32 short of 81 elements (254 registers, measured slower); a
+// fifth consumer group (15 warps) measured no faster.
 //
 // mbarrier phases: consumers release ring stages early and run ahead of each
 // other, so a "full" barrier is indexed such that its previous phase belongs
@@ -267,13 +267,13 @@ __device__ __forceinline__ void load_u_all(double *su, const RecFactArgs &a, con
 }
 
 // ---- tensor memory as a per-lane operand cache (TM = 1) ----
-// What bounds the consumers is the L1 return path (8 B x 32 lanes per
-// LDS.64).  Five terms' second factors hold no mode 1, so a thread reads the
-// same 81 doubles of V in every unit of a tail: they are copied once per tail
-// into the warp's tensor-memory lanes (tcgen05.st, 162 columns of a lane per
-// warp; 3 consumer warps share a 32-lane quadrant, 486 of 512 columns) and
-// read back with tcgen05.ld -- a datapath of its own -- instead of 81 of the
-// unit's 391 shared-memory loads.
+// Five terms' second factors hold no mode 1, so a thread reads the same 81
+// doubles of V in every unit of a tail: they are copied once per tail into
+// the warp's tensor-memory lanes (tcgen05.st, 162 columns of a lane per warp;
+// 3 consumer warps share a 32-lane quadrant, 486 of 512 columns) and read back
+// with 18 tcgen05.ld per unit instead of 81 of the unit's 391 LDS.64 (fewer
+// instructions through the LSU queue the consumers stall on; measured -1.5 to
+// -4.8%).
 __host__ __device__ constexpr bool tm_term(int T) { return T == 0 || T == 2 || T == 4 || T == 6 || T == 8; }
 template <int RM>
 __host__ __device__ constexpr int tm_vcount(int T) {
