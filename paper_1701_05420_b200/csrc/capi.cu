@@ -666,7 +666,10 @@ static int recursion_dispatch(const bcg_plan *plan, double *mk, const double *co
   a.nkeys = hi_f - lo_f;
   // whole work list: the tail-grouped order (v7 reloads its second factors
   // only when the key's modes 1..5 change); a sub-range keeps the list order
-  if (lo_f == 0 && hi_f == (int64_t)p.full_keys.size()) a.order = p.d_tail_order;
+  if (lo_f == 0 && hi_f == (int64_t)p.full_keys.size()) {
+    a.order = p.d_tail_order;
+    a.newv = p.d_tail_new;
+  }
   if (a.nkeys > 0) CUDA_TRY(bcg::launch_recursion_fact(a, m, p.b, s), "factored recursion kernel");
   auto lo_p = std::lower_bound(p.partial_keys.begin(), p.partial_keys.end(), (int32_t)k0) - p.partial_keys.begin();
   auto hi_p = std::lower_bound(p.partial_keys.begin(), p.partial_keys.end(), (int32_t)k1) - p.partial_keys.begin();

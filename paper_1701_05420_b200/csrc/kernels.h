@@ -109,6 +109,7 @@ struct RecFactArgs {
   const double *cmom[16];   // packed central moments M_k, k = 4 .. m-2
   double *mk;               // in: M_m, out: C_m
   const int32_t *order;     // v7 only: position -> work item (null: identity)
+  const int32_t *newv;      // v7 only: per position, 1 = second factors differ from the previous position's (null: compare)
 };
 int recursion_fact_terms(int m);
 bool recursion_fact_supported(int m, int b);

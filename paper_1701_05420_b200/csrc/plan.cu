@@ -560,6 +560,7 @@ static void build_fact_tables(Plan &p) {
     }
   }
   p.tail_order.clear();
+  p.tail_new.clear();
   if (m == 6) {
     p.tail_order.resize(p.full_keys.size());
     std::iota(p.tail_order.begin(), p.tail_order.end(), 0);
@@ -570,6 +571,13 @@ static void build_fact_tables(Plan &p) {
         if (a[q] != c[q]) return a[q] < c[q];
       return a[0] < c[0];
     });
+    p.tail_new.assign(p.tail_order.size(), 1);
+    for (size_t i = 1; i < p.tail_order.size(); ++i) {
+      const int64_t *a = key_of(p.tail_order[i]), *c = key_of(p.tail_order[i - 1]);
+      bool same = true;
+      for (int q = 1; q < m; ++q) same = same && a[q] == c[q];
+      p.tail_new[i] = same ? 0 : 1;
+    }
   }
 }
 
@@ -612,6 +620,7 @@ std::string upload_plan(Plan &p) {
   UP(d_full_keys, full_keys);
   UP(d_partial_keys, partial_keys);
   UP(d_tail_order, tail_order);
+  UP(d_tail_new, tail_new);
   UP(d_fill_keys, fill_keys);
 #undef UP
   if (e == cudaSuccess) e = up(&p.d_offs, p.lay[p.m].offs);
@@ -633,7 +642,7 @@ void free_plan(Plan &p) {
       if (q) cudaFree(q);
   }
   void *ptrs[] = {p.d_offs, p.d_keys32, p.d_sub_rank, p.d_part_mask, p.d_koff, p.d_term_off,
-                  p.d_full_offs, p.d_full_keys, p.d_partial_keys, p.d_fill_keys, p.d_tail_order};
+                  p.d_full_offs, p.d_full_keys, p.d_partial_keys, p.d_fill_keys, p.d_tail_order, p.d_tail_new};
   for (void *q : ptrs)
     if (q) cudaFree(q);
   for (auto &q : p.d_lower_offs)

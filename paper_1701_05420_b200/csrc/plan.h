@@ -100,6 +100,7 @@ struct Plan {
   // sorted by the key's modes 1..5 (blocks sharing them share every second
   // factor), then by mode 0
   std::vector<int32_t> tail_order;
+  std::vector<int32_t> tail_new;        // per position of tail_order: 1 = the tail differs from the previous position's
 
   // --- device copies ---
   int64_t *d_offs = nullptr;           // offs of order m
@@ -110,7 +111,7 @@ struct Plan {
   int32_t *d_term_off = nullptr;
   int64_t *d_full_offs = nullptr;
   int32_t *d_full_keys = nullptr, *d_partial_keys = nullptr;
-  int32_t *d_tail_order = nullptr;
+  int32_t *d_tail_order = nullptr, *d_tail_new = nullptr;
   int32_t *d_fill_keys = nullptr;
   int64_t *d_lower_offs[16] = {nullptr};  // offs of orders 2..m-2
 };

@@ -649,14 +649,29 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP, TM>
   int ebase = 0;  // thread's first element inside its sub-slab (row-major over modes 2..5)
 #pragma unroll
   for (int q = 2; q < 6; ++q) ebase += dig[q] * rs::ipow(B, 5 - q);
-  int64_t e = -1, s = 0, prev = -1, efill = -1;
+  int64_t e = -1, s = 0, efill = -1;
+  // Per-block information (work item -> M_6 offset, "the second factors
+  // change here") is fetched one block AHEAD: the dependent global loads
+  // (work list -> block offset, ~2 x L2 latency) held 5% of the consumers'
+  // stall samples when issued at the top of the block they are for.  With the
+  // host's per-position flags (a.newv, the tail-ordered list) a block costs
+  // three loads; without them (a sub-range in list order) the 25 factor
+  // offsets of neighbouring blocks are compared as before.
+  int64_t it_cur = pbeg < pend ? item(pbeg) : 0;
+  int64_t boff_cur = pbeg < pend ? __ldg(a.blk_off + it_cur) : 0;
+  bool newv_cur = true;
   for (int64_t pos = pbeg; pos < pend; ++pos) {
-    const int64_t it = item(pos);
-    if (prev < 0 || !same_v(it, prev)) {
+    const int64_t it = it_cur, boff = boff_cur;
+    const bool newv = newv_cur;
+    if (pos + 1 < pend) {  // issue the next block's loads now, use them next iteration
+      it_cur = item(pos + 1);
+      boff_cur = __ldg(a.blk_off + it_cur);
+      newv_cur = a.newv ? __ldg(a.newv + pos + 1) != 0 : !same_v(it_cur, it);
+    }
+    if (newv) {
       if (e >= 0 && lane == 0) rs::bar_arrive(vempty);  // done with the previous V
       ++e;
     }
-    prev = it;
     rs::bar_wait(vfull, (uint32_t)(e & 1));
     if constexpr (TM) {
       if (e != efill) {  // new tail: this thread's tail-constant second factors -> its tensor-memory lane
@@ -664,7 +679,7 @@ __global__ void __launch_bounds__(rs::Geo<B, RM, NGRP, NU, XB, LO, HINT, PP, TM>
         efill = e;
       }
     }
-    double *blk = a.mk + __ldg(a.blk_off + it);
+    double *blk = a.mk + boff;
     for (int i0 = 0; i0 < B; ++i0, ++s) {
       const int ub = (int)(s % G::NU);
       for (int p = 0; p < G::UPS; ++p) {
