@@ -202,8 +202,9 @@ def cumulants_upto_sharded(x_local, m_max: int, b: int = 2, group=None, ops=None
     t_local, n = X.shape
     sums, _, bad = ops.colstats(X)
     # one small all-reduce: column sums, row count and a non-finite flag
-    head = torch.cat([sums, torch.tensor([float(t_local), 0.0], dtype=torch.float64, device=sums.device)])
-    head[n + 1] = float(int(bad.item()) >= 0)
+    # (the flag stays on the device: no host sync before the collective)
+    head = torch.cat([sums, torch.tensor([float(t_local)], dtype=torch.float64, device=sums.device),
+                      (bad.reshape(-1)[:1] >= 0).to(device=sums.device, dtype=torch.float64)])
     dist.all_reduce(head, group=group)
     if head[n + 1].item() > 0:
         raise ValidationError(f"non-finite value in the data shard of some rank (this rank: {int(bad.item()) >= 0})")
